@@ -1,0 +1,20 @@
+# Build the sm_100a engine library in-tree (travels to the GPU box with the repo).
+NVCC ?= nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -cudart static -Iinclude
+LIB := paper_2210_15874_b200/lib/libqtn_b200.so
+SRC := paper_2210_15874_b200/csrc/qtn_b200.cu
+
+all: $(LIB)
+
+$(LIB): $(SRC) include/qtn_b200.h
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -o $@ $(SRC)
+
+sass: $(LIB)
+	cuobjdump -sass $(LIB) | grep -E "Function|LDG|STG|ATOM|RED" | head -50
+
+clean:
+	rm -f $(LIB)
+
+.PHONY: all clean sass

@@ -1,0 +1,129 @@
+"""ctypes binding of libqtn_b200.so (include/qtn_b200.h).
+
+The shared library is built in-tree by `__graft_entry__.build()` /
+`make -C paper_2210_15874_b200` into `paper_2210_15874_b200/lib/`.  There is no
+CPU fallback: if the library or a CUDA device is missing, every compute entry
+point raises `NativeUnavailable`.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libqtn_b200.so")
+
+QTN_OK = 0
+QTN_E_INVALID = -1
+QTN_E_CUDA = -2
+QTN_E_UNSUPPORTED = -3
+QTN_E_NODEVICE = -4
+QTN_C64 = 0
+QTN_C128 = 1
+QTN_FINALIZE = -1
+MAX_MEMBERS = 8
+MAX_WIDTH = 40
+ABI_VERSION = 1
+
+# every symbol include/qtn_b200.h declares
+EXPORTS = (
+    "qtn_abi_version",
+    "qtn_last_error",
+    "qtn_device_count",
+    "qtn_program_grid",
+    "qtn_program_reset",
+    "qtn_program_launch",
+    "qtn_permute",
+)
+
+BUCKET_DT = np.dtype([
+    ("out_off", "<u8"), ("w", "<i4"), ("tile_bits", "<i4"), ("mem_begin", "<i4"),
+    ("n_mem", "<i4"), ("dep_begin", "<i4"), ("n_dep", "<i4"), ("tick_begin", "<i4"),
+    ("n_tiles", "<i4"), ("slot", "<i4"), ("smem_elems", "<i4"),
+])
+MEMBER_DT = np.dtype([("off", "<u8"), ("mask", "<u8")])
+DEP_DT = np.dtype([("bucket", "<i4"), ("need", "<i4")])
+assert BUCKET_DT.itemsize == 48 and MEMBER_DT.itemsize == 16 and DEP_DT.itemsize == 8
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA library or device is missing: the B200 path cannot run."""
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code, msg):
+        self.code = code
+        super().__init__(f"qtn_b200 error {code}: {msg}")
+
+
+class ProgramC(ctypes.Structure):
+    _fields_ = [
+        ("dtype", ctypes.c_int32), ("n_buckets", ctypes.c_int32), ("n_tickets", ctypes.c_int32),
+        ("smem_bytes", ctypes.c_int32), ("grid", ctypes.c_int32), ("flags", ctypes.c_int32),
+        ("buckets", ctypes.c_void_p), ("members", ctypes.c_void_p), ("deps", ctypes.c_void_p),
+        ("tick_begin", ctypes.c_void_p), ("ctrl", ctypes.c_void_p), ("arena", ctypes.c_void_p),
+        ("results", ctypes.c_void_p), ("timing", ctypes.c_void_p),
+    ]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load the library (no device needed) and declare the signatures."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise NativeUnavailable(f"{path} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    lib.qtn_abi_version.restype = ctypes.c_int
+    lib.qtn_abi_version.argtypes = []
+    lib.qtn_last_error.restype = ctypes.c_char_p
+    lib.qtn_last_error.argtypes = []
+    lib.qtn_device_count.restype = ctypes.c_int
+    lib.qtn_device_count.argtypes = [ctypes.POINTER(ctypes.c_int)]
+    lib.qtn_program_grid.restype = ctypes.c_int
+    lib.qtn_program_grid.argtypes = [i32, i32, ctypes.POINTER(i32)]
+    lib.qtn_program_reset.restype = ctypes.c_int
+    lib.qtn_program_reset.argtypes = [ctypes.POINTER(ProgramC), vp]
+    lib.qtn_program_launch.restype = ctypes.c_int
+    lib.qtn_program_launch.argtypes = [ctypes.POINTER(ProgramC), vp]
+    lib.qtn_permute.restype = ctypes.c_int
+    lib.qtn_permute.argtypes = [i32, vp, i64, i32, vp, i32, ctypes.POINTER(i64), vp]
+    if lib.qtn_abi_version() != ABI_VERSION:
+        raise NativeUnavailable(f"ABI mismatch: library {lib.qtn_abi_version()} != {ABI_VERSION}")
+    _lib = lib
+    return lib
+
+
+def check(rc: int):
+    if rc != QTN_OK:
+        raise NativeError(rc, _lib.qtn_last_error().decode(errors="replace"))
+
+
+def require_device():
+    """Fail loudly (no CPU fallback) when no CUDA device is usable."""
+    lib = load()
+    import torch
+    n = ctypes.c_int(0)
+    lib.qtn_device_count(ctypes.byref(n))
+    if n.value < 1 or not torch.cuda.is_available():
+        raise NativeUnavailable("no CUDA device: the B200 backend has no CPU fallback")
+    return lib
+
+
+def program_grid(dtype_code: int, smem_bytes: int) -> int:
+    lib = require_device()
+    g = ctypes.c_int32(0)
+    check(lib.qtn_program_grid(dtype_code, smem_bytes, ctypes.byref(g)))
+    return g.value
+
+
+def permute(src_dtype, src_ptr, src_offset, dst_dtype, dst_ptr, rank, strides, stream):
+    lib = require_device()
+    arr = (ctypes.c_int64 * max(1, rank))(*[int(s) for s in strides])
+    check(lib.qtn_permute(src_dtype, ctypes.c_void_p(src_ptr), int(src_offset), dst_dtype,
+                          ctypes.c_void_p(dst_ptr), int(rank), arr, ctypes.c_void_p(stream)))

@@ -1,0 +1,187 @@
+"""Work units, sharding and the energy all-reduce.
+
+The reference parallelises the energy over lightcones with a thread pool
+(src/tn_build.py:176-186) and sums (1 - <ZZ>)/2 in sorted-edge order
+(src/tn_build.py:199).  Here:
+
+  * every cone is planned on the host; a cone wider than the slice target is
+    expanded into 2^s slice units (suggest_slicing, src/ordering.py:192-230);
+  * units are costed by algorithmic bytes and assigned to
+    ranks with LPT (largest first, to the least-loaded rank, ties to the
+    lowest rank) — deterministic, no data-path communication;
+  * each rank runs its units as batched device programs (one persistent
+    launch per batch) and writes each unit's complex value into its slot of
+    a zero-filled float64 vector;
+  * one all-reduce (NCCL over NVLink on GPUs, gloo on CPU) sums the slot
+    vector.  Every slot has exactly one non-zero contributor, so the sum is
+    exact and the per-cone totals (summed on the host in slice order) are
+    bitwise identical for any number of ranks.
+"""
+from __future__ import annotations
+
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import engine as E
+from .tensor_core import Backend, BucketStats, memory_estimate
+
+
+@dataclass
+class Unit:
+    cone: int
+    assignment: dict
+    cost: int
+
+
+@dataclass
+class UnitPlan:
+    cones: list
+    templates: list
+    raws: list
+    units: list
+    widths: list = field(default_factory=list)
+
+
+def plan_units(cones, backend: Backend, heuristic="minfill", mem_cap=4 << 30, slice_target=None, n_workers=1):
+    """Order every cone, slice the wide ones, build templates and units."""
+    from .ordering import MemoryCapError, dry_run, greedy_order, suggest_slicing
+
+    def one(lc):
+        tn = lc.network
+        order = greedy_order(tn, heuristic)
+        width = dry_run(tn, order).contraction_width
+        sliced = []
+        if slice_target is not None and width > slice_target:
+            sliced = suggest_slicing(tn, order, slice_target)
+        tmpl = E.plan_template([t.indices for t in tn.tensors], order, backend.dtype, fixed=sliced)
+        if memory_estimate(tmpl.max_width, backend.dtype) > mem_cap:
+            raise MemoryCapError(tmpl.max_width, memory_estimate(tmpl.max_width, backend.dtype), mem_cap)
+        raw = np.concatenate([np.asarray(t.data, np.complex128).ravel() for t in tn.tensors])
+        return tmpl, sliced, raw
+
+    if n_workers > 1:
+        with ThreadPoolExecutor(max_workers=n_workers) as pool:
+            res = list(pool.map(one, cones))
+    else:
+        res = [one(lc) for lc in cones]
+    units = []
+    templates, raws = [], []
+    for ci, (tmpl, sliced, raw) in enumerate(res):
+        templates.append(tmpl)
+        raws.append(raw)
+        cost = E.algorithmic_bytes(tmpl, backend.dtype)
+        for bits in np.ndindex(*(2,) * len(sliced)):
+            units.append(Unit(ci, dict(zip(sliced, (int(b) for b in bits))), cost))
+    return UnitPlan(list(cones), templates, raws, units)
+
+
+def lpt_assign(costs, n_ranks):
+    """Largest-processing-time-first assignment; returns rank per unit."""
+    owner = [0] * len(costs)
+    load = [0] * n_ranks
+    for u in sorted(range(len(costs)), key=lambda i: (-costs[i], i)):
+        r = min(range(n_ranks), key=lambda k: (load[k], k))
+        owner[u] = r
+        load[r] += costs[u]
+    return owner
+
+
+def _batches(units, plan, backend, budget_bytes):
+    """Greedy batching of units into programs under an HBM budget."""
+    esz = backend.elem_bytes
+    cur, cur_b = [], 0
+    for ui in units:
+        t = plan.templates[plan.units[ui].cone]
+        b = (t.n_in_elems + t.n_inter_elems) * esz + 4096
+        if cur and cur_b + b > budget_bytes:
+            yield cur
+            cur, cur_b = [], 0
+        cur.append(ui)
+        cur_b += b
+    if cur:
+        yield cur
+
+
+def run_local(plan: UnitPlan, mine, backend: Backend, device: int, budget_bytes=None):
+    """Execute units `mine` on one device; returns {unit: complex}, {cone: stats}."""
+    import torch
+    if budget_bytes is None:
+        free, _ = torch.cuda.mem_get_info(device)
+        budget_bytes = int(0.6 * free)
+    be = Backend(backend.kind, backend.threshold, backend.dtype, device, backend.profile)
+    vals, stats = {}, {}
+    for batch in _batches(mine, plan, be, budget_bytes):
+        insts = [E.Instance(plan.templates[plan.units[u].cone], plan.units[u].assignment) for u in batch]
+        prog = E.Program(insts, be.dtype)
+        ex = E.Executor(prog, device=device, timing=be.profile)
+        res = ex.run([plan.raws[plan.units[u].cone] for u in batch])
+        if be.profile:
+            t0, t1 = ex.fetch_timing()
+        for k, u in enumerate(batch):
+            vals[u] = complex(res[k])
+            ci = plan.units[u].cone
+            tm = plan.templates[ci]
+            if be.profile:
+                g = prog.bucket_gid[k]
+                el = np.maximum(t1[g] - t0[g], 0)
+            else:
+                el = np.zeros(len(tm.w), np.int64)
+            stats.setdefault(ci, []).extend(
+                BucketStats(int(w), int(e), be.route(int(w))) for w, e in zip(tm.w, el))
+    return vals, stats
+
+
+def _combine(plan, slot_vec):
+    n_cones = len(plan.cones)
+    values = [0j] * n_cones
+    for u, unit in enumerate(plan.units):   # units are in (cone, ndindex) order
+        values[unit.cone] += complex(slot_vec[2 * u], slot_vec[2 * u + 1])
+    return values
+
+
+def run_units(plan: UnitPlan, backend: Backend, group=None, n_gpus=None):
+    """Run all units; returns (per-cone complex values, per-cone stats)."""
+    import torch
+    import torch.distributed as dist
+    costs = [u.cost for u in plan.units]
+    n_units = len(plan.units)
+    if group is not None or (dist.is_available() and dist.is_initialized()):
+        rank = dist.get_rank(group)
+        world = dist.get_world_size(group)
+        owner = lpt_assign(costs, world)
+        mine = [u for u in range(n_units) if owner[u] == rank]
+        dev = torch.cuda.current_device() if torch.cuda.is_available() else backend.device
+        vals, stats = run_local(plan, mine, backend, dev) if mine else ({}, {})
+        slots = np.zeros(2 * n_units, np.float64)
+        for u, v in vals.items():
+            slots[2 * u], slots[2 * u + 1] = v.real, v.imag
+        on_gpu = dist.get_backend(group) == "nccl"
+        t = torch.from_numpy(slots).to("cuda" if on_gpu else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        slots = t.cpu().numpy()
+        st = [stats.get(ci, []) for ci in range(len(plan.cones))]
+        return _combine(plan, slots), st
+    ng = n_gpus or 1
+    owner = lpt_assign(costs, ng)
+    results = [None] * ng
+
+    def work(r):
+        mine = [u for u in range(n_units) if owner[u] == r]
+        with torch.cuda.device(r):
+            results[r] = run_local(plan, mine, backend, r) if mine else ({}, {})
+
+    if ng > 1:
+        with ThreadPoolExecutor(max_workers=ng) as pool:
+            list(pool.map(work, range(ng)))
+    else:
+        results[0] = run_local(plan, list(range(n_units)), backend, backend.device)
+    slots = np.zeros(2 * n_units, np.float64)
+    stats = {}
+    for vals, st in results:
+        for u, v in vals.items():
+            slots[2 * u], slots[2 * u + 1] = v.real, v.imag
+        for ci, s in st.items():
+            stats.setdefault(ci, []).extend(s)
+    return _combine(plan, slots), [stats.get(ci, []) for ci in range(len(plan.cones))]

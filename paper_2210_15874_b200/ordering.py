@@ -1,0 +1,342 @@
+"""Elimination ordering, symbolic dry runs, device bucket elimination and
+index slicing (reference: src/ordering.py).
+
+`greedy_order`, `dry_run` and `suggest_slicing` are host planning (the
+reference's heap discipline and tie-breaks are kept, so orders and widths are
+identical).  `contract_network` / `contract_sliced` freeze the bucket lists
+into a device program (engine.py) and run it with one persistent-kernel launch
+per batch; the get-result scalar is the program's finaliser slot.
+"""
+from __future__ import annotations
+
+import heapq
+import threading
+from collections import OrderedDict
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import engine as E
+from .tensor_core import Backend, BucketStats, DeviceTensor, Tensor, memory_estimate
+from .tn_build import TensorNetwork
+
+DEFAULT_MEM_CAP = 4 << 30     # src/ordering.py:13
+HEURISTICS = ("minfill", "mindegree")
+
+
+class MemoryCapError(Exception):
+    """Raised before any allocation when the widest bucket would exceed the
+    cap (src/ordering.py:18-23)."""
+
+    def __init__(self, width: int, needed: int, cap: int):
+        self.width = width
+        self.needed = needed
+        self.cap = cap
+        super().__init__(f"memory cap exceeded: width {width} needs {needed} bytes")
+
+
+def line_graph(tn: TensorNetwork) -> dict:
+    """Index adjacency: two indices are adjacent iff some tensor holds both
+    (src/ordering.py:26-36)."""
+    adj = {}
+    for t in tn.tensors:
+        ids = t.indices
+        for a in ids:
+            s = adj.setdefault(a, set())
+            s.update(ids)
+            s.discard(a)
+    return adj
+
+
+def _missing_fill(adj, v) -> int:
+    """Number of absent edges among v's neighbours (src/ordering.py:39-47)."""
+    nb = list(adj[v])
+    miss = 0
+    for i, a in enumerate(nb):
+        na = adj[a]
+        for b in nb[i + 1:]:
+            if b not in na:
+                miss += 1
+    return miss
+
+
+def greedy_order(tn: TensorNetwork, heuristic: str = "minfill") -> list:
+    """Greedy min-fill / min-degree elimination order (src/ordering.py:50-94).
+
+    A (score, id) min-heap with lazy invalidation: eliminating v turns its
+    live/open neighbours into a clique; only vertices whose score changed are
+    re-pushed, so ties always break toward the smallest index id."""
+    if heuristic not in HEURISTICS:
+        raise ValueError(f"unknown heuristic {heuristic!r}")
+    adj = line_graph(tn)
+    opened = set(tn.open_indices)
+    live = set(adj) - opened
+    use_fill = heuristic == "minfill"
+    score = (lambda v: _missing_fill(adj, v)) if use_fill else (lambda v: len(adj[v]))
+    cur = {v: score(v) for v in live}
+    heap = [(s, v) for v, s in cur.items()]
+    heapq.heapify(heap)
+    out = []
+    while live:
+        s, v = heapq.heappop(heap)
+        if v not in live or cur[v] != s:
+            continue
+        out.append(v)
+        live.discard(v)
+        nbrs = [x for x in adj[v] if x in live or x in opened]
+        for x in adj[v]:
+            adj[x].discard(v)
+        del adj[v]
+        for i, a in enumerate(nbrs):
+            sa = adj[a]
+            for b in nbrs[i + 1:]:
+                if b not in sa:
+                    sa.add(b)
+                    adj[b].add(a)
+        touched = set(nbrs)
+        if use_fill:
+            for x in nbrs:
+                touched |= adj[x]
+        for x in touched:
+            if x in live:
+                s2 = score(x)
+                if s2 != cur[x]:
+                    cur[x] = s2
+                    heapq.heappush(heap, (s2, x))
+    return out
+
+
+@dataclass(frozen=True)
+class WidthProfile:
+    per_bucket_widths: tuple
+    bucket_indices: tuple
+
+    @property
+    def contraction_width(self) -> int:
+        return max(self.per_bucket_widths, default=0)
+
+
+def _replay(index_sets, active, target_step=None):
+    """Symbolic bucket replay (src/ordering.py:104-145,212-230).  Returns the
+    widths, or the union of bucket `target_step` (before removing its index)."""
+    pos = {x: k for k, x in enumerate(active)}
+    buckets = {x: [] for x in active}
+    for s in index_sets:
+        closed = [i for i in s if i in pos]
+        if closed:
+            buckets[min(closed, key=pos.__getitem__)].append(s)
+    widths = []
+    for step, x in enumerate(active):
+        union = set()
+        for s in buckets[x]:
+            union |= s
+        if step == target_step:
+            return union
+        union.discard(x)
+        widths.append(len(union))
+        closed = [i for i in union if i in pos]
+        if closed:
+            buckets[min(closed, key=pos.__getitem__)].append(frozenset(union))
+    if target_step is not None:
+        raise AssertionError("target step beyond profile length")
+    return widths
+
+
+def dry_run(tn: TensorNetwork, order, fixed=()) -> WidthProfile:
+    """Widths of every bucket without numeric work (src/ordering.py:119-145).
+    `fixed` indices are sliced out."""
+    fixed = set(fixed)
+    active = [i for i in order if i not in fixed]
+    missing = tn.all_indices() - set(order) - set(tn.open_indices) - fixed
+    if missing:
+        raise ValueError(f"order is missing indices: {sorted(missing)}")
+    sets = [frozenset(t.indices) - fixed for t in tn.tensors]
+    return WidthProfile(tuple(_replay(sets, active)), tuple(active))
+
+
+def suggest_slicing(tn: TensorNetwork, order, target_width: int) -> list:
+    """Greedy slicing: while the profile is wider than the target, slice the
+    smallest not-yet-sliced id of the widest bucket's union (src/ordering.py:192-230)."""
+    if target_width < 1:
+        raise ValueError("target_width must be >= 1")
+    sliced = []
+    while True:
+        prof = dry_run(tn, order, fixed=sliced)
+        if prof.contraction_width <= target_width:
+            return sliced
+        step = int(np.argmax(prof.per_bucket_widths))
+        fixed = set(sliced)
+        sets = [frozenset(t.indices) - fixed for t in tn.tensors]
+        union = _replay(sets, list(prof.bucket_indices), target_step=step)
+        cands = sorted(i for i in union if i not in fixed) or [prof.bucket_indices[step]]
+        sliced.append(cands[0])
+
+
+def slice_network(tn: TensorNetwork, assignment: dict) -> TensorNetwork:
+    """Fix indices to constants, removing them from the tensors (src/ordering.py:233-248)."""
+    out = []
+    for t in tn.tensors:
+        hit = [i for i in t.indices if i in assignment]
+        if not hit:
+            out.append(t)
+            continue
+        d = np.asarray(t.data)
+        kept = list(t.indices)
+        for i in hit:
+            ax = kept.index(i)
+            d = np.take(d, assignment[i], axis=ax)
+            kept.pop(ax)
+        out.append(Tensor(tuple(kept), d))
+    return TensorNetwork(out, tn.open_indices)
+
+
+# ---------------------------------------------------------------------------
+# device execution
+# ---------------------------------------------------------------------------
+class _PlanCache:
+    """LRU of (structure, order, fixed, dtype, device) -> (Template, Executor, lock).
+    The symbolic plan depends only on index structure, never on values."""
+
+    def __init__(self, cap=32):
+        self.cap = cap
+        self.d = OrderedDict()
+        self.lock = threading.Lock()
+
+    def get(self, key):
+        with self.lock:
+            v = self.d.get(key)
+            if v is not None:
+                self.d.move_to_end(key)
+            return v
+
+    def put(self, key, val):
+        with self.lock:
+            self.d[key] = val
+            self.d.move_to_end(key)
+            while len(self.d) > self.cap:
+                self.d.popitem(last=False)
+
+    def clear(self):
+        with self.lock:
+            self.d.clear()
+
+
+PLAN_CACHE = _PlanCache()
+
+
+def _raw_inputs(tn: TensorNetwork) -> np.ndarray:
+    parts = [np.asarray(t.data, dtype=np.complex128).ravel() for t in tn.tensors]
+    return np.concatenate(parts) if parts else np.zeros(0, np.complex128)
+
+
+def _template(tn, order, backend, fixed=()):
+    key = ("tmpl", tuple(t.indices for t in tn.tensors), tuple(order), tuple(fixed), backend.dtype)
+    hit = PLAN_CACHE.get(key)
+    if hit is None:
+        hit = E.plan_template([t.indices for t in tn.tensors], order, backend.dtype, fixed)
+        PLAN_CACHE.put(key, hit)
+    return key, hit
+
+
+def _check_cap(tmpl, backend, mem_cap):
+    worst = tmpl.max_width
+    need = memory_estimate(worst, backend.dtype)
+    if need > mem_cap:
+        raise MemoryCapError(worst, need, mem_cap)
+
+
+def _executor(key, progfn, backend, n_inst):
+    ekey = ("exec", key, n_inst, backend.device, backend.profile)
+    hit = PLAN_CACHE.get(ekey)
+    if hit is None:
+        ex = E.Executor(progfn(), device=backend.device, timing=backend.profile)
+        hit = (ex, threading.Lock())
+        PLAN_CACHE.put(ekey, hit)
+    return hit
+
+
+def _stats(tmpl, ex, backend, inst=0):
+    if backend.profile:
+        t0, t1 = ex.fetch_timing()
+        gids = ex.prog.bucket_gid[inst]
+        el = np.maximum(t1[gids] - t0[gids], 0)
+    else:
+        el = np.zeros(len(tmpl.w), np.int64)
+    return [BucketStats(width=int(w), elapsed_ns=int(e), backend_used=backend.route(int(w)))
+            for w, e in zip(tmpl.w, el)]
+
+
+def contract_network(tn: TensorNetwork, order, backend: Backend = None, mem_cap: int = DEFAULT_MEM_CAP):
+    """Full bucket elimination on the B200; returns (scalar, [BucketStats])
+    (src/ordering.py:148-189).
+
+    The network must be closed; a dry-run memory pre-check raises
+    MemoryCapError before any device allocation.  Stats are one per non-empty
+    bucket in elimination order (width == dry-run width)."""
+    backend = backend or Backend()
+    if tn.open_indices:
+        raise ValueError("contract_network requires a closed network")
+    missing = tn.all_indices() - set(order)
+    if missing:
+        raise ValueError(f"order is missing indices: {sorted(missing)}")
+    key, tmpl = _template(tn, order, backend)
+    _check_cap(tmpl, backend, mem_cap)
+    ex, lock = _executor(key, lambda: E.Program([E.Instance(tmpl)], backend.dtype), backend, 1)
+    raw = _raw_inputs(tn)
+    with lock:
+        vals = ex.run([raw])
+        stats = _stats(tmpl, ex, backend)
+    return complex(vals[0]), stats
+
+
+def get_result_data(tn: TensorNetwork, order, backend: Backend = None, mem_cap: int = DEFAULT_MEM_CAP):
+    """BASELINE.json vocabulary: the get-result scalar of contract_network."""
+    return contract_network(tn, order, backend, mem_cap)[0]
+
+
+def _instances_per_launch(tmpl, backend, n_total):
+    import torch
+    free, _ = torch.cuda.mem_get_info(backend.device)
+    per = (tmpl.n_in_elems + tmpl.n_inter_elems) * backend.elem_bytes + 4096
+    fit = max(1, int(0.6 * free) // max(per, 1))
+    return int(min(n_total, fit, 4096))
+
+
+def contract_sliced(tn: TensorNetwork, order, sliced, backend: Backend = None, mem_cap: int = DEFAULT_MEM_CAP):
+    """Sum of the network's value over every assignment of the sliced indices
+    (src/ordering.py:251-267).  The slices share one plan; each is a program
+    instance whose inputs are gathered at a base-pointer offset (no
+    np.take), batched as many per launch as HBM allows, summed in
+    np.ndindex order."""
+    backend = backend or Backend()
+    sliced = [int(s) for s in sliced]
+    if tn.open_indices:
+        raise ValueError("contract_network requires a closed network")
+    sub_order = [i for i in order if i not in sliced]
+    missing = tn.all_indices() - set(sliced) - set(sub_order)
+    if missing:
+        raise ValueError(f"order is missing indices: {sorted(missing)}")
+    key, tmpl = _template(tn, order, backend, fixed=tuple(sliced))
+    _check_cap(tmpl, backend, mem_cap)
+    n = 1 << len(sliced)
+    assigns = [dict(zip(sliced, bits)) for bits in np.ndindex(*(2,) * len(sliced))] if sliced else [{}]
+    per = _instances_per_launch(tmpl, backend, n)
+    raw = _raw_inputs(tn)
+    vals = []
+    for start in range(0, n, per):
+        chunk = assigns[start:start + per]
+        prog = E.Program([E.Instance(tmpl, a) for a in chunk], backend.dtype)
+        ex = E.Executor(prog, device=backend.device, timing=False)
+        vals.extend(ex.run([raw] * len(chunk)))
+    total = 0.0 + 0.0j
+    for v in vals:
+        total += complex(v)
+    return total
+
+
+def write_width_profile_csv(path, profile: WidthProfile):
+    """step,bucket_index,width (src/ordering.py:270-276)."""
+    with open(path, "w") as f:
+        f.write("step,bucket_index,width\n")
+        for step, (idx, w) in enumerate(zip(profile.bucket_indices, profile.per_bucket_widths)):
+            f.write(f"{step},{idx},{w}\n")

@@ -1,0 +1,344 @@
+"""Tensors, buckets, backend policy and the process-bucket call on B200.
+
+Mirrors the reference's L0 (src/tensor_core.py): `Tensor`, `Bucket`,
+`BucketStats`, `Backend`, `memory_estimate`, `permute`, `contract_bucket`.
+The CPU kernels (`reference_kernel`, `fast_kernel`) are replaced by the
+sm_100a program kernel; there is no CPU fallback — a missing library or
+device raises `NativeUnavailable`.
+
+Host tensors (`Tensor`) are exactly the reference's: immutable complex128
+numpy arrays of shape (2,)*rank, C order, last listed index fastest.
+`DeviceTensor` is the same contract with the data resident in HBM (torch
+storage); `.data` copies it back lazily.
+"""
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from . import engine as E
+
+B200 = "b200"
+DEFAULT_MIXED_THRESHOLD = 11   # src/tensor_core.py:17 (small/large split)
+KINDS = (B200,)
+
+
+@dataclass(frozen=True)
+class Backend:
+    """Kernel policy.  `kind` is always "b200".
+
+    threshold: buckets with result width <= threshold are reported as the
+      small-bucket schedule ("b200-small"), wider ones as the fused large-bucket
+      path ("b200-large") — the B200 analogue of the reference's Mixed routing
+      (src/tensor_core.py:176-184); both run inside the same persistent launch.
+    dtype: "complex64" or "complex128" (the reference is complex128 only).
+    device: CUDA device ordinal.
+    profile: record per-bucket device time (BucketStats.elapsed_ns).
+    """
+
+    kind: str = B200
+    threshold: int = DEFAULT_MIXED_THRESHOLD
+    dtype: str = "complex128"
+    device: int = 0
+    profile: bool = True
+
+    def __post_init__(self):
+        if self.kind not in KINDS:
+            raise ValueError(f"unknown backend kind: {self.kind!r}")
+        if self.threshold < 0:
+            raise ValueError("mixed threshold must be >= 0")
+        object.__setattr__(self, "dtype", E.norm_dtype(self.dtype))
+
+    @classmethod
+    def b200(cls, dtype="complex128", threshold=DEFAULT_MIXED_THRESHOLD, device=0, profile=True):
+        return cls(B200, threshold, dtype, device, profile)
+
+    # drop-in aliases for code written against the reference's constructors
+    @classmethod
+    def fast(cls) -> "Backend":
+        return cls(B200)
+
+    @classmethod
+    def reference(cls) -> "Backend":
+        return cls(B200)
+
+    @classmethod
+    def mixed(cls, threshold: int = DEFAULT_MIXED_THRESHOLD) -> "Backend":
+        return cls(B200, threshold)
+
+    def route(self, width: int) -> str:
+        return "b200-large" if width > self.threshold else "b200-small"
+
+    @property
+    def elem_bytes(self) -> int:
+        return E.ELEM_BYTES[self.dtype]
+
+
+class Tensor:
+    """Immutable dense host tensor over binary indices (src/tensor_core.py:46-74)."""
+
+    __slots__ = ("indices", "data")
+
+    def __init__(self, indices, data):
+        indices = tuple(int(i) for i in indices)
+        if len(set(indices)) != len(indices):
+            raise ValueError("duplicate index id in tensor")
+        data = np.asarray(data, dtype=np.complex128)
+        if data.shape != (2,) * len(indices):
+            data = data.reshape((2,) * len(indices))
+        data.setflags(write=False)
+        object.__setattr__(self, "indices", indices)
+        object.__setattr__(self, "data", data)
+
+    def __setattr__(self, *a):
+        raise AttributeError("Tensor is immutable")
+
+    @property
+    def rank(self) -> int:
+        return len(self.indices)
+
+    def __repr__(self):
+        return f"Tensor(indices={self.indices}, rank={self.rank})"
+
+
+class DeviceTensor:
+    """Tensor resident in HBM: a flat torch complex tensor of 2^rank elements,
+    C order over `indices`.  `.data` returns a host numpy copy (complex128,
+    shape (2,)*rank) so code written against `Tensor` keeps working."""
+
+    __slots__ = ("indices", "storage", "_host")
+
+    def __init__(self, indices, storage):
+        indices = tuple(int(i) for i in indices)
+        if len(set(indices)) != len(indices):
+            raise ValueError("duplicate index id in tensor")
+        if storage.numel() != 1 << len(indices):
+            raise ValueError("storage size does not match rank")
+        object.__setattr__(self, "indices", indices)
+        object.__setattr__(self, "storage", storage)
+        object.__setattr__(self, "_host", None)
+
+    def __setattr__(self, *a):
+        raise AttributeError("DeviceTensor is immutable")
+
+    @property
+    def rank(self) -> int:
+        return len(self.indices)
+
+    @property
+    def dtype(self) -> str:
+        return E.norm_dtype(self.storage.dtype)
+
+    @property
+    def data(self) -> np.ndarray:
+        if self._host is None:
+            h = self.storage.detach().cpu().numpy().astype(np.complex128).reshape((2,) * self.rank)
+            h.setflags(write=False)
+            object.__setattr__(self, "_host", h)
+        return self._host
+
+    def to_host(self) -> Tensor:
+        return Tensor(self.indices, self.data)
+
+    @classmethod
+    def from_host(cls, t, dtype="complex128", device=0):
+        import torch
+        dt = torch.complex64 if E.norm_dtype(dtype) == "complex64" else torch.complex128
+        arr = np.array(np.asarray(t.data).ravel(), dtype=np.complex128)  # writable copy
+        return cls(t.indices, torch.from_numpy(arr).to(device=f"cuda:{device}", dtype=dt))
+
+    def __repr__(self):
+        return f"DeviceTensor(indices={self.indices}, rank={self.rank}, dtype={self.dtype})"
+
+
+@dataclass(frozen=True)
+class Bucket:
+    """All tensors sharing `bucket_index` (src/tensor_core.py:77-90)."""
+
+    bucket_index: int
+    tensors: tuple
+
+    def __post_init__(self):
+        object.__setattr__(self, "tensors", tuple(self.tensors))
+        for t in self.tensors:
+            if self.bucket_index not in t.indices:
+                raise ValueError(f"tensor {t!r} does not contain bucket index {self.bucket_index}")
+
+
+@dataclass(frozen=True)
+class BucketStats:
+    """width = result rank; elapsed_ns = device time of the bucket (first tile
+    start -> last tile end, %globaltimer) or 0 when profiling is off;
+    backend_used = "b200-small" / "b200-large" (src/tensor_core.py:93-97)."""
+
+    width: int
+    elapsed_ns: int
+    backend_used: str
+
+
+def memory_estimate(width: int, dtype: str = "complex128") -> int:
+    """Bytes of one rank-`width` tensor (src/tensor_core.py:100-104; dtype-aware)."""
+    if width < 0:
+        raise ValueError("width must be >= 0")
+    return E.ELEM_BYTES[E.norm_dtype(dtype)] * (1 << width)
+
+
+def permute(t, new_order):
+    """Reorder tensor indices keeping element values (src/tensor_core.py:107-114).
+    Host tensors are permuted with numpy; device tensors with qtn_permute."""
+    new_order = tuple(int(i) for i in new_order)
+    if sorted(new_order) != sorted(t.indices) or len(new_order) != t.rank:
+        raise ValueError("new_order is not a permutation of the tensor's indices")
+    if isinstance(t, DeviceTensor):
+        return _device_permute(t, new_order, t.dtype)
+    src = {idx: ax for ax, idx in enumerate(t.indices)}
+    return Tensor(new_order, np.transpose(t.data, tuple(src[i] for i in new_order)))
+
+
+def _result_indices(b: Bucket) -> tuple:
+    u = set()
+    for t in b.tensors:
+        u.update(t.indices)
+    u.discard(b.bucket_index)
+    return tuple(sorted(u))
+
+
+def _device_permute(t: DeviceTensor, new_order, dtype) -> DeviceTensor:
+    """Device copy of `t` with axes `new_order` and element type `dtype`."""
+    import torch
+    dtype = E.norm_dtype(dtype)
+    if tuple(new_order) == t.indices and t.dtype == dtype:
+        return t
+    r = t.rank
+    srcpos = {idx: ax for ax, idx in enumerate(t.indices)}
+    # dst bit j (j = 0 fastest) is axis new_order[r-1-j]
+    strides = [1 << (r - 1 - srcpos[new_order[r - 1 - j]]) for j in range(r)]
+    tdt = torch.complex64 if dtype == "complex64" else torch.complex128
+    out = torch.empty(1 << r, dtype=tdt, device=t.storage.device)
+    stream = torch.cuda.current_stream(t.storage.device).cuda_stream
+    N.permute(E.DTYPE_CODE[t.dtype], t.storage.data_ptr(), 0, E.DTYPE_CODE[dtype], out.data_ptr(),
+              r, strides, stream)
+    return DeviceTensor(new_order, out)
+
+
+class _BucketLauncher:
+    """Single-bucket program (no arena: member and result offsets are absolute
+    device addresses / element size)."""
+
+    _grid = {}
+
+    @classmethod
+    def run(cls, members, masks, out, w, dtype):
+        import torch
+        dev = out.device
+        esz = E.ELEM_BYTES[dtype]
+        lmax = E.TILE_BITS[dtype]
+        L = min(w, lmax)
+        while True:
+            low = (1 << L) - 1
+            st = sum(2 << bin(m & low).count("1") for m in masks if (m & low) != low)
+            if st * esz <= E.SMEM_BUDGET or L == 0:
+                break
+            L -= 1
+        B = np.zeros(1, N.BUCKET_DT)
+        B["out_off"] = out.data_ptr() // esz
+        B["w"] = w
+        B["tile_bits"] = L
+        B["n_mem"] = len(members)
+        B["n_tiles"] = 1 << (w - L)
+        B["slot"] = -1
+        B["smem_elems"] = st
+        M = np.zeros(len(members), N.MEMBER_DT)
+        for k, (m, msk) in enumerate(zip(members, masks)):
+            M[k] = (m.data_ptr() // esz, msk)
+        blob = np.zeros(48 + 16 * N.MAX_MEMBERS + 16 + 16, np.uint8)
+        blob[0:48] = np.frombuffer(B.tobytes(), np.uint8)
+        blob[48:48 + M.nbytes] = np.frombuffer(M.tobytes(), np.uint8)
+        tb_off = 48 + 16 * N.MAX_MEMBERS          # tick_begin[0] = 0, then ctrl[3] = 0
+        dtab = torch.from_numpy(blob).to(dev)
+        base = dtab.data_ptr()
+        key = (dtype, st * esz, dev.index)
+        if key not in cls._grid:
+            cls._grid[key] = N.program_grid(E.DTYPE_CODE[dtype], _smem_bytes(st * esz))
+        c = N.ProgramC()
+        c.dtype = E.DTYPE_CODE[dtype]
+        c.n_buckets = 1
+        c.n_tickets = 1 << (w - L)
+        c.smem_bytes = _smem_bytes(st * esz)
+        c.grid = min(cls._grid[key], c.n_tickets)
+        c.buckets = base
+        c.members = base + 48
+        c.deps = base + 48
+        c.tick_begin = base + tb_off
+        c.ctrl = base + tb_off + 4
+        c.arena = None
+        c.results = None
+        c.timing = None
+        stream = torch.cuda.current_stream(dev)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        N.check(N.load().qtn_program_launch(ctypes.byref(c), ctypes.c_void_p(stream.cuda_stream)))
+        ev1.record(stream)
+        # keep the table alive until the launch has consumed it
+        ev1.synchronize()
+        del dtab
+        return int(ev0.elapsed_time(ev1) * 1e6)
+
+
+def _smem_bytes(n):
+    return (n + 15) // 16 * 16
+
+
+def contract_bucket(b: Bucket, backend: Backend = None):
+    """Process-bucket: sum `bucket_index` out of the product of the members
+    (src/tensor_core.py:167-188), on the B200.
+
+    Returns (result, BucketStats).  The result's indices are the sorted union
+    minus the bucket index (src/tensor_core.py:117-122).  Host members give a
+    host `Tensor`; if any member is a `DeviceTensor` the result stays on the
+    device as a `DeviceTensor`."""
+    import torch
+    backend = backend or Backend()
+    if not b.tensors:
+        raise ValueError("empty bucket")
+    N.require_device()
+    res = _result_indices(b)
+    w = len(res)
+    if len(b.tensors) > N.MAX_MEMBERS:
+        raise ValueError(f"bucket has {len(b.tensors)} members; at most {N.MAX_MEMBERS} supported")
+    dtype = backend.dtype
+    dev = torch.device("cuda", backend.device)
+    any_dev = any(isinstance(t, DeviceTensor) for t in b.tensors)
+    bit = {a: w - 1 - j for j, a in enumerate(res)}
+    members, masks = [], []
+    with torch.cuda.device(dev):
+        for t in b.tensors:
+            canon = (b.bucket_index,) + tuple(i for i in res if i in t.indices)
+            dt = t if isinstance(t, DeviceTensor) else DeviceTensor.from_host(t, "complex128", backend.device)
+            dt = _device_permute(dt, canon, dtype)
+            st = dt.storage
+            if not st.is_contiguous() or st.data_ptr() % 16:
+                st = st.contiguous().clone()   # vector loads need 16-byte alignment
+            members.append(st)
+            m = 0
+            for a in t.indices:
+                if a != b.bucket_index:
+                    m |= 1 << bit[a]
+            masks.append(m)
+        tdt = torch.complex64 if dtype == "complex64" else torch.complex128
+        out = torch.empty(max(1 << w, 2), dtype=tdt, device=dev)[: 1 << w]
+        elapsed = _BucketLauncher.run(members, masks, out, w, dtype)
+    result = DeviceTensor(res, out)
+    if not any_dev:
+        result = result.to_host()
+    return result, BucketStats(width=w, elapsed_ns=elapsed if backend.profile else 0,
+                               backend_used=backend.route(w))
+
+
+# BASELINE.json vocabulary: "process-bucket"
+process_bucket = contract_bucket

@@ -1,0 +1,155 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+golden vectors and the CPU oracle.  Tolerances (BASELINE.json north_star):
+complex128 <= 1e-10 (relative on scalars; 1e-12 abs on bucket elements),
+complex64 <= 1e-5."""
+import numpy as np
+import pytest
+
+from conftest import load_golden_buckets, load_json
+from oracle import qtn_oracle as O
+
+import paper_2210_15874_b200 as Q
+
+pytestmark = pytest.mark.gpu
+C128 = Q.Backend.b200(dtype="complex128")
+C64 = Q.Backend.b200(dtype="complex64")
+
+
+def _cfg(name):
+    g = load_json("qaoa.json")[name]
+    graph = Q.Graph(g["n"], tuple(tuple(e) for e in g["edges"])) if "edges" in g else None
+    params = Q.QaoaParams(g["p"], g["gammas"], g["betas"])
+    return g, graph, params
+
+
+@pytest.mark.parametrize("case", range(len(load_golden_buckets())))
+def test_bucket_golden_c128(case):
+    bidx, mem, ridx, rdata = load_golden_buckets()[case]
+    b = Q.Bucket(bidx, [Q.Tensor(i, d) for i, d in mem])
+    out, st = Q.contract_bucket(b, C128)
+    assert out.indices == ridx and st.width == len(ridx)
+    np.testing.assert_allclose(out.data, rdata, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("case", range(len(load_golden_buckets())))
+def test_bucket_golden_c64(case):
+    bidx, mem, ridx, rdata = load_golden_buckets()[case]
+    b = Q.Bucket(bidx, [Q.Tensor(i, d) for i, d in mem])
+    out, _ = Q.contract_bucket(b, C64)
+    scale = max(1.0, float(np.abs(rdata).max()))
+    np.testing.assert_allclose(out.data, rdata, rtol=1e-5, atol=1e-5 * scale)
+
+
+def test_bucket_device_tensors_stay_on_device():
+    rng = np.random.default_rng(5)
+    a = Q.Tensor((3, 1, 0), rng.standard_normal((2, 2, 2)) + 1j * rng.standard_normal((2, 2, 2)))
+    b = Q.Tensor((0, 2), rng.standard_normal((2, 2)) + 0j)
+    da = Q.DeviceTensor.from_host(a)
+    out, _ = Q.contract_bucket(Q.Bucket(0, [da, b]), C128)
+    assert isinstance(out, Q.DeviceTensor) and out.indices == (1, 2, 3)
+    ridx, ref = O.bucket_fast(0, [(a.indices, a.data), (b.indices, b.data)])
+    np.testing.assert_allclose(out.data, ref, atol=1e-12)
+
+
+def test_bucket_errors():
+    with pytest.raises(ValueError, match="empty bucket"):
+        Q.contract_bucket(Q.Bucket(0, []), C128)
+
+
+@pytest.mark.parametrize("k", range(12))
+def test_networks_golden(k):
+    rec = load_json("networks.json")[k]
+    c = Q.Circuit(rec["n"], [Q.Gate(a, tuple(b), x) for a, b, x in rec["gates"]])
+    tn = Q.amplitude_network(c, rec["bits"])
+    order = rec["order_minfill"]
+    for be, tol in ((C128, 1e-10), (C64, 1e-5)):
+        v, stats = Q.contract_network(tn, order, be)
+        assert abs(v - complex(*rec["value"])) <= tol
+        assert [s.width for s in stats] == [w for w in rec["widths_minfill"]]
+        sv = Q.contract_sliced(tn, order, rec["sliced"], be)
+        assert abs(sv - complex(*rec["sliced_value"])) <= tol
+
+
+def test_cfg1_energy_c128_c64():
+    g, graph, params = _cfg("cfg1")
+    e128 = Q.qaoa_energy(graph, params, C128)
+    assert abs(e128 - g["energy"]) <= 1e-10 * abs(g["energy"])
+    e64 = Q.qaoa_energy(graph, params, C64)
+    assert abs(e64 - g["energy"]) <= 1e-5 * abs(g["energy"])
+    det = Q.qaoa_energy_detailed(graph, params, C128)
+    for (edge, zz, stats), rec in zip(det, g["cones"]):
+        assert list(edge) == rec["edge"]
+        assert abs(zz - rec["zz"][0]) <= 1e-10
+        assert [s.width for s in stats] == rec["widths"]
+
+
+@pytest.mark.parametrize("ci", [0, 1])
+def test_cfg2_lightcone(ci):
+    g, graph, params = _cfg("cfg2")
+    rec = g["cones"][ci]
+    c = Q.qaoa_maxcut_circuit(graph, params)
+    lc = Q.extract_lightcone(c, tuple(rec["edge"]), cone="tight")
+    order = Q.greedy_order(lc.network)
+    assert order == rec["order"]
+    v128, st = Q.contract_network(lc.network, order, C128)
+    assert abs(v128.real - rec["zz"][0]) <= 1e-10
+    assert [s.width for s in st] == rec["widths"]
+    v64, _ = Q.contract_network(lc.network, order, C64)
+    assert abs(v64.real - rec["zz"][0]) <= 1e-5
+    # repeated launches of the cached program (self-resetting control block)
+    for _ in range(3):
+        again, _ = Q.contract_network(lc.network, order, C64)
+        assert again == v64
+
+
+def test_cfg2_sliced_equals_unsliced():
+    g, graph, params = _cfg("cfg2")
+    rec = g["cones"][1]
+    c = Q.qaoa_maxcut_circuit(graph, params)
+    lc = Q.extract_lightcone(c, tuple(rec["edge"]), cone="tight")
+    order = rec["order"]
+    sl = Q.suggest_slicing(lc.network, order, 21)
+    assert Q.dry_run(lc.network, order, fixed=sl).contraction_width <= 21
+    v = Q.contract_sliced(lc.network, order, sl, C128)
+    assert abs(v.real - rec["zz"][0]) <= 1e-10
+
+
+def test_cfg3_energy_tight_c64():
+    g, graph, params = _cfg("cfg3")
+    e = Q.qaoa_energy(graph, params, C64, cone="tight")
+    assert abs(e - g["energy"]) <= 1e-5 * abs(g["energy"])
+    det = Q.qaoa_energy_detailed(graph, params, C128, cone="tight")
+    for (edge, zz, _), rec in zip(det, g["cones_tight"]):
+        assert abs(zz - rec["zz"][0]) <= 1e-10
+
+
+def test_cfg4_sample_cones():
+    g = load_json("qaoa.json")["cfg4"]
+    graph = Q.random_regular_graph(200, 3, seed=0)
+    params = Q.QaoaParams(5, g["gammas"], g["betas"])
+    c = Q.qaoa_maxcut_circuit(graph, params)
+    for rec in g["cones"]:
+        lc = Q.extract_lightcone(c, tuple(rec["edge"]), cone="tight")
+        order = Q.greedy_order(lc.network)
+        v, st = Q.contract_network(lc.network, order, C64)
+        assert abs(v.real - rec["zz"][0]) <= 1e-5
+        assert [s.width for s in st] == rec["widths"]
+
+
+def test_memory_cap_and_open_network():
+    g, graph, params = _cfg("cfg2")
+    c = Q.qaoa_maxcut_circuit(graph, params)
+    lc = Q.extract_lightcone(c, (0, 15), cone="tight")
+    order = Q.greedy_order(lc.network)
+    with pytest.raises(Q.MemoryCapError, match="memory cap exceeded"):
+        Q.contract_network(lc.network, order, C64, mem_cap=1 << 20)
+    tn = Q.TensorNetwork([Q.Tensor((0,), [1, 2])], open_indices=(0,))
+    with pytest.raises(ValueError, match="closed"):
+        Q.contract_network(tn, [], C64)
+
+
+def test_rank0_and_scalar_inputs():
+    tn = Q.TensorNetwork([Q.Tensor((), 2.0 + 1j), Q.Tensor((0,), [1, 2]), Q.Tensor((0,), [3, 4j])])
+    v, st = Q.contract_network(tn, [0], C128)
+    assert abs(v - (2 + 1j) * (3 + 8j)) < 1e-12
+    assert [s.width for s in st] == [0]

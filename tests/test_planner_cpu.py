@@ -1,0 +1,167 @@
+"""Host planner parity (CPU): orders, dry runs and slicing choices equal the
+reference's golden outputs; device programs emulated in numpy equal the
+oracle's values."""
+import numpy as np
+import pytest
+
+from conftest import load_golden_buckets, load_json
+from emulator import run_program
+from oracle import qtn_oracle as O
+
+import paper_2210_15874_b200 as Q
+from paper_2210_15874_b200 import engine as E
+
+
+def _gates(rec):
+    return [Q.Gate(k, tuple(q), a) for k, q, a in rec["gates"]]
+
+
+def _cfg(name):
+    g = load_json("qaoa.json")[name]
+    graph = Q.Graph(g["n"], tuple(tuple(e) for e in g["edges"]))
+    params = Q.QaoaParams(g["p"], g["gammas"], g["betas"])
+    return g, graph, params
+
+
+def _emulate(tn, order, dtype="complex128", fixed=(), assignment=None):
+    t = E.plan_template([x.indices for x in tn.tensors], order, dtype, fixed)
+    prog = E.Program([E.Instance(t, assignment or {})], dtype)
+    raw = np.concatenate([np.asarray(x.data).ravel() for x in tn.tensors])
+    return run_program(prog, [raw])[0], t, prog
+
+
+@pytest.mark.parametrize("k", range(12))
+def test_network_orders_and_values(k):
+    rec = load_json("networks.json")[k]
+    c = Q.Circuit(rec["n"], _gates(rec))
+    tn = Q.amplitude_network(c, rec["bits"])
+    for h in ("minfill", "mindegree"):
+        order = Q.greedy_order(tn, h)
+        assert order == rec[f"order_{h}"]
+        assert list(Q.dry_run(tn, order).per_bucket_widths) == rec[f"widths_{h}"]
+    v, t, _ = _emulate(tn, rec["order_minfill"])
+    assert abs(v - complex(*rec["value"])) < 1e-12
+    assert list(t.w) == [w for w in rec["widths_minfill"]][: len(t.w)]
+    if "suggest" in rec:
+        assert Q.suggest_slicing(tn, rec["order_minfill"], rec["slice_target"]) == rec["suggest"]
+    # sliced: sum of emulated slices
+    sl = rec["sliced"]
+    t = E.plan_template([x.indices for x in tn.tensors], rec["order_minfill"], "complex128", sl)
+    insts = [E.Instance(t, dict(zip(sl, bits))) for bits in np.ndindex(*(2,) * len(sl))]
+    prog = E.Program(insts, "complex128")
+    raw = np.concatenate([np.asarray(x.data).ravel() for x in tn.tensors])
+    vals = run_program(prog, [raw] * len(insts))
+    assert abs(vals.sum() - complex(*rec["sliced_value"])) < 1e-12
+
+
+def test_cfg1_emulated_energy():
+    g, graph, params = _cfg("cfg1")
+    c = Q.qaoa_maxcut_circuit(graph, params)
+    tot = 0.0
+    for rec in g["cones"]:
+        lc = Q.extract_lightcone(c, tuple(rec["edge"]))
+        order = Q.greedy_order(lc.network)
+        assert order == rec["order"]
+        v, _, _ = _emulate(lc.network, order)
+        assert abs(v.real - rec["zz"][0]) < 1e-12
+        tot += 0.5 * (1 - v.real)
+    assert tot == pytest.approx(g["energy"], abs=1e-12)
+
+
+def test_cfg1_batched_program_and_c64():
+    g, graph, params = _cfg("cfg1")
+    c = Q.qaoa_maxcut_circuit(graph, params)
+    insts, raws = [], []
+    for rec in g["cones"]:
+        tn = Q.extract_lightcone(c, tuple(rec["edge"])).network
+        insts.append(E.Instance(E.plan_template([x.indices for x in tn.tensors], rec["order"], "complex64")))
+        raws.append(np.concatenate([np.asarray(x.data).ravel() for x in tn.tensors]))
+    prog = E.Program(insts, "complex64")
+    vals = run_program(prog, raws)
+    for v, rec in zip(vals, g["cones"]):
+        assert abs(v.real - rec["zz"][0]) < 1e-5
+
+
+def test_cfg2_tight_cone_structure_and_plan():
+    g, graph, params = _cfg("cfg2")
+    c = Q.qaoa_maxcut_circuit(graph, params)
+    for rec in g["cones"]:
+        lc = Q.extract_lightcone(c, tuple(rec["edge"]), cone="tight")
+        assert len(lc.network.tensors) == rec["n_tensors"]
+        order = Q.greedy_order(lc.network)
+        assert order == rec["order"]
+        assert list(Q.dry_run(lc.network, order).per_bucket_widths) == rec["widths"]
+        t = E.plan_template([x.indices for x in lc.network.tensors], order, "complex64")
+        assert t.max_width == max(rec["widths"])
+        prog = E.Program([E.Instance(t)], "complex64")
+        # every dependency points to a lower ticket; smem fits the budget
+        tb = prog.buckets["tick_begin"]
+        for b in prog.buckets:
+            for d in prog.deps[b["dep_begin"]: b["dep_begin"] + b["n_dep"]]:
+                assert tb[d["bucket"]] < b["tick_begin"]
+        assert prog.smem_bytes <= E.SMEM_BUDGET
+
+
+def test_tight_cone_matches_reference_cone_small():
+    """Tight and reference cones give the same <ZZ>."""
+    g, graph, params = _cfg("cfg1")
+    c = Q.qaoa_maxcut_circuit(graph, params)
+    for e in graph.edges[:6]:
+        a = Q.extract_lightcone(c, e)
+        b = Q.extract_lightcone(c, e, cone="tight")
+        va, _, _ = _emulate(a.network, Q.greedy_order(a.network))
+        vb, _, _ = _emulate(b.network, Q.greedy_order(b.network))
+        assert abs(va - vb) < 1e-13
+
+
+def test_random_graph_matches_oracle_and_statevector():
+    graph = Q.random_regular_graph(8, 3, seed=3)
+    params = Q.QaoaParams(2, [0.5, 0.2], [0.3, 0.6])
+    c = Q.qaoa_maxcut_circuit(graph, params)
+    e_tot = 0.0
+    for e in graph.edges:
+        lc = Q.extract_lightcone(c, e)
+        v, _, _ = _emulate(lc.network, Q.greedy_order(lc.network))
+        e_tot += 0.5 * (1 - v.real)
+    sv = O.statevector_energy(8, list(graph.edges), list(params.gammas), list(params.betas))
+    assert abs(e_tot - sv) < 1e-10
+
+
+def test_graph_and_params_generators():
+    assert list(Q.random_regular_graph(30, 3, 0).edges) == O.random_regular_graph(30, 3, 0)
+    p = Q.QaoaParams.seeded(4, 0)
+    gm, bt = O.seeded_angles(4, 0)
+    assert list(p.gammas) == gm and list(p.betas) == bt
+
+
+def test_errors_mirror_reference(rng):
+    tn = Q.TensorNetwork([Q.Tensor((0, 1), np.ones((2, 2))), Q.Tensor((1,), [1, 2])])
+    with pytest.raises(ValueError, match="missing"):
+        Q.dry_run(tn, [0])
+    with pytest.raises(ValueError):
+        Q.greedy_order(tn, "bogus")
+    with pytest.raises(ValueError):
+        Q.Tensor((0, 0), np.zeros((2, 2)))
+    with pytest.raises(ValueError):
+        Q.Bucket(3, [Q.Tensor((0,), [1, 2])])
+    assert Q.memory_estimate(27) == 2147483648
+    assert Q.memory_estimate(27, "complex64") == 1073741824
+    with pytest.raises(ValueError):
+        Q.memory_estimate(-1)
+
+
+def test_plan_masks_follow_canonical_layout():
+    """Every member of a bucket carries the bucket index as its slowest axis
+    and a mask whose bits are a subset of the result axes."""
+    g, graph, params = _cfg("cfg2")
+    c = Q.qaoa_maxcut_circuit(graph, params)
+    lc = Q.extract_lightcone(c, (0, 15), cone="tight")
+    order = Q.greedy_order(lc.network)
+    t = E.plan_template([x.indices for x in lc.network.tensors], order, "complex64")
+    for b in range(len(t.w)):
+        full = (1 << int(t.w[b])) - 1
+        for k in range(t.mem_ptr[b], t.mem_ptr[b + 1]):
+            assert int(t.mem_mask[k]) & ~full == 0
+    # algorithmic bytes of the cfg-2 cone (1.468 GB c64)
+    gb = E.algorithmic_bytes(t, "complex64") / 1e9
+    assert gb == pytest.approx(1.468, abs=0.01)
