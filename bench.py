@@ -1,0 +1,360 @@
+"""Benchmark of the north-star path: one N=30, p=4 QAOA MaxCut edge lightcone
+(BASELINE.json configs[1]; SURVEY 8(d) cfg 2: tight cone of edge (0,15),
+width 25, 270 buckets, 1.468 GB algorithmic traffic at complex64) contracted
+by bucket elimination on the B200.
+
+  python bench.py [--gpus N --steps K --warmup W --dtype c64|c128]
+  python bench.py --impl reference ...   (the reference algorithm on host cores)
+
+A step = one full contraction of the lightcone (plus, at N > 1, the NCCL
+all-reduce of the per-rank <ZZ> slot vector).  Weak scaling: every rank
+contracts one lightcone per step.  `value` is device time (CUDA events on
+the launching stream, L2 flushed before every step, max over ranks); `e2e`
+is the public API call `contract_network(tn, order, backend)` from host
+tensors with the input upload and the result download inside the timed
+region (wall clock, max over ranks).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "lightcones/s (N=30,p=4 single-lightcone contraction)"
+UNIT = "lightcones/s"
+PAPER_BEST_S = 2.1       # NumPy+CuPy mixed, V100
+EDGE = (0, 15)
+WORKLOAD = "cfg2: 3-regular N=30 (seed 0), p=4 (seeded angles), tight lightcone of edge (0,15): 564 tensors, 270 buckets, widths 0-25"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-sample", type=int, default=2, help="oracle contractions for cpu_baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget-s", type=float, default=150.0)
+    return ap.parse_args()
+
+
+def build_workload():
+    import paper_2210_15874_b200 as Q
+    g = Q.random_regular_graph(30, 3, seed=0)
+    params = Q.QaoaParams.seeded(4, 0)
+    c = Q.qaoa_maxcut_circuit(g, params)
+    lc = Q.extract_lightcone(c, EDGE, cone="tight")
+    order = Q.greedy_order(lc.network)
+    return g, params, lc, order
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                smax.append(float(p[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(dtype):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(dtype)
+    except Exception:
+        return None
+
+
+def dist_setup(n):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_oracle_time(lc, order, n):
+    """The reference algorithm (oracle port of src/ordering.py:148-189 +
+    src/tensor_core.py:148-164, numpy complex128) on one host core."""
+    from oracle import qtn_oracle as O
+    ts = [(t.indices, t.data) for t in lc.network.tensors]
+    t0 = time.perf_counter()
+    val = None
+    for _ in range(n):
+        val, _ = O.contract_network(ts, order)
+    dt = (time.perf_counter() - t0) / n
+    return dt, val
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import qtn_oracle as O
+    g, params, lc, order = build_workload()
+    ts = [(t.indices, t.data) for t in lc.network.tensors]
+    threads = max(1, min(os.cpu_count() or 1, 16))
+
+    def one(_):
+        v, _ = O.contract_network(ts, order)
+        return v
+
+    pool = ThreadPoolExecutor(max_workers=threads)
+    t0 = time.perf_counter()
+    list(pool.map(one, range(threads)))       # warm-up step (capped at 1)
+    est = time.perf_counter() - t0
+    steps = max(1, min(args.steps, int(args.ref_budget_s // max(est, 1e-3))))
+    t0 = time.perf_counter()
+    vals = []
+    for _ in range(steps):
+        vals = list(pool.map(one, range(threads)))
+    dt = time.perf_counter() - t0
+    pool.shutdown()
+    value = threads * steps / dt
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
+        "steps_requested": args.steps, "warmup": 1, "ms_per_step": 1e3 * dt / steps,
+        "s_per_lightcone": dt / steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded graph/angles)",
+        "config": {"workload": WORKLOAD, "impl": "oracle port of the reference NumPy path (Backend.fast())",
+                   "threads": threads, "zz": vals[0].real},
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{steps} steps x {threads} concurrent full contractions of the cfg-2 lightcone "
+                                   f"(numpy complex128, one thread each)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import paper_2210_15874_b200 as Q
+    from paper_2210_15874_b200 import engine as E
+
+    rank, world, local = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    dtype = "complex64" if args.dtype == "c64" else "complex128"
+    g, params, lc, order = build_workload()
+    tn = lc.network
+    be = Q.Backend.b200(dtype=dtype, device=local, profile=False)
+
+    # ---- device-resident program (inputs in HBM before the timed region) ----
+    tmpl = E.plan_template([t.indices for t in tn.tensors], order, dtype)
+    prog = E.Program([E.Instance(tmpl)], dtype)
+    ex = E.Executor(prog, device=local, timing=False)
+    raw = np.concatenate([np.asarray(t.data).ravel() for t in tn.tensors])
+    ex.stage_inputs([raw])
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+    slots = torch.zeros(2 * world, dtype=torch.float64, device="cuda")
+    alg_bytes = prog.algorithmic_bytes()
+
+    def step_device():
+        ex.launch(stream)
+        if world > 1:
+            slots.zero_()
+            slots[2 * rank: 2 * rank + 2].copy_(ex.results[:2])
+            torch.distributed.all_reduce(slots)
+
+    for _ in range(max(3, args.warmup)):
+        step_device()
+    torch.cuda.synchronize()
+    val = complex(*ex.results[:2].cpu().numpy())
+    if world > 1:
+        torch.distributed.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kern = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            kern[i][0].record(stream)
+            ex.launch(stream)
+            kern[i][1].record(stream)
+            if world > 1:
+                slots.zero_()
+                slots[2 * rank: 2 * rank + 2].copy_(ex.results[:2])
+                torch.distributed.all_reduce(slots)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        t_dev = sum(a.elapsed_time(b) for a, b in ev) / 1e3
+        t_kern = sum(a.elapsed_time(b) for a, b in kern) / 1e3
+        if world > 1:
+            torch.distributed.barrier()
+
+        # ---- e2e: public API from host tensors ----
+        for _ in range(max(3, args.warmup)):
+            Q.contract_network(tn, order, be)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            v_e2e, _ = Q.contract_network(tn, order, be)
+        torch.cuda.synchronize()
+        t_e2e = time.perf_counter() - t0
+    clocks = clk.summary()
+    t_dev = max_over_ranks(t_dev, world)
+    t_e2e = max_over_ranks(t_e2e, world)
+    t_kern = max_over_ranks(t_kern, world)
+
+    # c128 device time as a side figure (same program structure)
+    side = {}
+    if dtype == "complex64":
+        tm2 = E.plan_template([t.indices for t in tn.tensors], order, "complex128")
+        ex2 = E.Executor(E.Program([E.Instance(tm2)], "complex128"), device=local, timing=False)
+        ex2.stage_inputs([raw])
+        for _ in range(3):
+            ex2.launch(stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n2 = max(10, args.steps // 4)
+        tot = 0.0
+        for _ in range(n2):
+            flush.zero_()
+            e0.record(stream)
+            ex2.launch(stream)
+            e1.record(stream)
+            e1.synchronize()
+            tot += e0.elapsed_time(e1) / 1e3
+        side = {"c128_ms_per_lightcone": 1e3 * tot / n2,
+                "c128_gbs": ex2.prog.algorithmic_bytes() / (tot / n2) / 1e9,
+                "c128_zz": float(ex2.fetch_results()[0].real)}
+        del ex2
+
+    if rank != 0:
+        return 0
+    peak, peak_src = peak_hbm()
+    achieved = alg_bytes / (t_kern / args.steps) / 1e9
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        dt, v_cpu = cpu_oracle_time(lc, order, args.cpu_sample)
+        cpu = {"value": 1.0 / dt, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"{args.cpu_sample} full contractions of the cfg-2 lightcone, oracle port of the reference "
+                         f"NumPy path (complex128, one core); <ZZ> = {v_cpu.real:.15f}"}
+    n_in = prog.n_input_elems * E.ELEM_BYTES[dtype]
+    value = world * args.steps / t_dev
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": 1e3 * t_dev / args.steps,
+        "s_per_lightcone": t_dev / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": value * PAPER_BEST_S, "dtype": args.dtype, "data": "synthetic (seeded graph/angles)",
+        "config": {"workload": WORKLOAD, "parallelism": f"{world} rank(s), one lightcone per rank per step",
+                   "l2": "flushed (256 MiB write) before every timed step", "zz": val.real,
+                   "algorithmic_bytes_per_step": alg_bytes, "grid": ex.grid, "smem_bytes": prog.smem_bytes,
+                   "n_buckets": prog.n_buckets, "n_tickets": prog.n_tickets,
+                   "vs_baseline_ref": "value x 2.1 s: speed-up over the paper's best single-lightcone time "
+                                      "(NumPy+CuPy mixed on V100, PAPER.md:64)", **side},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": ncu_traffic(args.dtype), "peak_source": peak_src,
+                     "kernel": "program_kernel<float>" if dtype == "complex64" else "program_kernel<double>"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": world * args.steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": n_in,
+                "d2h_bytes_per_step": 16, "s_per_lightcone": t_e2e / args.steps,
+                "call": "paper_2210_15874_b200.contract_network(tn, order, Backend.b200(...)) from host Tensors",
+                "zz": v_e2e.real},
+        "gpu_launches": args.steps,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

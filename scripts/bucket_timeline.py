@@ -1,0 +1,51 @@
+"""Per-bucket device timeline of the cfg-2 lightcone program (globaltimer
+stamps recorded by the program kernel): where the 0.x ms go."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2210_15874_b200 import engine as E  # noqa: E402
+
+dtype = sys.argv[1] if len(sys.argv) > 1 else "complex64"
+g, params, lc, order = bench.build_workload()
+tn = lc.network
+t = E.plan_template([x.indices for x in tn.tensors], order, dtype)
+prog = E.Program([E.Instance(t)], dtype)
+ex = E.Executor(prog, timing=True)
+raw = np.concatenate([np.asarray(x.data).ravel() for x in tn.tensors])
+ex.stage_inputs([raw])
+for _ in range(5):
+    ex.launch()
+torch.cuda.synchronize()
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+flush.zero_()
+ex.launch()
+torch.cuda.synchronize()
+t0, t1 = ex.fetch_timing()
+esz = E.ELEM_BYTES[dtype]
+B = prog.buckets
+origin = t0.min()
+rows = []
+for gid in range(prog.n_buckets):
+    b = B[gid]
+    if b["w"] < 0:
+        continue
+    mem = prog.members[b["mem_begin"]: b["mem_begin"] + b["n_mem"]]
+    by = (1 << int(b["w"])) + sum(1 << (1 + bin(int(m["mask"])).count("1")) for m in mem)
+    rows.append((t0[gid] - origin, t1[gid] - origin, int(b["w"]), int(b["tile_bits"]), int(b["n_tiles"]),
+                 int(b["n_mem"]), by * esz))
+rows.sort()
+tot = t1.max() - origin
+print(f"total {tot/1e3:.1f} us, buckets {len(rows)}")
+small = [r for r in rows if r[2] < 12]
+print(f"small (w<12): {len(small)} buckets, span {max(r[1] for r in small)/1e3:.1f} us")
+print(" start_us   end_us   dur_us  w  L  tiles nmem   MB    GB/s")
+for r in rows:
+    if r[2] >= 12:
+        d = r[1] - r[0]
+        print(f"{r[0]/1e3:8.1f} {r[1]/1e3:8.1f} {d/1e3:8.1f} {r[2]:2d} {r[3]:2d} {r[4]:6d} {r[5]:3d} {r[6]/1e6:7.1f} {r[6]/max(d,1):7.0f}")
