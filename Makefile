@@ -1,7 +1,8 @@
 # Build the sm_100a engine library in-tree (travels to the GPU box with the repo).
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -cudart static -Iinclude
+MINB ?= 2
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -cudart static -Iinclude -DQTN_MINB=$(MINB)
 LIB := paper_2210_15874_b200/lib/libqtn_b200.so
 SRC := paper_2210_15874_b200/csrc/qtn_b200.cu
 
@@ -10,6 +11,10 @@ all: $(LIB)
 $(LIB): $(SRC) include/qtn_b200.h
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -o $@ $(SRC)
+
+# variant build for A/B measurements: make variant MINB=3 -> lib/libqtn_b200_mb3.so
+variant:
+	$(NVCC) $(NVFLAGS) -o paper_2210_15874_b200/lib/libqtn_b200_mb$(MINB).so $(SRC)
 
 sass: $(LIB)
 	cuobjdump -sass $(LIB) | grep -E "Function|LDG|STG|ATOM|RED" | head -50

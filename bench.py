@@ -328,8 +328,8 @@ def run_ours(args):
         "vs_baseline": value * PAPER_BEST_S, "dtype": args.dtype, "data": "synthetic (seeded graph/angles)",
         "config": {"workload": WORKLOAD, "parallelism": f"{world} rank(s), one lightcone per rank per step",
                    "l2": "flushed (256 MiB write) before every timed step", "zz": val.real,
-                   "algorithmic_bytes_per_step": alg_bytes, "grid": ex.grid, "smem_bytes": prog.smem_bytes,
-                   "n_buckets": prog.n_buckets, "n_tickets": prog.n_tickets,
+                   "algorithmic_bytes_per_step": alg_bytes, "executed_bytes_per_step": prog.executed_bytes(),
+                   "program": prog.describe(),
                    "vs_baseline_ref": "value x 2.1 s: speed-up over the paper's best single-lightcone time "
                                       "(NumPy+CuPy mixed on V100, PAPER.md:64)", **side},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

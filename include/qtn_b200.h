@@ -17,12 +17,17 @@
  *    (thread-local).  No exceptions cross the ABI.
  *  - Element types: complex64 (float2) or complex128 (double2), QTN_C64/QTN_C128.
  *  - Canonical layout: every tensor in a program is stored with its axes
- *    sorted by elimination position, earliest-eliminated axis SLOWEST.  A
- *    member of bucket b therefore has b as its slowest axis and its other
- *    axes in the same relative order as the bucket's result axes, so its
- *    element offset is   b * 2^popc(mask) + pext(r, mask)   for result
- *    element r, where bit j of `mask` says the member carries result axis j
- *    (j = 0 is the fastest result axis).
+ *    sorted by elimination position, earliest-eliminated axis SLOWEST.
+ *  - A work item sums k >= 1 indices at once (k = 1 is one reference bucket;
+ *    k > 1 is a chain of reference buckets merged by the planner — the
+ *    intermediate results never touch HBM).  The summed indices are all
+ *    eliminated before any result index, so a member's summed axes are its
+ *    slowest axes and its element offset is
+ *        (pext(s, smask) << popc(mask)) + pext(r, mask)
+ *    for summed assignment s (k bits) and result element r (w bits); bit j
+ *    of `mask` / `smask` says the member carries result / summed axis j
+ *    (j = 0 is the fastest, i.e. latest-eliminated, axis).
+ *    out[r] = sum_{s = 0 .. 2^k - 1} prod_i member_i(s, r), s ascending.
  *  - Thread safety: launches on distinct streams are independent; a program's
  *    control block must not be shared by concurrent launches.
  */
@@ -35,7 +40,7 @@
 extern "C" {
 #endif
 
-#define QTN_ABI_VERSION 1
+#define QTN_ABI_VERSION 4
 
 enum {
   QTN_OK = 0,
@@ -52,21 +57,35 @@ enum { QTN_C64 = 0, QTN_C128 = 1 };
 #define QTN_MAX_MEMBERS 8
 /* Largest result width a bucket may have (2^40 elements). */
 #define QTN_MAX_WIDTH 40
+/* Largest number of indices one work item sums (merged bucket chain). */
+#define QTN_MAX_SUMMED 6
 
-/* One member tensor of one bucket (16 bytes). */
+/* Member classes for the large-item kernels (chosen by the planner from the
+ * item's tile bits L and step mask): */
+enum {
+  QTN_CLS_STREAMED = 0,  /* carries every tile bit: 16-byte loads from HBM/L2   */
+  QTN_CLS_UNIFORM = 1,   /* carries no tile bit: folded into U[s] once per tile */
+  QTN_CLS_INVARIANT = 2, /* none of the step bits: folded into P[s] (k == 1)    */
+  QTN_CLS_VARYING = 3    /* staged run in smem, gathered per step              */
+};
+
+/* One member tensor of one work item (24 bytes). */
 typedef struct {
-  uint64_t off;  /* element offset of the member in the arena            */
-  uint64_t mask; /* result-axis coverage, bit j = result axis j (j=0 fastest) */
+  uint64_t off;   /* element offset of the member in the arena             */
+  uint64_t mask;  /* result-axis coverage, bit j = result axis j (j=0 fastest) */
+  uint32_t smask; /* summed-axis coverage (k bits)                         */
+  uint32_t cls;   /* QTN_CLS_* (large items)                               */
 } qtn_member_t;
 
-/* One work item: a bucket contraction (w >= 0) or an instance finaliser
- * (w == QTN_FINALIZE) that multiplies rank-0 values into a result slot —
- * the get-result step (src/ordering.py:167-170,183-184).  48 bytes. */
+/* One work item: a (merged) bucket contraction (w >= 0) or an instance
+ * finaliser (w == QTN_FINALIZE) that multiplies rank-0 values into a result
+ * slot — the get-result step (src/ordering.py:167-170,183-184).  56 bytes. */
 #define QTN_FINALIZE (-1)
 typedef struct {
   uint64_t out_off;   /* element offset of the result in the arena          */
   int32_t w;          /* result rank, or QTN_FINALIZE                       */
   int32_t tile_bits;  /* L: each tile computes 2^L consecutive results      */
+  int32_t k;          /* summed indices, 1..QTN_MAX_SUMMED                  */
   int32_t mem_begin;  /* first member in the member table                   */
   int32_t n_mem;      /* 1..QTN_MAX_MEMBERS (finaliser: any count >= 0)     */
   int32_t dep_begin;  /* first dependency in the dependency table           */
@@ -75,6 +94,9 @@ typedef struct {
   int32_t n_tiles;    /* 2^(w - L); 1 for a finaliser                       */
   int32_t slot;       /* finaliser: result slot (double2); else -1          */
   int32_t smem_elems; /* staged elements per tile (<= program smem budget)  */
+  uint32_t stmask;    /* tile bits each thread walks sequentially (vector
+                         path; 0 = default).  Members not carrying any of
+                         them are multiplied once per tile and reused.       */
 } qtn_bucket_t;
 
 /* Dependency: wait until bucket `bucket` has completed `need` tiles. */
@@ -85,14 +107,16 @@ typedef struct {
 
 /* A planned program (one or many lightcones / slices).  All pointers are
  * DEVICE pointers owned by the caller.  `tick_begin` must be a dense int32
- * copy of buckets[i].tick_begin (used for ticket -> bucket search). */
+ * copy of buckets[i].tick_begin (stage-relative tickets of small items, used
+ * for ticket -> item search).  ctrl = 2 words per graph node (small-stage
+ * ticket and exit counters) followed by one completion counter per item. */
 typedef struct {
   int32_t dtype;                /* QTN_C64 / QTN_C128                         */
   int32_t n_buckets;
   int32_t n_tickets;
   int32_t smem_bytes;           /* dynamic shared memory per block (staging)  */
   int32_t grid;                 /* 0 = all resident blocks (occupancy)        */
-  int32_t flags;                /* reserved, 0                                */
+  int32_t n_nodes;              /* graph nodes (ctrl layout, see above)       */
   const qtn_bucket_t* buckets;
   const qtn_member_t* members;
   const qtn_dep_t* deps;
@@ -104,20 +128,48 @@ typedef struct {
   unsigned long long* timing;   /* optional: 2 per bucket (first start, last end, ns) */
 } qtn_program_t;
 
+/* Execution node of a program graph.
+ *  QTN_NODE_SMALL: a persistent launch over items [first, first + count) —
+ *    the batched small-bucket schedule (K2): dependencies inside the stage
+ *    are per-item completion counters, tickets are stage-relative.
+ *  QTN_NODE_LARGE: one item, one launch of the large-item kernel (K1)
+ *    specialised by `variant`. */
+enum { QTN_NODE_SMALL = 0, QTN_NODE_LARGE = 1 };
+#define QTN_VARIANT_GENERIC (-1)
+/* variant = log2(2^k) | (varying staged members) << 4 | (one streamed member) << 8,
+ * for k <= 3 and at most 4 varying members; otherwise QTN_VARIANT_GENERIC. */
+typedef struct {
+  int32_t kind;
+  int32_t first;
+  int32_t count;
+  int32_t n_tickets;  /* SMALL: tickets of the stage                         */
+  int32_t variant;    /* LARGE: kernel variant                               */
+  int32_t dep_begin;  /* into the node dependency list                       */
+  int32_t n_dep;
+  int32_t smem_bytes; /* dynamic shared memory of the node's kernel          */
+} qtn_node_t;
+
+typedef struct qtn_graph qtn_graph_t;
+
 /* ABI version (QTN_ABI_VERSION). */
 int qtn_abi_version(void);
 /* Last error message of the calling thread ("" if none). */
 const char* qtn_last_error(void);
 /* Number of visible CUDA devices (0 on a CPU-only host; never fails). */
 int qtn_device_count(int* count);
-/* Resident blocks of the program kernel for dtype/smem on the current device. */
-int qtn_program_grid(int32_t dtype, int32_t smem_bytes, int32_t* grid_out);
-/* Zero the control block (tickets, exit count, per-bucket completion). */
+/* Zero the control block (ticket / exit counters and item completions). */
 int qtn_program_reset(const qtn_program_t* prog, void* stream);
-/* Launch the persistent program kernel on `stream` (cudaStream_t, may be 0).
- * The kernel leaves the control block zeroed on exit, so launches of the
- * same program can be issued back to back (or captured in a CUDA graph). */
-int qtn_program_launch(const qtn_program_t* prog, void* stream);
+/* Launch one node (host-side description) on `stream`: the whole dependency
+ * order of a program can be driven by issuing its nodes in a topological
+ * order on one stream. */
+int qtn_node_launch(const qtn_program_t* prog, const qtn_node_t* node, int32_t node_index, void* stream);
+/* Build a CUDA graph of the program's nodes (node_deps holds, per node, the
+ * indices of the nodes it waits for) on the current device. */
+int qtn_graph_create(const qtn_program_t* prog, const qtn_node_t* nodes, int32_t n_nodes,
+                     const int32_t* node_deps, qtn_graph_t** out);
+/* Launch the instantiated graph (one call per program execution). */
+int qtn_graph_launch(qtn_graph_t* g, void* stream);
+int qtn_graph_destroy(qtn_graph_t* g);
 /* dst[e] = convert(src[sum_j bit_j(e) * src_strides[j]]) for e < 2^rank,
  * j = 0 the fastest dst axis; src/dst element types given separately
  * (complex128 -> complex64 narrowing allowed).  General axis permutation +

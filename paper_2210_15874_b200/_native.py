@@ -12,7 +12,8 @@ import os
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libqtn_b200.so")
+LIB_PATH = os.environ.get("QTN_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib",
+                                                     "libqtn_b200.so")
 
 QTN_OK = 0
 QTN_E_INVALID = -1
@@ -24,27 +25,36 @@ QTN_C128 = 1
 QTN_FINALIZE = -1
 MAX_MEMBERS = 8
 MAX_WIDTH = 40
-ABI_VERSION = 1
+MAX_SUMMED = 6
+ABI_VERSION = 4
+QTN_NODE_SMALL = 0
+QTN_NODE_LARGE = 1
+QTN_VARIANT_GENERIC = -1
 
 # every symbol include/qtn_b200.h declares
 EXPORTS = (
     "qtn_abi_version",
     "qtn_last_error",
     "qtn_device_count",
-    "qtn_program_grid",
     "qtn_program_reset",
-    "qtn_program_launch",
+    "qtn_node_launch",
+    "qtn_graph_create",
+    "qtn_graph_launch",
+    "qtn_graph_destroy",
     "qtn_permute",
 )
 
 BUCKET_DT = np.dtype([
-    ("out_off", "<u8"), ("w", "<i4"), ("tile_bits", "<i4"), ("mem_begin", "<i4"),
+    ("out_off", "<u8"), ("w", "<i4"), ("tile_bits", "<i4"), ("k", "<i4"), ("mem_begin", "<i4"),
     ("n_mem", "<i4"), ("dep_begin", "<i4"), ("n_dep", "<i4"), ("tick_begin", "<i4"),
-    ("n_tiles", "<i4"), ("slot", "<i4"), ("smem_elems", "<i4"),
+    ("n_tiles", "<i4"), ("slot", "<i4"), ("smem_elems", "<i4"), ("stmask", "<u4"),
 ])
-MEMBER_DT = np.dtype([("off", "<u8"), ("mask", "<u8")])
+MEMBER_DT = np.dtype([("off", "<u8"), ("mask", "<u8"), ("smask", "<u4"), ("cls", "<u4")])
+NODE_DT = np.dtype([("kind", "<i4"), ("first", "<i4"), ("count", "<i4"), ("n_tickets", "<i4"),
+                    ("variant", "<i4"), ("dep_begin", "<i4"), ("n_dep", "<i4"), ("smem_bytes", "<i4")])
 DEP_DT = np.dtype([("bucket", "<i4"), ("need", "<i4")])
-assert BUCKET_DT.itemsize == 48 and MEMBER_DT.itemsize == 16 and DEP_DT.itemsize == 8
+assert BUCKET_DT.itemsize == 56 and MEMBER_DT.itemsize == 24 and DEP_DT.itemsize == 8
+assert NODE_DT.itemsize == 32
 
 
 class NativeUnavailable(RuntimeError):
@@ -60,7 +70,7 @@ class NativeError(RuntimeError):
 class ProgramC(ctypes.Structure):
     _fields_ = [
         ("dtype", ctypes.c_int32), ("n_buckets", ctypes.c_int32), ("n_tickets", ctypes.c_int32),
-        ("smem_bytes", ctypes.c_int32), ("grid", ctypes.c_int32), ("flags", ctypes.c_int32),
+        ("smem_bytes", ctypes.c_int32), ("grid", ctypes.c_int32), ("n_nodes", ctypes.c_int32),
         ("buckets", ctypes.c_void_p), ("members", ctypes.c_void_p), ("deps", ctypes.c_void_p),
         ("tick_begin", ctypes.c_void_p), ("ctrl", ctypes.c_void_p), ("arena", ctypes.c_void_p),
         ("results", ctypes.c_void_p), ("timing", ctypes.c_void_p),
@@ -85,12 +95,16 @@ def load(path: str = LIB_PATH):
     lib.qtn_last_error.argtypes = []
     lib.qtn_device_count.restype = ctypes.c_int
     lib.qtn_device_count.argtypes = [ctypes.POINTER(ctypes.c_int)]
-    lib.qtn_program_grid.restype = ctypes.c_int
-    lib.qtn_program_grid.argtypes = [i32, i32, ctypes.POINTER(i32)]
     lib.qtn_program_reset.restype = ctypes.c_int
     lib.qtn_program_reset.argtypes = [ctypes.POINTER(ProgramC), vp]
-    lib.qtn_program_launch.restype = ctypes.c_int
-    lib.qtn_program_launch.argtypes = [ctypes.POINTER(ProgramC), vp]
+    lib.qtn_node_launch.restype = ctypes.c_int
+    lib.qtn_node_launch.argtypes = [ctypes.POINTER(ProgramC), vp, i32, vp]
+    lib.qtn_graph_create.restype = ctypes.c_int
+    lib.qtn_graph_create.argtypes = [ctypes.POINTER(ProgramC), vp, i32, vp, ctypes.POINTER(ctypes.c_void_p)]
+    lib.qtn_graph_launch.restype = ctypes.c_int
+    lib.qtn_graph_launch.argtypes = [ctypes.c_void_p, vp]
+    lib.qtn_graph_destroy.restype = ctypes.c_int
+    lib.qtn_graph_destroy.argtypes = [ctypes.c_void_p]
     lib.qtn_permute.restype = ctypes.c_int
     lib.qtn_permute.argtypes = [i32, vp, i64, i32, vp, i32, ctypes.POINTER(i64), vp]
     if lib.qtn_abi_version() != ABI_VERSION:
@@ -113,13 +127,6 @@ def require_device():
     if n.value < 1 or not torch.cuda.is_available():
         raise NativeUnavailable("no CUDA device: the B200 backend has no CPU fallback")
     return lib
-
-
-def program_grid(dtype_code: int, smem_bytes: int) -> int:
-    lib = require_device()
-    g = ctypes.c_int32(0)
-    check(lib.qtn_program_grid(dtype_code, smem_bytes, ctypes.byref(g)))
-    return g.value
 
 
 def permute(src_dtype, src_ptr, src_offset, dst_dtype, dst_ptr, rank, strides, stream):

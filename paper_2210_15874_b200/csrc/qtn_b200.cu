@@ -1,28 +1,36 @@
 // qtn_b200.cu — sm_100a kernels + C ABI of the bucket-elimination engine.
 //
-// One persistent "program" kernel executes a whole planned elimination
-// (one lightcone, one slice, or a batch of them) in a single launch:
+// A planned program (engine.py) is a list of *items* — one reference bucket
+// (src/ordering.py:175-187), or a chain of them merged into one contraction
+// summing k indices — in a topological order, grouped into graph *nodes*:
 //
-//  * Work is a dense ticket space: bucket i owns tickets
-//    [tick_begin_i, tick_begin_i + n_tiles_i); buckets appear in a
-//    topological order of the bucket in-tree (src/ordering.py:175-187), so a
-//    block that takes a ticket only ever waits on LOWER tickets.  Tickets are
-//    taken by running blocks (atomicAdd), which makes the schedule
-//    deadlock-free whatever the residency.
-//  * A tile is 2^L consecutive result elements of one bucket.  Its members
-//    are either STREAMED (the member carries all L tile axes: two contiguous
-//    2^L runs, b = 0 and b = 1, read with 16-byte vector loads straight from
-//    HBM/L2) or STAGED (the member carries a subset of the tile axes: its two
-//    contiguous 2^popc runs are copied to shared memory once per tile and
-//    gathered with a precomputed pext table).
-//  * out[r] = prod_i T_i[b=0] + prod_i T_i[b=1] — the reference's
-//    fast_kernel product order (src/tensor_core.py:148-164): members in
-//    bucket order, then b = 0 + b = 1.
-//  * Completion is a per-bucket tile counter (release: __syncthreads +
-//    __threadfence + atomicAdd; acquire: ld.acquire.gpu spin).  Data produced
-//    inside the launch is read with ld.global.cg (L2, never a stale L1 line).
-//  * Finaliser items multiply an instance's rank-0 values in double precision
-//    into a result slot: the get-result scalar (src/ordering.py:167-170,183-184).
+//  K2  small_kernel   A persistent launch over a stage of small items (result
+//      tiles below one vector step).  Tickets are stage-relative; a block that
+//      takes a ticket only waits on LOWER tickets of the same stage (per-item
+//      completion counters, acquire/release), so the schedule is deadlock-free
+//      whatever the residency.  Threads cover (result element, summed
+//      assignment) pairs, read members straight from L2 and reduce the
+//      assignments in order through shared memory.  Finaliser items multiply
+//      an instance's rank-0 values into its result slot (get-result,
+//      src/ordering.py:167-170,183-184).
+//
+//  K1  large_kernel   One launch per large item, specialised at compile time
+//      by (NS = 2^k, NV = varying staged members, ST = one streamed member),
+//      so every variant gets its own register allocation.  A tile is 2^L
+//      consecutive results; members are classified by the planner:
+//        streamed   carries every tile bit — 16-byte loads from HBM/L2, the NS
+//                   summed-assignment values prefetched together
+//        uniform    carries no tile bit — folded into U[s] once per tile
+//        invariant  carries none of the thread's step bits — folded into P[s]
+//                   in registers once per tile (k == 1)
+//        varying    staged in shared memory by bulk async copies (TMA engine,
+//                   cp.async.bulk + mbarrier), gathered per step
+//      out[r] = sum_s prod_i member_i(s, r), s ascending (deterministic).
+//
+// Nodes are stitched into one CUDA graph per program (dependency edges from
+// the item DAG), so independent items overlap and a whole lightcone is one
+// cudaGraphLaunch.  Data produced inside a launch by other blocks is read with
+// ld.global.cg (L2) — never a stale L1 line.
 //
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo ...
 #include "qtn_b200.h"
@@ -32,6 +40,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <string>
+#include <vector>
 
 namespace {
 
@@ -52,8 +61,10 @@ int cuda_err(cudaError_t e, const char* what) {
 }
 
 constexpr int NT = 256;                 // threads per block
-constexpr int MAXM = QTN_MAX_MEMBERS;   // members per bucket
+constexpr int MAXM = QTN_MAX_MEMBERS;   // members per item
 constexpr int MAXS = 16;                // vector steps per tile: 2^L / (VEC * NT)
+constexpr int MAXNS = 1 << QTN_MAX_SUMMED;
+constexpr int SMALL_PROD_ELEMS = 1024;  // smem products per round of a small tile
 
 template <typename R> struct Cx;
 template <> struct Cx<float> {
@@ -76,7 +87,6 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 
-// vector <-> element views
 __device__ __forceinline__ void split(float4 v, float2 (&e)[2]) {
   e[0] = make_float2(v.x, v.y);
   e[1] = make_float2(v.z, v.w);
@@ -90,6 +100,15 @@ __device__ __forceinline__ uint32_t pext32(uint32_t x, uint32_t m) {
   for (int k = 0; m; ++k) {
     const uint32_t low = m & (0u - m);
     if (x & low) r |= 1u << k;
+    m ^= low;
+  }
+  return r;
+}
+__device__ __forceinline__ uint32_t pdep32(uint32_t x, uint32_t m) {
+  uint32_t r = 0;
+  for (int k = 0; m; ++k) {
+    const uint32_t low = m & (0u - m);
+    if ((x >> k) & 1u) r |= low;
     m ^= low;
   }
   return r;
@@ -115,66 +134,86 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-// Per-block view of the bucket being processed (shared memory).
-struct BlockCtx {
+// ---- mbarrier + bulk async copy (TMA engine, non-tensor form) ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
+
+// =========================================================================
+// K2: persistent small-stage kernel
+// =========================================================================
+struct SmallCtx {
   qtn_bucket_t b;
-  uint64_t off[MAXM];    // member element offset in arena
-  uint64_t mhi[MAXM];    // member mask >> L
-  uint64_t bstr[MAXM];   // b stride = 2^popc(mask)
-  uint64_t base[MAXM];   // b = 0 offset of the member's run for this tile
-  uint32_t mlo[MAXM];    // member mask & (2^L - 1)
-  int32_t pclo[MAXM];    // popc(mlo)
-  int32_t seg[MAXM];     // staged: smem element offset of the run pair; streamed: -1
-  int32_t seglen[MAXM];  // staged: 2^pclo
-  int32_t gs[MAXM][MAXS];  // pext(VEC*NT*s, mlo)
-  int32_t bucket;
+  uint64_t base[MAXM];
+  uint64_t mhi[MAXM];
+  uint64_t off[MAXM];
+  uint32_t mlo[MAXM];
+  int32_t pc[MAXM];
+  int32_t pclo[MAXM];
+  int16_t sig[MAXM][MAXNS];
+  int32_t item;
   int32_t tick;
   int32_t next;
   int32_t last;
 };
 
 template <typename R>
-__global__ void __launch_bounds__(NT) program_kernel(const qtn_program_t P) {
+__global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_t first, int32_t count,
+                                                   int32_t n_tickets, uint32_t* ctl) {
   using T = typename Cx<R>::T;
-  using V = typename Cx<R>::V;
-  constexpr int VEC = Cx<R>::VEC;
-
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* sseg = reinterpret_cast<T*>(smem_raw);
-  __shared__ BlockCtx S;
-
-  T* A = reinterpret_cast<T*>(P.arena);
-  uint32_t* done = P.ctrl + 2;
+  T* sprod = reinterpret_cast<T*>(smem_raw);
+  __shared__ SmallCtx S;
+  const T* A = reinterpret_cast<const T*>(P.arena);
+  T* Aw = reinterpret_cast<T*>(P.arena);
+  uint32_t* done = P.ctrl + 2 * P.n_nodes;
   const int tid = threadIdx.x;
+  const int last_item = first + count - 1;
+  int cur = first;
+  int prepared = -1;
+  uint32_t pend_cnt = 0;   // thread 0: finished, unpublished tiles of pend_item
+  int pend_item = 0;
 
-  int cur = 0;         // bucket of the current ticket (block-uniform, monotone)
-  int prepared = -1;   // bucket whose per-bucket tables are loaded in S
-  int gt[MAXM];        // per-thread pext(VEC*tid, mlo_i)
-
-  if (tid == 0) S.next = (int)atomicAdd(&P.ctrl[0], 1u);
+  if (tid == 0) S.next = (int)atomicAdd(&ctl[0], 1u);
   for (;;) {
     __syncthreads();
     if (tid == 0) {
       S.tick = S.next;
-      // prefetch the following ticket; its latency overlaps this tile
-      if (S.tick < P.n_tickets) S.next = (int)atomicAdd(&P.ctrl[0], 1u);
+      if (S.tick < n_tickets) S.next = (int)atomicAdd(&ctl[0], 1u);   // prefetch
     }
     __syncthreads();
     const int tk = S.tick;
-    if (tk >= P.n_tickets) break;
-
-    // ---- ticket -> bucket: 32-ary search over tick_begin[cur..] (warp 0) ----
+    if (tk >= n_tickets) break;
+    // ---- ticket -> item: 32-ary search over tick_begin[cur..last] (warp 0) ----
     if (tid < 32) {
-      int lo = cur, hi = P.n_buckets - 1;
-      if (lo < hi && __ldg(&P.tick_begin[lo + 1]) > tk) hi = lo;  // same bucket
+      int lo = cur, hi = last_item;
+      if (lo < hi && __ldg(&P.tick_begin[lo + 1]) > tk) hi = lo;
       while (hi > lo) {
-        const int span = hi - lo;
-        const int step = (span + 31) / 32;
+        const int step = (hi - lo + 31) / 32;
         int p = lo + (tid + 1) * step;
         if (p > hi) p = hi;
-        const bool ok = __ldg(&P.tick_begin[p]) <= tk;
-        const unsigned bal = __ballot_sync(0xffffffffu, ok);
-        const int c = __popc(bal);   // predicate is monotone: a prefix of lanes
+        const unsigned bal = __ballot_sync(0xffffffffu, __ldg(&P.tick_begin[p]) <= tk);
+        const int c = __popc(bal);
         if (c == 0) {
           hi = lo + step - 1;
         } else {
@@ -184,61 +223,49 @@ __global__ void __launch_bounds__(NT) program_kernel(const qtn_program_t P) {
           if (c < 32 && pnext - 1 < hi) hi = pnext - 1;
         }
       }
-      if (tid == 0) S.bucket = lo;
+      if (tid == 0) {
+        S.item = lo;
+        if (lo != prepared) S.b = P.buckets[lo];
+      }
     }
     __syncthreads();
-    cur = S.bucket;
-
-    // ---- per-bucket preparation (once per bucket per block) ----
+    cur = S.item;
     if (cur != prepared) {
-      if (tid == 0) S.b = P.buckets[cur];
-      __syncthreads();
+      // publish finished tiles of the previous item before any waiting
+      if (tid == 0 && pend_cnt) {
+        __threadfence();
+        atomicAdd(&done[pend_item], pend_cnt);
+        pend_cnt = 0;
+      }
       const int nm = S.b.w >= 0 ? S.b.n_mem : 0;
       const int L = S.b.tile_bits;
-      // wait for producers (and WAR predecessors)
-      for (int k = tid; k < S.b.n_dep; k += NT) {
-        const qtn_dep_t d = P.deps[S.b.dep_begin + k];
-        const uint32_t* c = done + d.bucket;
-        while (ld_acquire(c) < (uint32_t)d.need) __nanosleep(64);
-      }
+      const int k = S.b.w >= 0 ? S.b.k : 0;
       if (tid < nm) {
         const qtn_member_t m = P.members[S.b.mem_begin + tid];
-        const uint32_t lowmask = (L >= 32) ? 0xffffffffu : ((1u << L) - 1u);
+        const uint32_t lowmask = (1u << L) - 1u;
         S.off[tid] = m.off;
         S.mlo[tid] = (uint32_t)(m.mask & lowmask);
         S.mhi[tid] = m.mask >> L;
+        S.pc[tid] = __popcll(m.mask);
         S.pclo[tid] = __popc((uint32_t)(m.mask & lowmask));
-        S.bstr[tid] = 1ull << __popcll(m.mask);
-        S.seglen[tid] = 1 << S.pclo[tid];
+        for (int q = 0; q < (1 << k); ++q) S.sig[tid][q] = (int16_t)pext32((uint32_t)q, m.smask);
       }
-      __syncthreads();
-      if (tid == 0) {
-        int acc = 0;
-        for (int i = 0; i < nm; ++i) {
-          if (S.pclo[i] == L) {
-            S.seg[i] = -1;
-          } else {
-            S.seg[i] = acc;
-            acc += 2 * S.seglen[i];
-          }
+      for (int d = tid; d < S.b.n_dep; d += NT) {
+        const qtn_dep_t dp = P.deps[S.b.dep_begin + d];
+        const uint32_t* c = done + dp.bucket;
+        int spins = 0;
+        while (ld_acquire(c) < (uint32_t)dp.need) {
+          if (++spins > 64) __nanosleep(32);
         }
       }
-      if (tid < nm * MAXS) {
-        const int i = tid / MAXS, s = tid % MAXS;
-        S.gs[i][s] = (int)pext32((uint32_t)(VEC * NT * s), S.mlo[i]);
-      }
       __syncthreads();
-#pragma unroll
-      for (int i = 0; i < MAXM; ++i) gt[i] = (i < nm) ? (int)pext32((uint32_t)(VEC * tid), S.mlo[i]) : 0;
       prepared = cur;
     }
-
     const int h = tk - S.b.tick_begin;
     unsigned long long t_start = 0;
     if (P.timing && tid == 0) t_start = globaltimer();
-
     if (S.b.w < 0) {
-      // ---- finaliser: product of rank-0 values, in double, member order ----
+      // finaliser: product of rank-0 values, in double, member order
       if (tid == 0) {
         double re = 1.0, im = 0.0;
         for (int i = 0; i < S.b.n_mem; ++i) {
@@ -256,121 +283,424 @@ __global__ void __launch_bounds__(NT) program_kernel(const qtn_program_t P) {
     } else {
       const int nm = S.b.n_mem;
       const int L = S.b.tile_bits;
+      const int ns = 1 << S.b.k;
       const int nelem = 1 << L;
       if (tid < nm) S.base[tid] = S.off[tid] + (pext64((uint64_t)h, S.mhi[tid]) << S.pclo[tid]);
       __syncthreads();
-      // stage partial-coverage members (two contiguous runs each) into smem
-      for (int i = 0; i < nm; ++i) {
-        const int sg = S.seg[i];
-        if (sg < 0) continue;
-        const int len = S.seglen[i];
-        const T* src0 = A + S.base[i];
-        const T* src1 = src0 + S.bstr[i];
-        for (int q = tid; q < 2 * len; q += NT)
-          sseg[sg + q] = __ldcg(q < len ? src0 + q : src1 + (q - len));
-      }
-      __syncthreads();
-      T* out = A + S.b.out_off + (uint64_t)h * (uint64_t)nelem;
-      if (nelem >= VEC * NT) {
-        const int ns = nelem / (VEC * NT);
-        for (int s = 0; s < ns; ++s) {
-          const int e0 = VEC * (tid + NT * s);
-          T p0[VEC], p1[VEC];
-#pragma unroll
-          for (int i = 0; i < MAXM; ++i) {
-            if (i >= nm) break;
-            T x0[VEC], x1[VEC];
-            if (S.seg[i] < 0) {
-              const V* v0 = reinterpret_cast<const V*>(A + S.base[i] + e0);
-              const V* v1 = reinterpret_cast<const V*>(A + S.base[i] + S.bstr[i] + e0);
-              split(__ldcg(v0), x0);
-              split(__ldcg(v1), x1);
-            } else {
-              const int idx = gt[i] + S.gs[i][s];
-              const T* s0 = sseg + S.seg[i];
-              const T* s1 = s0 + S.seglen[i];
-              const int bit0 = (int)(S.mlo[i] & 1u);
-#pragma unroll
-              for (int v = 0; v < VEC; ++v) {
-                x0[v] = s0[idx + (v & bit0)];
-                x1[v] = s1[idx + (v & bit0)];
-              }
-            }
-            if (i == 0) {
-#pragma unroll
-              for (int v = 0; v < VEC; ++v) { p0[v] = x0[v]; p1[v] = x1[v]; }
-            } else {
-#pragma unroll
-              for (int v = 0; v < VEC; ++v) { p0[v] = cmul(p0[v], x0[v]); p1[v] = cmul(p1[v], x1[v]); }
-            }
-          }
-          T r[VEC];
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) r[v] = cadd(p0[v], p1[v]);
-          *reinterpret_cast<V*>(out + e0) = join(r);
-        }
-      } else {
-        for (int e = tid; e < nelem; e += NT) {
-          T p0, p1;
+      T* out = Aw + S.b.out_off + (uint64_t)h * (uint64_t)nelem;
+      // threads cover (element, assignment) pairs, 4 per thread per round with
+      // every member load issued before the multiplies
+      const int chunk = max(1, min(ns, SMALL_PROD_ELEMS / nelem));
+      T acc = T{};
+      for (int s0 = 0; s0 < ns; s0 += chunk) {
+        const int cs = min(chunk, ns - s0);
+        const int nu = cs * nelem;
+        for (int u0 = tid; u0 < nu; u0 += 4 * NT) {
+          T prod[4];
           for (int i = 0; i < nm; ++i) {
-            T x0, x1;
-            if (S.seg[i] < 0) {
-              x0 = __ldcg(A + S.base[i] + e);
-              x1 = __ldcg(A + S.base[i] + S.bstr[i] + e);
-            } else {
-              const int idx = (int)pext32((uint32_t)e, S.mlo[i]);
-              x0 = sseg[S.seg[i] + idx];
-              x1 = sseg[S.seg[i] + S.seglen[i] + idx];
+            T x[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int u = min(u0 + j * NT, nu - 1);
+              const int e = u & (nelem - 1), sc = s0 + (u >> L);
+              const uint64_t o = S.base[i] + ((uint64_t)S.sig[i][sc] << S.pc[i]) +
+                                 (S.pclo[i] == L ? (uint64_t)e : (uint64_t)pext32((uint32_t)e, S.mlo[i]));
+              x[j] = __ldcg(A + o);
             }
-            if (i == 0) {
-              p0 = x0;
-              p1 = x1;
-            } else {
-              p0 = cmul(p0, x0);
-              p1 = cmul(p1, x1);
-            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) prod[j] = (i == 0) ? x[j] : cmul(prod[j], x[j]);
           }
-          out[e] = cadd(p0, p1);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (u0 + j * NT < nu) sprod[u0 + j * NT] = prod[j];
         }
+        __syncthreads();
+        if (tid < nelem)
+          for (int c = 0; c < cs; ++c) acc = (s0 + c == 0) ? sprod[c * nelem + tid] : cadd(acc, sprod[c * nelem + tid]);
+        __syncthreads();
       }
+      if (tid < nelem) out[tid] = acc;
     }
-
-    // ---- publish completion of this tile ----
     __syncthreads();
     if (tid == 0) {
-      __threadfence();
-      atomicAdd(&done[cur], 1u);
+      ++pend_cnt;
+      pend_item = cur;
       if (P.timing) {
         atomicMin(&P.timing[2 * cur], t_start);
         atomicMax(&P.timing[2 * cur + 1], globaltimer());
       }
     }
   }
-
-  // ---- exit: the last block out leaves the control block zeroed ----
+  // exit: publish, then the last block out zeroes the stage's counters
   if (tid == 0) {
-    const unsigned v = atomicAdd(&P.ctrl[1], 1u);
+    if (pend_cnt) {
+      __threadfence();
+      atomicAdd(&done[pend_item], pend_cnt);
+    }
+    const unsigned v = atomicAdd(&ctl[1], 1u);
     S.last = (v == gridDim.x - 1) ? 1 : 0;
   }
   __syncthreads();
   if (S.last) {
     __threadfence();
-    for (int i = tid; i < P.n_buckets; i += NT) done[i] = 0u;
+    for (int i = first + tid; i < first + count; i += NT) done[i] = 0u;
     if (tid == 0) {
-      P.ctrl[0] = 0u;
-      P.ctrl[1] = 0u;
+      ctl[0] = 0u;
+      ctl[1] = 0u;
     }
   }
 }
 
+// =========================================================================
+// K1: large-item kernels
+// =========================================================================
+struct LargeCtx {
+  qtn_bucket_t b;
+  uint64_t off[MAXM];
+  uint64_t mhi[MAXM];
+  uint64_t base[MAXM];
+  uint32_t mlo[MAXM];
+  int32_t cls[MAXM];
+  int32_t pc[MAXM];
+  int32_t pclo[MAXM];
+  int32_t nsig[MAXM];
+  int32_t seglen[MAXM];
+  int32_t seg[MAXM];       // smem element offset of the staged runs, -1 if not staged
+  int32_t vlist[MAXM];     // varying members (compile-time count NV)
+  int16_t sig[MAXM][MAXNS];
+  int32_t gs[MAXM][MAXS];  // pext(est[st], mlo)
+  int32_t gt[MAXM][NT];    // pext(eth[tid], mlo)
+  int32_t eth[NT];         // tile offset of the thread's first result
+  int32_t est[MAXS];       // tile offset of step st
+  int32_t s0m;             // the streamed member (ST == 1)
+  int32_t uoff;            // smem offset of U[s] (tile-uniform product)
+  int32_t has_u;
+  int32_t nbulk;
+};
+
+// Per-block preparation of a large item: member tables, smem layout, thread
+// mapping (v -> bit 0 for c64, lane -> the next 5 bits for coalesced warp
+// stores, warp and step bits -> the rest; step bits = the item's stmask).
+template <typename R>
+__device__ __forceinline__ void large_prep(LargeCtx& S, const qtn_program_t& P, int item) {
+  using T = typename Cx<R>::T;
+  constexpr int VEC = Cx<R>::VEC;
+  constexpr int EPV = 16 / (int)sizeof(T);
+  const int tid = threadIdx.x;
+  if (tid == 0) S.b = P.buckets[item];
+  __syncthreads();
+  const int nm = S.b.n_mem;
+  const int L = S.b.tile_bits;
+  const int k = S.b.k;
+  if (tid < nm) {
+    const qtn_member_t m = P.members[S.b.mem_begin + tid];
+    const uint32_t lowmask = (1u << L) - 1u;
+    S.off[tid] = m.off;
+    S.mlo[tid] = (uint32_t)(m.mask & lowmask);
+    S.mhi[tid] = m.mask >> L;
+    S.pc[tid] = __popcll(m.mask);
+    S.pclo[tid] = __popc((uint32_t)(m.mask & lowmask));
+    S.nsig[tid] = 1 << __popc(m.smask);
+    S.seglen[tid] = 1 << S.pclo[tid];
+    S.cls[tid] = (int)m.cls;
+    for (int q = 0; q < (1 << k); ++q) S.sig[tid][q] = (int16_t)pext32((uint32_t)q, m.smask);
+  }
+  {
+    constexpr int LB = (VEC == 2) ? 1 : 0;
+    const uint32_t hi = ((1u << L) - 1u) & ~((1u << (LB + 5)) - 1u);
+    uint32_t stm = S.b.stmask & hi;
+    if (__popc(stm) != L - LB - 8) stm = hi & ~((1u << (LB + 8)) - 1u);
+    const uint32_t wm = hi & ~stm;
+    S.eth[tid] = (int)(((uint32_t)(tid & 31) << LB) | pdep32((uint32_t)(tid >> 5), wm));
+    if (tid < MAXS) S.est[tid] = (int)pdep32((uint32_t)tid, stm);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int acc = 0, nv = 0, sm = -1, hu = 0, nb = 0;
+    for (int i = 0; i < nm; ++i) {
+      const int c = S.cls[i];
+      if (c == QTN_CLS_STREAMED) {
+        S.seg[i] = -1;
+        if (sm < 0) sm = i;
+      } else {
+        S.seg[i] = acc;
+        acc += S.nsig[i] * S.seglen[i];
+        acc = (acc + EPV - 1) & ~(EPV - 1);   // 16-byte aligned runs (bulk copies)
+        if (S.seglen[i] * (int)sizeof(T) >= 16) nb += S.nsig[i];
+      }
+      if (c == QTN_CLS_UNIFORM) hu = 1;
+      if (c == QTN_CLS_VARYING) S.vlist[nv++] = i;
+    }
+    S.s0m = sm;
+    S.has_u = hu;
+    S.uoff = acc;
+    S.nbulk = nb;
+  }
+  __syncthreads();
+  if (tid < nm * MAXS) {
+    const int i = tid / MAXS, st = tid % MAXS;
+    S.gs[i][st] = (int)pext32((uint32_t)S.est[st], S.mlo[i]);
+  }
+  for (int i = 0; i < nm; ++i) S.gt[i][tid] = (int)pext32((uint32_t)S.eth[tid], S.mlo[i]);
+  __syncthreads();
+}
+
+// Stage the non-streamed members of tile h: each run of >= 16 bytes is one
+// bulk async copy completing on `bar`; shorter runs are plain loads.  Then
+// U[s] = product of the tile-uniform members.
+template <typename R>
+__device__ __forceinline__ void large_stage(LargeCtx& S, const typename Cx<R>::T* A, typename Cx<R>::T* sseg,
+                                            uint64_t* bar, uint32_t& phase, int h) {
+  using T = typename Cx<R>::T;
+  const int tid = threadIdx.x;
+  const int nm = S.b.n_mem;
+  const int ns = 1 << S.b.k;
+  if (tid < nm) S.base[tid] = S.off[tid] + (pext64((uint64_t)h, S.mhi[tid]) << S.pclo[tid]);
+  __syncthreads();
+  if (tid == 0 && S.nbulk) {
+    uint32_t bytes = 0;
+    fence_proxy_async();   // order acquired generic-proxy data before async-proxy reads
+    for (int i = 0; i < nm; ++i) {
+      if (S.seg[i] < 0) continue;
+      const uint32_t rb = (uint32_t)S.seglen[i] * (uint32_t)sizeof(T);
+      if (rb < 16) continue;
+      const T* src = A + S.base[i];
+      for (int r = 0; r < S.nsig[i]; ++r) {
+        bulk_g2s(sseg + S.seg[i] + r * S.seglen[i], src + ((uint64_t)r << S.pc[i]), rb, bar);
+        bytes += rb;
+      }
+    }
+    mbar_arrive_expect_tx(bar, bytes);
+  }
+  for (int i = 0; i < nm; ++i) {
+    if (S.seg[i] < 0 || S.seglen[i] * (int)sizeof(T) >= 16) continue;
+    const T* src = A + S.base[i];
+    for (int q = tid; q < S.nsig[i]; q += NT) sseg[S.seg[i] + q] = __ldcg(src + ((uint64_t)q << S.pc[i]));
+  }
+  if (S.nbulk) {
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+  }
+  __syncthreads();
+  if (S.has_u && tid < ns) {
+    T u = T{};
+    bool first = true;
+    for (int i = 0; i < nm; ++i) {
+      if (S.cls[i] != QTN_CLS_UNIFORM) continue;
+      const T x = sseg[S.seg[i] + S.sig[i][tid]];
+      u = first ? x : cmul(u, x);
+      first = false;
+    }
+    sseg[S.uoff + tid] = u;
+  }
+  __syncthreads();
+}
+
+// Compute tile h (after large_stage): fully unrolled over the NS summed
+// assignments and the NV varying members; per-thread smem addresses and run
+// offsets live in registers.
+template <typename R, int NS, int NV, int ST>
+__device__ __forceinline__ void large_compute(const LargeCtx& S, const typename Cx<R>::T* __restrict__ A,
+                                              const typename Cx<R>::T* sseg, typename Cx<R>::T* out) {
+  using T = typename Cx<R>::T;
+  using V = typename Cx<R>::V;
+  constexpr int VEC = Cx<R>::VEC;
+  const int tid = threadIdx.x;
+  const int nm = S.b.n_mem;
+  const int nst = (1 << S.b.tile_bits) / (VEC * NT);
+  const T* qv[NV > 0 ? NV : 1];
+  int ro[NV > 0 ? NV : 1][NS];
+  int b0[NV > 0 ? NV : 1];
+  int vi[NV > 0 ? NV : 1];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int i = S.vlist[j];
+    vi[j] = i;
+    qv[j] = sseg + S.seg[i] + S.gt[i][tid];
+    b0[j] = (int)(S.mlo[i] & 1u);
+#pragma unroll
+    for (int c = 0; c < NS; ++c) ro[j][c] = S.sig[i][c] << S.pclo[i];
+  }
+  const T* sp = nullptr;
+  int64_t sro[NS];
+  if (ST) {
+    const int sm = S.s0m;
+    sp = A + S.base[sm] + S.eth[tid];
+#pragma unroll
+    for (int c = 0; c < NS; ++c) sro[c] = (int64_t)S.sig[sm][c] << S.pc[sm];
+  }
+  // thread-invariant members (k == 1): P[s] once per tile
+  T P[NS][VEC];
+  bool haveP = false;
+  if (NS == 2) {
+    for (int i = 0; i < nm; ++i) {
+      if (S.cls[i] != QTN_CLS_INVARIANT) continue;
+      const T* q = sseg + S.seg[i] + S.gt[i][tid];
+      const int bb = (int)(S.mlo[i] & 1u);
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        const T* qc = q + (S.sig[i][c] << S.pclo[i]);
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          const T x = qc[v & bb];
+          P[c][v] = haveP ? cmul(P[c][v], x) : x;
+        }
+      }
+      haveP = true;
+    }
+  }
+  const bool hu = S.has_u;
+  T U[NS];
+#pragma unroll
+  for (int c = 0; c < NS; ++c) U[c] = hu ? sseg[S.uoff + c] : T{};
+  for (int st = 0; st < nst; ++st) {
+    const int est = S.est[st];
+    T prod[NS][VEC];
+    bool started = false;
+    if (ST) {
+#pragma unroll
+      for (int c = 0; c < NS; ++c) split(__ldcg(reinterpret_cast<const V*>(sp + est + sro[c])), prod[c]);
+      started = true;
+    }
+    if (hu) {
+#pragma unroll
+      for (int c = 0; c < NS; ++c)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) prod[c][v] = started ? cmul(prod[c][v], U[c]) : U[c];
+      started = true;
+    }
+    if (NS == 2 && haveP) {
+#pragma unroll
+      for (int c = 0; c < NS; ++c)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) prod[c][v] = started ? cmul(prod[c][v], P[c][v]) : P[c][v];
+      started = true;
+    }
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const T* q = qv[j] + S.gs[vi[j]][st];
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        T x[VEC];
+        if (VEC == 2) {
+          if (b0[j]) {
+            split(*reinterpret_cast<const V*>(q + ro[j][c]), x);
+          } else {
+            x[0] = q[ro[j][c]];
+            x[VEC - 1] = x[0];
+          }
+        } else {
+          x[0] = q[ro[j][c]];
+        }
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) prod[c][v] = started ? cmul(prod[c][v], x[v]) : x[v];
+      }
+      started = true;
+    }
+    T acc[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      acc[v] = prod[0][v];
+#pragma unroll
+      for (int c = 1; c < NS; ++c) acc[v] = cadd(acc[v], prod[c][v]);
+    }
+    *reinterpret_cast<V*>(out + S.eth[tid] + est) = join(acc);
+  }
+}
+
+// Generic compute (any k, any member mix): summed assignments in chunks of 2,
+// member parameters read from the block tables.
+template <typename R>
+__device__ __forceinline__ void large_compute_generic(const LargeCtx& S, const typename Cx<R>::T* __restrict__ A,
+                                                      const typename Cx<R>::T* sseg, typename Cx<R>::T* out) {
+  using T = typename Cx<R>::T;
+  using V = typename Cx<R>::V;
+  constexpr int VEC = Cx<R>::VEC;
+  constexpr int SC = 2;
+  const int tid = threadIdx.x;
+  const int nm = S.b.n_mem;
+  const int ns = 1 << S.b.k;
+  const int nst = (1 << S.b.tile_bits) / (VEC * NT);
+  for (int st = 0; st < nst; ++st) {
+    const int e0 = S.eth[tid] + S.est[st];
+    T acc[VEC];
+    for (int s0 = 0; s0 < ns; s0 += SC) {
+      T prod[SC][VEC];
+      for (int i = 0; i < nm; ++i) {
+        T x[SC][VEC];
+        if (S.seg[i] < 0) {
+          const T* q = A + S.base[i] + e0;
+#pragma unroll
+          for (int c = 0; c < SC; ++c)
+            split(__ldcg(reinterpret_cast<const V*>(q + ((int64_t)S.sig[i][s0 + c] << S.pc[i]))), x[c]);
+        } else {
+          const T* q = sseg + S.seg[i] + S.gt[i][tid] + S.gs[i][st];
+          const int bit0 = (int)(S.mlo[i] & 1u);
+#pragma unroll
+          for (int c = 0; c < SC; ++c) {
+            const T* qc = q + (S.sig[i][s0 + c] << S.pclo[i]);
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) x[c][v] = qc[v & bit0];
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < SC; ++c)
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) prod[c][v] = (i == 0) ? x[c][v] : cmul(prod[c][v], x[c][v]);
+      }
+#pragma unroll
+      for (int c = 0; c < SC; ++c)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[v] = (s0 + c == 0) ? prod[c][v] : cadd(acc[v], prod[c][v]);
+    }
+    *reinterpret_cast<V*>(out + e0) = join(acc);
+  }
+}
+
+// NS < 0: generic compute.
+template <typename R, int NS, int NV, int ST>
+__global__ void __launch_bounds__(NT) large_kernel(const qtn_program_t P, int32_t item) {
+  using T = typename Cx<R>::T;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sseg = reinterpret_cast<T*>(smem_raw);
+  __shared__ LargeCtx S;
+  __shared__ uint64_t bar;
+  const T* A = reinterpret_cast<const T*>(P.arena);
+  T* Aw = reinterpret_cast<T*>(P.arena);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  large_prep<R>(S, P, item);
+  unsigned long long t_start = 0;
+  if (P.timing && tid == 0) t_start = globaltimer();
+  uint32_t phase = 0;
+  const int ntiles = S.b.n_tiles;
+  const uint64_t nelem = 1ull << S.b.tile_bits;
+  for (int h = blockIdx.x; h < ntiles; h += gridDim.x) {
+    large_stage<R>(S, A, sseg, &bar, phase, h);
+    T* out = Aw + S.b.out_off + (uint64_t)h * nelem;
+    if (NS > 0)
+      large_compute<R, (NS > 0 ? NS : 2), NV, ST>(S, A, sseg, out);
+    else
+      large_compute_generic<R>(S, A, sseg, out);
+    __syncthreads();
+  }
+  if (P.timing && tid == 0) {
+    atomicMin(&P.timing[2 * item], t_start);
+    atomicMax(&P.timing[2 * item + 1], globaltimer());
+  }
+}
+
+// ---- permutation (tensors entering a program in a non-canonical layout) ----
 struct PermStrides {
   int64_t s[QTN_MAX_WIDTH + 4];
 };
 
 template <typename RS, typename RD>
 __global__ void permute_kernel(const typename Cx<RS>::T* __restrict__ src, int64_t src_off,
-                               typename Cx<RD>::T* __restrict__ dst, int rank, PermStrides st,
-                               uint64_t n) {
+                               typename Cx<RD>::T* __restrict__ dst, int rank, PermStrides st, uint64_t n) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride) {
     int64_t o = src_off;
@@ -383,41 +713,114 @@ __global__ void permute_kernel(const typename Cx<RS>::T* __restrict__ src, int64
   }
 }
 
+// =========================================================================
+// host side: kernel selection, launch configuration, graphs
+// =========================================================================
+using LargeFn = void (*)(const qtn_program_t, int32_t);
+
 template <typename R>
-int configure_program(int smem) {
-  const cudaError_t e = cudaFuncSetAttribute(program_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return cuda_err(e, "cudaFuncSetAttribute(program_kernel)");
+LargeFn large_fn(int variant) {
+  if (variant < 0) return large_kernel<R, -1, 0, 0>;
+  const int ks = variant & 15, nv = (variant >> 4) & 15, st = (variant >> 8) & 1;
+#define QTN_NV_CASES(NS, ST)                   \
+  switch (nv) {                                \
+    case 0: return large_kernel<R, NS, 0, ST>; \
+    case 1: return large_kernel<R, NS, 1, ST>; \
+    case 2: return large_kernel<R, NS, 2, ST>; \
+    case 3: return large_kernel<R, NS, 3, ST>; \
+    case 4: return large_kernel<R, NS, 4, ST>; \
+    default: return large_kernel<R, -1, 0, 0>; \
+  }
+  if (ks == 1) {
+    if (st) { QTN_NV_CASES(2, 1) } else { QTN_NV_CASES(2, 0) }
+  } else if (ks == 2) {
+    if (st) { QTN_NV_CASES(4, 1) } else { QTN_NV_CASES(4, 0) }
+  } else if (ks == 3) {
+    if (st) { QTN_NV_CASES(8, 1) } else { QTN_NV_CASES(8, 0) }
+  }
+#undef QTN_NV_CASES
+  return large_kernel<R, -1, 0, 0>;
+}
+
+int sm_count() {
+  int dev = 0, nsm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
+  return nsm;
+}
+
+int resident_grid(const void* fn, int smem, int* grid) {
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return cuda_err(e, "cudaFuncSetAttribute");
+  int nb = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, NT, smem);
+  if (e != cudaSuccess) return cuda_err(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+  if (nb < 1) return set_err(QTN_E_UNSUPPORTED, "kernel cannot be resident with %d B smem", smem);
+  *grid = nb * sm_count();
   return QTN_OK;
 }
 
-template <typename R>
-int grid_for(int smem, int* grid) {
-  int dev = 0, nsm = 0, nb = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return cuda_err(e, "cudaGetDevice");
-  e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  if (e != cudaSuccess) return cuda_err(e, "cudaDeviceGetAttribute");
-  int rc = configure_program<R>(smem);
-  if (rc) return rc;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, program_kernel<R>, NT, smem);
-  if (e != cudaSuccess) return cuda_err(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
-  if (nb < 1) return set_err(QTN_E_UNSUPPORTED, "program kernel cannot be resident with %d B smem", smem);
-  *grid = nb * nsm;
-  return QTN_OK;
-}
+struct LaunchSpec {
+  const void* fn;
+  int grid;
+  int smem;
+  void* args[5];
+  // storage for the arguments (the graph copies them at node creation)
+  qtn_program_t prog;
+  int32_t a0, a1, a2;
+  uint32_t* ctl;
+};
 
 int check_program(const qtn_program_t* p) {
   if (!p) return set_err(QTN_E_INVALID, "null program");
   if (p->dtype != QTN_C64 && p->dtype != QTN_C128) return set_err(QTN_E_INVALID, "bad dtype %d", p->dtype);
-  if (p->n_buckets < 0 || p->n_tickets < 0) return set_err(QTN_E_INVALID, "negative sizes");
-  // arena may be NULL: member/result offsets are then absolute addresses / element size
+  if (p->n_buckets < 0 || p->n_nodes < 0) return set_err(QTN_E_INVALID, "negative sizes");
   if (p->n_buckets > 0 && (!p->buckets || !p->tick_begin || !p->ctrl))
     return set_err(QTN_E_INVALID, "null device table");
-  if (p->smem_bytes < 0 || p->smem_bytes > 227 * 1024) return set_err(QTN_E_INVALID, "smem_bytes %d", p->smem_bytes);
+  return QTN_OK;
+}
+
+// Fill the launch of node `ni` (n_tiles: tiles of a LARGE node's item).
+int make_launch(const qtn_program_t* p, const qtn_node_t* nd, int ni, int32_t n_tiles, LaunchSpec* L) {
+  L->prog = *p;
+  L->smem = nd->smem_bytes;
+  if (L->smem < 0 || L->smem > 227 * 1024) return set_err(QTN_E_INVALID, "node smem %d", L->smem);
+  int rc;
+  if (nd->kind == QTN_NODE_SMALL) {
+    L->fn = p->dtype == QTN_C64 ? (const void*)small_kernel<float> : (const void*)small_kernel<double>;
+    rc = resident_grid(L->fn, L->smem, &L->grid);
+    if (rc) return rc;
+    if (nd->n_tickets < L->grid) L->grid = nd->n_tickets > 0 ? nd->n_tickets : 1;
+    L->a0 = nd->first;
+    L->a1 = nd->count;
+    L->a2 = nd->n_tickets;
+    L->ctl = p->ctrl + 2 * ni;
+    L->args[0] = &L->prog;
+    L->args[1] = &L->a0;
+    L->args[2] = &L->a1;
+    L->args[3] = &L->a2;
+    L->args[4] = &L->ctl;
+  } else if (nd->kind == QTN_NODE_LARGE) {
+    L->fn = p->dtype == QTN_C64 ? (const void*)large_fn<float>(nd->variant)
+                                : (const void*)large_fn<double>(nd->variant);
+    rc = resident_grid(L->fn, L->smem, &L->grid);
+    if (rc) return rc;
+    if (n_tiles < L->grid) L->grid = n_tiles > 0 ? n_tiles : 1;
+    L->a0 = nd->first;
+    L->args[0] = &L->prog;
+    L->args[1] = &L->a0;
+  } else {
+    return set_err(QTN_E_INVALID, "bad node kind %d", nd->kind);
+  }
   return QTN_OK;
 }
 
 }  // namespace
+
+struct qtn_graph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
 
 extern "C" {
 
@@ -436,47 +839,113 @@ int qtn_device_count(int* count) {
   return QTN_OK;
 }
 
-int qtn_program_grid(int32_t dtype, int32_t smem_bytes, int32_t* grid_out) {
-  if (!grid_out) return set_err(QTN_E_INVALID, "null grid_out");
-  int g = 0;
-  const int rc = dtype == QTN_C64 ? grid_for<float>(smem_bytes, &g) : grid_for<double>(smem_bytes, &g);
-  if (rc) return rc;
-  *grid_out = g;
-  return QTN_OK;
-}
-
 int qtn_program_reset(const qtn_program_t* p, void* stream) {
   int rc = check_program(p);
   if (rc) return rc;
-  const cudaError_t e = cudaMemsetAsync(p->ctrl, 0, sizeof(uint32_t) * (2 + (size_t)p->n_buckets),
-                                        (cudaStream_t)stream);
+  const size_t words = 2 * (size_t)p->n_nodes + (size_t)p->n_buckets;
+  const cudaError_t e = cudaMemsetAsync(p->ctrl, 0, sizeof(uint32_t) * words, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_err(e, "cudaMemsetAsync(ctrl)");
   return QTN_OK;
 }
 
-int qtn_program_launch(const qtn_program_t* p, void* stream) {
+int qtn_node_launch(const qtn_program_t* p, const qtn_node_t* nd, int32_t ni, void* stream) {
   int rc = check_program(p);
   if (rc) return rc;
-  if (p->n_tickets == 0) return QTN_OK;
-  int grid = p->grid;
-  if (grid <= 0) {
-    rc = qtn_program_grid(p->dtype, p->smem_bytes, &grid);
-    if (rc) return rc;
-  } else {
-    rc = p->dtype == QTN_C64 ? configure_program<float>(p->smem_bytes) : configure_program<double>(p->smem_bytes);
-    if (rc) return rc;
+  if (!nd) return set_err(QTN_E_INVALID, "null node");
+  int32_t tiles = 0;
+  if (nd->kind == QTN_NODE_LARGE) {
+    if (nd->first < 0 || nd->first >= p->n_buckets) return set_err(QTN_E_INVALID, "item %d out of range", nd->first);
+    qtn_bucket_t b;
+    const cudaError_t e = cudaMemcpy(&b, p->buckets + nd->first, sizeof(b), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_err(e, "cudaMemcpy(item)");
+    tiles = b.n_tiles;
   }
-  if (p->dtype == QTN_C64)
-    program_kernel<float><<<grid, NT, p->smem_bytes, (cudaStream_t)stream>>>(*p);
-  else
-    program_kernel<double><<<grid, NT, p->smem_bytes, (cudaStream_t)stream>>>(*p);
-  const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_err(e, "program_kernel launch");
+  LaunchSpec L;
+  rc = make_launch(p, nd, ni, tiles, &L);
+  if (rc) return rc;
+  const cudaError_t e = cudaLaunchKernel(L.fn, dim3(L.grid), dim3(NT), L.args, L.smem, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_err(e, "cudaLaunchKernel");
   return QTN_OK;
 }
 
-int qtn_permute(int32_t src_dtype, const void* src, int64_t src_offset, int32_t dst_dtype, void* dst,
-                int32_t rank, const int64_t* src_strides, void* stream) {
+int qtn_graph_create(const qtn_program_t* p, const qtn_node_t* nodes, int32_t n_nodes, const int32_t* node_deps,
+                     qtn_graph_t** out) {
+  int rc = check_program(p);
+  if (rc) return rc;
+  if (!out || (n_nodes > 0 && !nodes)) return set_err(QTN_E_INVALID, "null argument");
+  std::vector<qtn_bucket_t> items(p->n_buckets);
+  if (p->n_buckets) {
+    const cudaError_t e =
+        cudaMemcpy(items.data(), p->buckets, sizeof(qtn_bucket_t) * items.size(), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_err(e, "cudaMemcpy(items)");
+  }
+  qtn_graph* g = new qtn_graph();
+  cudaError_t e = cudaGraphCreate(&g->graph, 0);
+  if (e != cudaSuccess) {
+    delete g;
+    return cuda_err(e, "cudaGraphCreate");
+  }
+  std::vector<cudaGraphNode_t> gn(n_nodes);
+  std::vector<LaunchSpec> specs(n_nodes);
+  for (int i = 0; i < n_nodes; ++i) {
+    const qtn_node_t& nd = nodes[i];
+    if (nd.kind == QTN_NODE_LARGE && (nd.first < 0 || nd.first >= p->n_buckets)) {
+      qtn_graph_destroy(g);
+      return set_err(QTN_E_INVALID, "node %d: item %d out of range", i, nd.first);
+    }
+    const int32_t tiles = nd.kind == QTN_NODE_LARGE ? items[nd.first].n_tiles : 0;
+    rc = make_launch(p, &nd, i, tiles, &specs[i]);
+    if (rc) {
+      qtn_graph_destroy(g);
+      return rc;
+    }
+    std::vector<cudaGraphNode_t> deps;
+    for (int d = 0; d < nd.n_dep; ++d) {
+      const int j = node_deps[nd.dep_begin + d];
+      if (j < 0 || j >= i) {
+        qtn_graph_destroy(g);
+        return set_err(QTN_E_INVALID, "node %d: dependency %d is not an earlier node", i, j);
+      }
+      deps.push_back(gn[j]);
+    }
+    cudaKernelNodeParams kp = {};
+    kp.func = const_cast<void*>(specs[i].fn);
+    kp.gridDim = dim3(specs[i].grid);
+    kp.blockDim = dim3(NT);
+    kp.sharedMemBytes = specs[i].smem;
+    kp.kernelParams = specs[i].args;
+    e = cudaGraphAddKernelNode(&gn[i], g->graph, deps.empty() ? nullptr : deps.data(), deps.size(), &kp);
+    if (e != cudaSuccess) {
+      qtn_graph_destroy(g);
+      return cuda_err(e, "cudaGraphAddKernelNode");
+    }
+  }
+  e = cudaGraphInstantiate(&g->exec, g->graph, 0);
+  if (e != cudaSuccess) {
+    qtn_graph_destroy(g);
+    return cuda_err(e, "cudaGraphInstantiate");
+  }
+  *out = g;
+  return QTN_OK;
+}
+
+int qtn_graph_launch(qtn_graph_t* g, void* stream) {
+  if (!g || !g->exec) return set_err(QTN_E_INVALID, "null graph");
+  const cudaError_t e = cudaGraphLaunch(g->exec, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_err(e, "cudaGraphLaunch");
+  return QTN_OK;
+}
+
+int qtn_graph_destroy(qtn_graph_t* g) {
+  if (!g) return QTN_OK;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  delete g;
+  return QTN_OK;
+}
+
+int qtn_permute(int32_t src_dtype, const void* src, int64_t src_offset, int32_t dst_dtype, void* dst, int32_t rank,
+                const int64_t* src_strides, void* stream) {
   if (!src || !dst) return set_err(QTN_E_INVALID, "null tensor");
   if (rank < 0 || rank > QTN_MAX_WIDTH) return set_err(QTN_E_UNSUPPORTED, "rank %d", rank);
   if (rank > 0 && !src_strides) return set_err(QTN_E_INVALID, "null strides");
@@ -486,7 +955,7 @@ int qtn_permute(int32_t src_dtype, const void* src, int64_t src_offset, int32_t 
   for (int j = 0; j < rank; ++j) st.s[j] = src_strides[j];
   const uint64_t n = 1ull << rank;
   const int threads = 256;
-  uint64_t blocks64 = (n + threads - 1) / threads;
+  const uint64_t blocks64 = (n + threads - 1) / threads;
   const int blocks = (int)(blocks64 > 148ull * 32 ? 148 * 32 : blocks64);
   cudaStream_t s = (cudaStream_t)stream;
   if (src_dtype == QTN_C128 && dst_dtype == QTN_C128)

@@ -25,7 +25,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import engine as E
-from .tensor_core import Backend, BucketStats, memory_estimate
+from .tensor_core import Backend, memory_estimate
 
 
 @dataclass
@@ -119,17 +119,13 @@ def run_local(plan: UnitPlan, mine, backend: Backend, device: int, budget_bytes=
         res = ex.run([plan.raws[plan.units[u].cone] for u in batch])
         if be.profile:
             t0, t1 = ex.fetch_timing()
+        from .ordering import ref_stats
         for k, u in enumerate(batch):
             vals[u] = complex(res[k])
             ci = plan.units[u].cone
             tm = plan.templates[ci]
-            if be.profile:
-                g = prog.bucket_gid[k]
-                el = np.maximum(t1[g] - t0[g], 0)
-            else:
-                el = np.zeros(len(tm.w), np.int64)
-            stats.setdefault(ci, []).extend(
-                BucketStats(int(w), int(e), be.route(int(w))) for w, e in zip(tm.w, el))
+            el = np.maximum(t1[prog.bucket_gid[k]] - t0[prog.bucket_gid[k]], 0) if be.profile else None
+            stats.setdefault(ci, []).extend(ref_stats(tm, be, el))
     return vals, stats
 
 

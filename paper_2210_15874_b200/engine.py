@@ -16,9 +16,10 @@ then executed by ONE launch of the persistent sm_100a kernel
   arena = [ input region | intermediate region ]   (one torch allocation)
 
 Every tensor is stored in the *canonical* layout: axes sorted by elimination
-position, the earliest-eliminated axis slowest.  A member of bucket x then
-has x as its slowest axis and its remaining axes in the order of the
-bucket's result axes, so its element offset is  b * 2^popc(mask) + pext(r, mask).
+position, the earliest-eliminated axis slowest.  A device item sums k >= 1
+indices (a chain of reference buckets merged by the cost model below); its
+summed indices are eliminated before all of its result indices, so each
+member's element offset is  (pext(s, smask) << popc(mask)) + pext(r, mask).
 
 Many instances (lightcones, slices) can share one program; each instance
 ends with a finaliser item that writes its scalar to a result slot.
@@ -26,6 +27,7 @@ ends with a finaliser item that writes its scalar to a result slot.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -60,49 +62,178 @@ def _tensor_align(size):
     return max(1, min(size, 32))
 
 
+KMAX = N.MAX_SUMMED
+SMALL_PROD_ELEMS = 1024   # smem products per round of a small tile (csrc)
+VEC = {"complex64": 2, "complex128": 1}
+# merge cost model (seconds), calibrated on the r01 per-bucket B200 timeline:
+# a dependency hop costs ~3 us of latency; streaming ~5.5 TB/s; one block
+# evaluates ~2.5e9 member-terms/s when every SM is shared by ~5 blocks; a
+# small-tile thread is L2-latency bound (~40 ns per dependent member load).
+HOP_S = 5.0e-6
+BW_BPS = 5.5e12
+BLOCK_TERMS_PS = {"complex64": 2.5e9, "complex128": 1.2e9}
+RESIDENT_BLOCKS = {"complex64": 296, "complex128": 296}
+SMALL_LOAD_S = 40e-9
+MIN_TILE_BITS = {"complex64": 9, "complex128": 8}   # vector path needs VEC*NT results
+# QTN_MERGE=0 disables chain merging (A/B measurements)
+MERGE_DEFAULT = os.environ.get("QTN_MERGE", "1") != "0"
+
+
 @dataclass
 class Template:
     """Symbolic plan of one network structure + order (+ sliced indices).
 
-    Offsets are relative to the instance's input / intermediate bases."""
+    Two levels: the reference buckets of the replay (one per non-empty
+    index in the order, for stats and algorithmic bytes) and the device
+    items — chains of reference buckets merged by the cost model, each
+    summing k indices.  Offsets are relative to the instance's input /
+    intermediate bases."""
     n_in_elems: int
     n_inter_elems: int
-    # per bucket (elimination order of non-empty buckets)
+    # device items (a topological order)
     w: np.ndarray            # result width
+    k: np.ndarray            # summed indices
     L: np.ndarray            # tile bits
     level: np.ndarray
     out_off: np.ndarray      # relative to intermediate base
     mem_ptr: np.ndarray      # CSR into mem_* arrays
-    mem_kind: np.ndarray     # 0 = input tensor, 1 = bucket result
-    mem_ref: np.ndarray      # input tensor id or bucket id
+    mem_kind: np.ndarray     # 0 = input tensor, 1 = item result
+    mem_ref: np.ndarray      # input tensor id or item id
     mem_mask: np.ndarray     # uint64 result-axis coverage
+    mem_smask: np.ndarray    # summed-axis coverage
     smem_elems: np.ndarray
-    step: np.ndarray         # position in the active order (for stats)
-    bucket_index: np.ndarray # eliminated index id
+    stmask: np.ndarray       # per-thread sequential tile bits (vector path)
+    mem_cls: np.ndarray      # member class (CLS_*) for the large-item kernels
+    variant: np.ndarray      # kernel variant per item (VARIANT_SMALL = K2 stage)
+    # reference buckets (elimination order of non-empty buckets)
+    ref_w: np.ndarray
+    ref_item: np.ndarray     # item that computes it
+    ref_last: np.ndarray     # 1 if it is its item's final bucket
+    ref_elems: np.ndarray    # algorithmic elements (sum of member sizes + output)
+    bucket_index: np.ndarray
     # finaliser (rank-0 values in reference multiplication order)
     fin_kind: np.ndarray
     fin_ref: np.ndarray
     # inputs
-    in_off: np.ndarray       # per input tensor: relative arena offset (-1 never)
+    in_off: np.ndarray       # per input tensor: relative arena offset
     gdst: np.ndarray         # canonical element -> relative input offset
     gsrc: np.ndarray         # ... -> element of the raw concatenated source data
     gfix: dict               # fixed index id -> per-element source offset weight
-    n_raw: int               # elements of the raw concatenation
+    n_raw: int
     max_width: int
 
+    @property
+    def n_items(self):
+        return len(self.w)
 
-def plan_template(index_sets, order, dtype, fixed=()):
+
+def _popc(x):
+    return bin(x).count("1")
+
+
+def _tile_bits(w, masks, smasks, dtype):
+    """Largest L <= TILE_BITS whose staged runs fit the smem budget."""
+    esz = ELEM_BYTES[dtype]
+    L = min(w, TILE_BITS[dtype])
+    while True:
+        low = (1 << L) - 1
+        st = sum(((1 << _popc(sm)) << _popc(m & low)) + 1 for m, sm in zip(masks, smasks) if (m & low) != low)
+        st += 1 << KMAX   # U[s] (tile-uniform product)
+        if st * esz <= SMEM_BUDGET or L == 0:
+            return L, st
+        L -= 1
+
+
+def _step_mask(L, masks, dtype):
+    """Tile bits each thread walks sequentially (vector path): among the bits
+    above lane + warp-minimum positions choose the subset that leaves the most
+    partially-covering (staged) members invariant, so they are multiplied
+    once per tile (csrc vec_tile_hoist)."""
+    lb = 1 if VEC[dtype] == 2 else 0
+    n_st = L - lb - 8
+    if n_st <= 0:
+        return 0
+    full = (1 << L) - 1
+    staged = [m & full for m in masks if (m & full) != full]
+    best, best_key = 0, None
+    from itertools import combinations
+    for bits in combinations(range(lb + 5, L), n_st):
+        sm = sum(1 << b for b in bits)
+        inv = sum(1 for m in staged if (m & sm) == 0)
+        key = (inv, sm)           # ties: prefer the higher bits
+        if best_key is None or key > best_key:
+            best, best_key = sm, key
+    return best
+
+
+CLS_STREAMED, CLS_UNIFORM, CLS_INVARIANT, CLS_VARYING = 0, 1, 2, 3
+VARIANT_SMALL = -2
+VARIANT_GENERIC = N.QTN_VARIANT_GENERIC
+
+
+def member_classes(w, k, L, stm, masks):
+    """Per-member class for the large-item kernels (csrc large_kernel)."""
+    full = (1 << L) - 1
+    out = []
+    for m in masks:
+        lo = m & full
+        if lo == full:
+            out.append(CLS_STREAMED)
+        elif lo == 0:
+            out.append(CLS_UNIFORM)
+        elif k == 1 and (lo & stm) == 0:
+            out.append(CLS_INVARIANT)
+        else:
+            out.append(CLS_VARYING)
+    return out
+
+
+def kernel_variant(w, k, L, cls, dtype):
+    """K2 small stage for tiles below one vector step; otherwise the K1
+    specialisation (2^k, varying members, streamed) or the generic kernel."""
+    if (1 << L) < VEC[dtype] * NT:
+        return VARIANT_SMALL
+    nv = sum(1 for c in cls if c == CLS_VARYING)
+    nst = sum(1 for c in cls if c == CLS_STREAMED)
+    if k <= 3 and nv <= 4 and nst <= 1:
+        return k | (nv << 4) | (nst << 8)
+    return VARIANT_GENERIC
+
+
+def _item_cost(w, k, L, sizes, dtype):
+    """Estimated device time of one item: dependency hop + max(streaming,
+    per-tile term evaluation x waves of tiles)."""
+    nm = max(1, len(sizes))
+    byt = ELEM_BYTES[dtype] * ((1 << w) + sum(sizes))
+    tiles = 1 << (w - L)
+    waves = -(-tiles // RESIDENT_BLOCKS[dtype])
+    nelem = 1 << L
+    if nelem >= VEC[dtype] * NT:
+        per_tile = (nelem << k) * nm / BLOCK_TERMS_PS[dtype]
+    else:
+        per_tile = 1e-6 + -(-(nelem << k) // NT) * nm * SMALL_LOAD_S
+    return HOP_S + max(byt / BW_BPS, waves * per_tile)
+
+
+def _cost_of(it, dtype):
+    masks, smasks = _masks(it["members"], it["X"], it["R"])
+    L, _ = _tile_bits(len(it["R"]), masks, smasks, dtype)
+    return _item_cost(len(it["R"]), len(it["X"]), L, [1 << len(s2) for _, _, s2 in it["members"]], dtype)
+
+
+def plan_template(index_sets, order, dtype, fixed=(), merge=None):
     """Replay contract_network's bucket assignment (src/ordering.py:165-187)
     over index sets only and freeze it into a Template.
 
     index_sets: per input tensor, its indices in its own storage order
-    (before slicing).  `fixed` indices are sliced out (src/ordering.py:233-248)."""
+    (before slicing).  `fixed` indices are sliced out (src/ordering.py:233-248).
+    merge: fold chains of buckets into k-sum items when the cost model says
+    the saved hop latency / HBM round trip outweighs the extra multiplies."""
     dtype = norm_dtype(dtype)
+    merge = MERGE_DEFAULT if merge is None else merge
     fixed = set(int(f) for f in fixed)
     act = [int(i) for i in order if int(i) not in fixed]
     pos = {x: k for k, x in enumerate(act)}
-    lmax = TILE_BITS[dtype]
-    esz = ELEM_BYTES[dtype]
 
     # ---- inputs: canonical layout and gather maps ----
     n_raw = 0
@@ -111,11 +242,9 @@ def plan_template(index_sets, order, dtype, fixed=()):
     gd, gs = [], []
     gfix = {f: [] for f in fixed}
     sets = []
-    raw_base = []
     for t, idx in enumerate(index_sets):
         idx = tuple(int(i) for i in idx)
         r0 = len(idx)
-        raw_base.append(n_raw)
         kept = [i for i in idx if i not in fixed]
         for i in kept:
             if i not in pos:
@@ -125,12 +254,11 @@ def plan_template(index_sets, order, dtype, fixed=()):
         size = 1 << r
         cur = _align(cur, _tensor_align(size))
         in_off[t] = cur
-        k = np.arange(size, dtype=np.int64)
+        kk = np.arange(size, dtype=np.int64)
         src = np.full(size, n_raw, dtype=np.int64)
-        for p, a in enumerate(canon):
-            bit = (k >> (r - 1 - p)) & 1
-            src += bit << (r0 - 1 - idx.index(a))
-        gd.append(cur + k)
+        for p_, a in enumerate(canon):
+            src += ((kk >> (r - 1 - p_)) & 1) << (r0 - 1 - idx.index(a))
+        gd.append(cur + kk)
         gs.append(src)
         for f in fixed:
             wgt = (1 << (r0 - 1 - idx.index(f))) if f in idx else 0
@@ -143,86 +271,154 @@ def plan_template(index_sets, order, dtype, fixed=()):
     gsrc = np.concatenate(gs) if gs else np.zeros(0, np.int64)
     gfix = {f: (np.concatenate(v) if v else np.zeros(0, np.int64)) for f, v in gfix.items()}
 
-    # ---- bucket replay ----
-    buckets = {x: [] for x in act}
-    fin = []  # (kind, ref) in multiplication order
-    for t, s in enumerate(sets):
-        if not s:
+    # ---- reference bucket replay ----
+    pending = {x: [] for x in act}
+    fin = []      # (kind, ref): kind 0 input tensor, kind 1 reference bucket
+    for t, st in enumerate(sets):
+        if not st:
             fin.append((0, t))
         else:
-            buckets[min(s, key=pos.__getitem__)].append((0, t, s))
-    W, Ls, lev, outo, mptr, mkind, mref, mmask, smem, steps, bidx = ([] for _ in range(11))
-    mptr.append(0)
-    inter = 0
-    maxw = 0
-    for step, x in enumerate(act):
-        mem = buckets.pop(x)
+            pending[min(st, key=pos.__getitem__)].append((0, t, st))
+    refs = []     # (x, members, R)
+    for x in act:
+        mem = pending.pop(x)
         if not mem:
             continue
-        b = len(W)
         union = set()
-        for _, _, s in mem:
-            union |= s
+        for _, _, st in mem:
+            union |= st
         union.discard(x)
         R = sorted(union, key=pos.__getitem__)
-        w = len(R)
-        if w > N.MAX_WIDTH:
-            raise ValueError(f"bucket width {w} exceeds {N.MAX_WIDTH}")
-        maxw = max(maxw, w)
-        bit = {a: w - 1 - j for j, a in enumerate(R)}
-        masks = []
-        lv = 0
-        for kind, ref, s in mem:
-            m = 0
-            for a in s:
-                if a != x:
-                    m |= 1 << bit[a]
-            masks.append(m)
-            if kind == 1:
-                lv = max(lv, lev[ref] + 1)
-        # tile bits: largest L <= lmax whose staged runs fit the smem budget
-        L = min(w, lmax)
-        while True:
-            low = (1 << L) - 1
-            st = sum(2 << bin(m & low).count("1") for m in masks if (m & low) != low)
-            if st * esz <= SMEM_BUDGET or L == 0:
+        if len(R) > N.MAX_WIDTH:
+            raise ValueError(f"bucket width {len(R)} exceeds {N.MAX_WIDTH}")
+        b = len(refs)
+        refs.append((x, mem, R))
+        if R:
+            pending[R[0]].append((1, b, frozenset(R)))
+        else:
+            fin.append((1, b))
+
+    # ---- merge chains into items ----
+    items = []           # dict(X, R, members[(kind, ref(item|input), set)], refs)
+    item_of = []
+    for b, (x, mem, R) in enumerate(refs):
+        it = {"X": [x], "R": R, "refs": [b],
+              "members": [(k_, (item_of[r_] if k_ == 1 else r_), st) for k_, r_, st in mem]}
+        it["cost"] = _cost_of(it, dtype)
+        changed = merge
+        while changed:
+            changed = False
+            for mi, (k_, r_, st) in enumerate(it["members"]):
+                if k_ != 1 or items[r_] is None:
+                    continue
+                p_ = items[r_]
+                X2 = sorted(set(it["X"]) | set(p_["X"]), key=pos.__getitem__)
+                mem2 = it["members"][:mi] + p_["members"] + it["members"][mi + 1:]
+                if len(X2) > KMAX or len(mem2) > N.MAX_MEMBERS:
+                    continue
+                w = len(R)
+                masks, smasks = _masks(mem2, X2, R)
+                L, _ = _tile_bits(w, masks, smasks, dtype)
+                if L < min(w, MIN_TILE_BITS[dtype]):
+                    continue
+                c2 = _item_cost(w, len(X2), L, [1 << len(s2) for _, _, s2 in mem2], dtype)
+                if c2 >= it["cost"] + p_["cost"]:
+                    continue
+                it["X"], it["members"], it["cost"] = X2, mem2, c2
+                it["refs"] = p_["refs"] + it["refs"]
+                items[r_] = None
+                changed = True
                 break
-            L -= 1
-        if len(mem) > N.MAX_MEMBERS:
-            raise ValueError(f"bucket with {len(mem)} members exceeds {N.MAX_MEMBERS}")
+        item_of.append(len(items))
+        items.append(it)
+    # compact (drop absorbed items) and renumber
+    live = [i for i, it in enumerate(items) if it is not None]
+    renum = {old: new for new, old in enumerate(live)}
+    W, K, Ls, lev, outo, mptr, mkind, mref, mmask, msmask, smem, stm, mcls, var = ([] for _ in range(14))
+    mptr.append(0)
+    inter = 0
+    ref_item = np.zeros(len(refs), np.int64)
+    ref_last = np.zeros(len(refs), np.int64)
+    for new, old in enumerate(live):
+        it = items[old]
+        R, X = it["R"], it["X"]
+        w, k = len(R), len(X)
+        masks, smasks = _masks(it["members"], X, R)
+        L, st = _tile_bits(w, masks, smasks, dtype)
+        lv = 0
+        for (k_, r_, _), m, sm in zip(it["members"], masks, smasks):
+            if k_ == 1:
+                r_ = renum[r_]
+                lv = max(lv, lev[r_] + 1)
+            mkind.append(k_)
+            mref.append(r_)
+            mmask.append(m)
+            msmask.append(sm)
+        mptr.append(len(mkind))
         size = 1 << w
         inter = _align(inter, _tensor_align(size))
-        W.append(w); Ls.append(L); lev.append(lv); outo.append(inter); smem.append(st)
-        steps.append(step); bidx.append(x)
+        W.append(w); K.append(k); Ls.append(L); lev.append(lv); outo.append(inter); smem.append(st)
+        sm_ = _step_mask(L, masks, dtype) if (1 << L) >= VEC[dtype] * NT else 0
+        stm.append(sm_)
+        cls_ = member_classes(w, k, L, sm_, masks)
+        mcls.extend(cls_)
+        var.append(kernel_variant(w, k, L, cls_, dtype))
         inter += size
-        for (kind, ref, s), m in zip(mem, masks):
-            mkind.append(kind); mref.append(ref); mmask.append(m)
-        mptr.append(len(mkind))
-        if w == 0:
-            fin.append((1, b))
-        else:
-            buckets[R[0]].append((1, b, frozenset(R)))
+        for r_ in it["refs"]:
+            ref_item[r_] = new
+        ref_last[it["refs"][-1]] = 1
+    ref_w = np.array([len(R) for _, _, R in refs], np.int64)
+    ref_elems = np.array([(1 << len(R)) + sum(1 << len(st) for _, _, st in mem) for _, mem, R in refs], np.int64)
+    fin_kind = np.array([k_ for k_, _ in fin], np.int64)
+    fin_ref = np.array([(ref_item[r_] if k_ == 1 else r_) for k_, r_ in fin], np.int64)
     return Template(
         n_in_elems=n_in, n_inter_elems=_align(inter, 32),
-        w=np.array(W, np.int64), L=np.array(Ls, np.int64), level=np.array(lev, np.int64),
-        out_off=np.array(outo, np.int64), mem_ptr=np.array(mptr, np.int64),
+        w=np.array(W, np.int64), k=np.array(K, np.int64), L=np.array(Ls, np.int64),
+        level=np.array(lev, np.int64), out_off=np.array(outo, np.int64), mem_ptr=np.array(mptr, np.int64),
         mem_kind=np.array(mkind, np.int64), mem_ref=np.array(mref, np.int64),
-        mem_mask=np.array(mmask, np.uint64), smem_elems=np.array(smem, np.int64),
-        step=np.array(steps, np.int64), bucket_index=np.array(bidx, np.int64),
-        fin_kind=np.array([k for k, _ in fin], np.int64), fin_ref=np.array([r for _, r in fin], np.int64),
-        in_off=in_off, gdst=gdst, gsrc=gsrc, gfix=gfix, n_raw=n_raw, max_width=maxw,
+        mem_mask=np.array(mmask, np.uint64), mem_smask=np.array(msmask, np.uint64),
+        smem_elems=np.array(smem, np.int64), stmask=np.array(stm, np.int64),
+        mem_cls=np.array(mcls, np.int64), variant=np.array(var, np.int64),
+        ref_w=ref_w, ref_item=ref_item, ref_last=ref_last, ref_elems=ref_elems,
+        bucket_index=np.array([x for x, _, _ in refs], np.int64),
+        fin_kind=fin_kind, fin_ref=fin_ref,
+        in_off=in_off, gdst=gdst, gsrc=gsrc, gfix=gfix, n_raw=n_raw,
+        max_width=int(ref_w.max()) if len(ref_w) else 0,
     )
 
 
+def _masks(members, X, R):
+    """Result / summed coverage masks: bit j <-> R[w-1-j] / X[k-1-j]."""
+    w, k = len(R), len(X)
+    rbit = {a: w - 1 - j for j, a in enumerate(R)}
+    sbit = {a: k - 1 - j for j, a in enumerate(X)}
+    masks, smasks = [], []
+    for _, _, st in members:
+        m = sm = 0
+        for a in st:
+            if a in rbit:
+                m |= 1 << rbit[a]
+            else:
+                sm |= 1 << sbit[a]   # KeyError = a planner bug (index outside X and R)
+        masks.append(m)
+        smasks.append(sm)
+    return masks, smasks
+
+
 def algorithmic_bytes(t: Template, dtype) -> int:
-    """per bucket (sum_members 2^rank_i + 2^w) * sizeof(elem)."""
-    esz = ELEM_BYTES[norm_dtype(dtype)]
+    """per reference bucket (sum_members 2^rank_i + 2^w) * sizeof(elem)."""
+    return int(t.ref_elems.sum()) * ELEM_BYTES[norm_dtype(dtype)]
+
+
+def executed_bytes(t: Template, dtype) -> int:
+    """Bytes the device items must move: every item reads each member once
+    and writes its result once (merged chains skip the intermediates)."""
     tot = 0
-    for b in range(len(t.w)):
-        tot += 1 << int(t.w[b])
-        for k in range(t.mem_ptr[b], t.mem_ptr[b + 1]):
-            tot += 1 << (1 + bin(int(t.mem_mask[k])).count("1"))
-    return tot * esz
+    for i in range(t.n_items):
+        tot += 1 << int(t.w[i])
+        for j in range(t.mem_ptr[i], t.mem_ptr[i + 1]):
+            tot += 1 << (_popc(int(t.mem_mask[j])) + _popc(int(t.mem_smask[j])))
+    return tot * ELEM_BYTES[norm_dtype(dtype)]
 
 
 @dataclass
@@ -232,7 +428,16 @@ class Instance:
 
 
 class Program:
-    """Several instances laid out in one arena and one ticket space."""
+    """Several instances laid out in one arena, their items grouped into the
+    nodes of one CUDA graph.
+
+    Items of all instances are ordered by (level, instance, item) — a
+    topological order.  Large items (K1 variants) are one node each; small
+    items (VARIANT_SMALL: tiles below one vector step) and finalisers are
+    batched into persistent K2 stages.  A small item joins the open stage
+    unless it depends on a large node created after the stage was opened
+    (that would be a cycle); dependencies inside a stage are per-item
+    completion counters, across nodes they are graph edges."""
 
     def __init__(self, instances, dtype):
         self.dtype = norm_dtype(dtype)
@@ -254,109 +459,176 @@ class Program:
         self.in_base = in_base
         self.inter_base = inter_base
 
-        # global ticket order: (level, instance, step) — a topological order
+        # ---- global item order (topological) ----
         keys = []
         for i, inst in enumerate(self.instances):
             t = inst.template
-            for b in range(len(t.w)):
+            for b in range(t.n_items):
                 keys.append((int(t.level[b]), i, b))
             top = int(t.level.max()) + 1 if len(t.level) else 0
             keys.append((top, i, -1))  # finaliser
-        keys.sort(key=lambda k: (k[0], k[1], k[2] if k[2] >= 0 else 1 << 40))
-        gid = {(i, b): g for g, (_, i, b) in enumerate(keys)}
+        keys.sort(key=lambda q: (q[0], q[1], q[2] if q[2] >= 0 else 1 << 40))
+
+        # ---- producers of every item (global ids) ----
+        order_gid = {(i, b): g for g, (_, i, b) in enumerate(keys)}
+        prods = []
+        for (_, i, b) in keys:
+            t = self.instances[i].template
+            if b >= 0:
+                ps = [order_gid[(i, int(t.mem_ref[j]))] for j in range(t.mem_ptr[b], t.mem_ptr[b + 1])
+                      if t.mem_kind[j] == 1]
+            else:
+                ps = [order_gid[(i, int(r))] for kd, r in zip(t.fin_kind, t.fin_ref) if kd == 1]
+            prods.append(ps)
+
+        # ---- nodes: large items alone, small items in stages ----
+        def is_small(q):
+            _, i, b = q
+            return b < 0 or int(self.instances[i].template.variant[b]) == VARIANT_SMALL
+
+        node_of = [-1] * len(keys)
+        nodes = []           # dict(kind, items, deps:set)
+        open_stage = -1
+        for g, q in enumerate(keys):
+            ext = {node_of[p] for p in prods[g]}
+            if is_small(q):
+                # join the open stage unless a producer is a node created after it
+                if open_stage >= 0 and all(n <= open_stage for n in ext):
+                    nd = open_stage
+                else:
+                    nodes.append({"kind": N.QTN_NODE_SMALL, "items": [], "deps": set()})
+                    open_stage = len(nodes) - 1
+                    nd = open_stage
+                nodes[nd]["items"].append(g)
+                nodes[nd]["deps"] |= {n for n in ext if n != nd}
+                node_of[g] = nd
+            else:
+                nodes.append({"kind": N.QTN_NODE_LARGE, "items": [g], "deps": set(ext)})
+                node_of[g] = len(nodes) - 1
+
+        # ---- final item numbering: node by node (stage items contiguous) ----
+        new_of = {}
+        for nd in nodes:
+            for g in nd["items"]:
+                new_of[g] = len(new_of)
+        item_keys = [None] * len(keys)
+        for g, q in enumerate(keys):
+            item_keys[new_of[g]] = (q, g)
+
         nb = len(keys)
         B = np.zeros(nb, N.BUCKET_DT)
         members, deps = [], []
-        tick = 0
         smem_max = 0
-        self.bucket_gid = []   # per instance: global id per local bucket
-        self.fin_gid = []
-        for i, inst in enumerate(self.instances):
-            t = inst.template
-            self.bucket_gid.append(np.array([gid[(i, b)] for b in range(len(t.w))], np.int64))
-            self.fin_gid.append(gid[(i, -1)])
+        self.bucket_gid = [np.zeros(inst.template.n_items, np.int64) for inst in self.instances]
+        self.fin_gid = [0] * len(self.instances)
         ntiles = np.zeros(nb, np.int64)
-        for g, (_, i, b) in enumerate(keys):
+        for gid, ((_, i, b), g) in enumerate(item_keys):
             t = self.instances[i].template
+            ntiles[gid] = (1 << int(t.w[b] - t.L[b])) if b >= 0 else 1
             if b >= 0:
-                ntiles[g] = 1 << int(t.w[b] - t.L[b])
+                self.bucket_gid[i][b] = gid
             else:
-                ntiles[g] = 1
-        for g, (_, i, b) in enumerate(keys):
-            t = self.instances[i].template
-            ib, xb = in_base[i], inter_base[i]
-            rec = B[g]
-            rec["tick_begin"] = tick
-            rec["n_tiles"] = ntiles[g]
-            rec["mem_begin"] = len(members)
-            rec["dep_begin"] = len(deps)
-            if b >= 0:
-                rec["w"] = t.w[b]
-                rec["tile_bits"] = t.L[b]
-                rec["out_off"] = xb + t.out_off[b]
-                rec["slot"] = -1
-                rec["smem_elems"] = t.smem_elems[b]
-                smem_max = max(smem_max, int(t.smem_elems[b]) * esz)
-                for k in range(t.mem_ptr[b], t.mem_ptr[b + 1]):
-                    kind, ref = int(t.mem_kind[k]), int(t.mem_ref[k])
-                    if kind == 0:
-                        off = ib + int(t.in_off[ref])
-                    else:
-                        pg = gid[(i, ref)]
-                        off = xb + int(t.out_off[ref])
-                        deps.append((pg, ntiles[pg]))
-                    members.append((off, int(t.mem_mask[k])))
-                rec["n_mem"] = t.mem_ptr[b + 1] - t.mem_ptr[b]
-            else:
-                rec["w"] = N.QTN_FINALIZE
-                rec["tile_bits"] = 0
-                rec["out_off"] = 0
-                rec["slot"] = i
-                rec["smem_elems"] = 0
-                for kind, ref in zip(t.fin_kind, t.fin_ref):
-                    if kind == 0:
-                        off = ib + int(t.in_off[ref])
-                    else:
-                        pg = gid[(i, int(ref))]
-                        off = xb + int(t.out_off[ref])
-                        deps.append((pg, ntiles[pg]))
-                    members.append((off, 0))
-                rec["n_mem"] = len(t.fin_kind)
-            rec["n_dep"] = len(deps) - rec["dep_begin"]
-            tick += int(ntiles[g])
-        if tick >= 2 ** 31 - 1 - 100000:
-            raise ValueError("program too large for one launch (ticket space)")
+                self.fin_gid[i] = gid
+        node_list = []
+        node_deps = []
+        for ni, nd in enumerate(nodes):
+            gids = [new_of[g] for g in nd["items"]]
+            first, count = min(gids), len(gids)
+            assert gids == list(range(first, first + count))
+            tick = 0
+            node_smem = SMALL_PROD_ELEMS * esz if nd["kind"] == N.QTN_NODE_SMALL else 0
+            variant = 0
+            for gid in gids:
+                (_, i, b), g = item_keys[gid]
+                t = self.instances[i].template
+                ib, xb = in_base[i], inter_base[i]
+                rec = B[gid]
+                rec["tick_begin"] = tick if nd["kind"] == N.QTN_NODE_SMALL else 0
+                rec["n_tiles"] = ntiles[gid]
+                rec["mem_begin"] = len(members)
+                rec["dep_begin"] = len(deps)
+                if b >= 0:
+                    rec["w"], rec["k"], rec["tile_bits"] = t.w[b], t.k[b], t.L[b]
+                    rec["out_off"] = xb + t.out_off[b]
+                    rec["slot"] = -1
+                    rec["smem_elems"] = t.smem_elems[b]
+                    rec["stmask"] = t.stmask[b]
+                    for j in range(t.mem_ptr[b], t.mem_ptr[b + 1]):
+                        kind, ref = int(t.mem_kind[j]), int(t.mem_ref[j])
+                        if kind == 0:
+                            off = ib + int(t.in_off[ref])
+                        else:
+                            pg = new_of[order_gid[(i, ref)]]
+                            off = xb + int(t.out_off[ref])
+                            if node_of[order_gid[(i, ref)]] == ni:
+                                deps.append((pg, ntiles[pg]))
+                        members.append((off, int(t.mem_mask[j]), int(t.mem_smask[j]), int(t.mem_cls[j])))
+                    rec["n_mem"] = t.mem_ptr[b + 1] - t.mem_ptr[b]
+                    if nd["kind"] == N.QTN_NODE_LARGE:
+                        variant = int(t.variant[b])
+                        node_smem = _align(int(t.smem_elems[b]) * esz, 16)
+                else:
+                    rec["w"] = N.QTN_FINALIZE
+                    rec["k"], rec["tile_bits"], rec["out_off"] = 0, 0, 0
+                    rec["slot"] = i
+                    for kd, ref in zip(t.fin_kind, t.fin_ref):
+                        if kd == 0:
+                            off = ib + int(t.in_off[ref])
+                        else:
+                            pg = new_of[order_gid[(i, int(ref))]]
+                            off = xb + int(t.out_off[int(ref)])
+                            if node_of[order_gid[(i, int(ref))]] == ni:
+                                deps.append((pg, ntiles[pg]))
+                        members.append((off, 0, 0, 0))
+                    rec["n_mem"] = len(t.fin_kind)
+                rec["n_dep"] = len(deps) - rec["dep_begin"]
+                tick += int(ntiles[gid])
+            smem_max = max(smem_max, node_smem)
+            dl = sorted(nd["deps"])
+            node_list.append((nd["kind"], first, count, tick if nd["kind"] == N.QTN_NODE_SMALL else 0,
+                              variant, len(node_deps), len(dl), node_smem))
+            node_deps.extend(dl)
+        if max(int(n[3]) for n in node_list) >= 2 ** 31 - 1:
+            raise ValueError("program stage too large (ticket space)")
         self.n_buckets = nb
-        self.n_tickets = tick
-        self.smem_bytes = _align(smem_max, 16)
+        self.nodes = np.array(node_list, dtype=N.NODE_DT)
+        self.node_deps = np.array(node_deps if node_deps else [0], dtype=np.int32)
+        self.n_nodes = len(node_list)
+        self.smem_bytes = smem_max
         self.buckets = B
-        self.members = np.array(members, dtype=N.MEMBER_DT) if members else np.zeros(0, N.MEMBER_DT)
-        self.deps = np.array(deps, dtype=N.DEP_DT) if deps else np.zeros(0, N.DEP_DT)
+        self.members = np.array(members, dtype=N.MEMBER_DT) if members else np.zeros(1, N.MEMBER_DT)
+        self.deps = np.array(deps, dtype=N.DEP_DT) if deps else np.zeros(1, N.DEP_DT)
         self.tick_begin = np.ascontiguousarray(B["tick_begin"]).astype(np.int32)
         # input image gather (per instance, slice assignment applied)
-        dst, src, srcinst = [], [], []
+        dst, src = [], []
         for i, inst in enumerate(self.instances):
             t = inst.template
-            s = t.gsrc.copy()
+            s_ = t.gsrc.copy()
             for f, bitv in inst.assignment.items():
                 if int(bitv):
-                    s += t.gfix[int(f)]
+                    s_ += t.gfix[int(f)]
             dst.append(in_base[i] + t.gdst)
-            src.append(s)
+            src.append(s_)
         self.img_dst = np.concatenate(dst) if dst else np.zeros(0, np.int64)
         self.img_src_parts = src
-
-    def table_bytes(self) -> bytes:
-        return b"".join([self.buckets.tobytes(), self.members.tobytes(), self.deps.tobytes(),
-                         self.tick_begin.tobytes()])
 
     def algorithmic_bytes(self) -> int:
         return sum(algorithmic_bytes(inst.template, self.dtype) for inst in self.instances)
 
+    def executed_bytes(self) -> int:
+        return sum(executed_bytes(inst.template, self.dtype) for inst in self.instances)
+
+    def describe(self):
+        kinds = self.nodes["kind"]
+        return {"items": int(self.n_buckets), "nodes": int(self.n_nodes),
+                "small_stages": int((kinds == N.QTN_NODE_SMALL).sum()),
+                "large_items": int((kinds == N.QTN_NODE_LARGE).sum())}
+
 
 class Executor:
     """Device-resident copy of a Program: tables, control block, arena and
-    result slots, all owned by torch; launches go through the C ABI."""
+    result slots owned by torch; the node graph is built once through the C
+    ABI (qtn_graph_create) and every run is one cudaGraphLaunch."""
 
     def __init__(self, prog: Program, device=0, timing=False):
         import torch
@@ -367,19 +639,19 @@ class Executor:
         dev = self.device
         tdt = torch.complex64 if prog.dtype == "complex64" else torch.complex128
         self.tdt = tdt
+        lib = N.load()
         with torch.cuda.device(dev):
-            # one table buffer: buckets | members | deps | tick_begin | ctrl
             parts = [prog.buckets.tobytes(), prog.members.tobytes(), prog.deps.tobytes(),
                      prog.tick_begin.tobytes()]
             offs, cur = [], 0
-            for p in parts:
+            for p_ in parts:
                 offs.append(cur)
-                cur = _align(cur + len(p), 16)
+                cur = _align(cur + len(p_), 16)
             ctrl_off = cur
-            total = ctrl_off + 4 * (2 + prog.n_buckets)
+            total = ctrl_off + 4 * (2 * prog.n_nodes + prog.n_buckets)
             host = np.zeros(_align(total, 16), np.uint8)
-            for o, p in zip(offs, parts):
-                host[o:o + len(p)] = np.frombuffer(p, np.uint8)
+            for o, p_ in zip(offs, parts):
+                host[o:o + len(p_)] = np.frombuffer(p_, np.uint8)
             self.tables = torch.from_numpy(host).to(dev)
             base = self.tables.data_ptr()
             self.arena = torch.empty(prog.arena_elems, dtype=tdt, device=dev)
@@ -391,14 +663,13 @@ class Executor:
                 self.timing_init = torch.zeros_like(self.timing)
                 self.timing_init[0::2] = np.iinfo(np.int64).max
             self.img_pinned = torch.zeros(max(1, prog.n_input_elems), dtype=tdt).pin_memory()
-            self.c = N.ProgramC()
-            c = self.c
+            c = N.ProgramC()
             c.dtype = DTYPE_CODE[prog.dtype]
             c.n_buckets = prog.n_buckets
-            c.n_tickets = prog.n_tickets
+            c.n_tickets = 0
             c.smem_bytes = prog.smem_bytes
-            c.grid = N.program_grid(c.dtype, prog.smem_bytes)
-            c.flags = 0
+            c.grid = 0
+            c.n_nodes = prog.n_nodes
             c.buckets = base + offs[0]
             c.members = base + offs[1]
             c.deps = base + offs[2]
@@ -407,7 +678,22 @@ class Executor:
             c.arena = self.arena.data_ptr()
             c.results = self.results.data_ptr()
             c.timing = self.timing.data_ptr() if timing else None
-        self.grid = c.grid
+            self.c = c
+            torch.cuda.synchronize(dev)
+            g = ctypes.c_void_p()
+            nodes = np.ascontiguousarray(prog.nodes)
+            deps = np.ascontiguousarray(prog.node_deps)
+            N.check(lib.qtn_graph_create(ctypes.byref(c), nodes.ctypes.data_as(ctypes.c_void_p), prog.n_nodes,
+                                         deps.ctypes.data_as(ctypes.c_void_p), ctypes.byref(g)))
+            self.graph = g
+
+    def __del__(self):
+        g = getattr(self, "graph", None)
+        if g is not None and g.value:
+            try:
+                N.load().qtn_graph_destroy(g)
+            except Exception:
+                pass
 
     # -- input image -------------------------------------------------------
     def stage_inputs(self, raw_parts):
@@ -428,8 +714,7 @@ class Executor:
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         if self.timing is not None:
             self.timing.copy_(self.timing_init, non_blocking=True)
-        lib = N.load()
-        N.check(lib.qtn_program_launch(ctypes.byref(self.c), ctypes.c_void_p(s.cuda_stream)))
+        N.check(N.load().qtn_graph_launch(self.graph, ctypes.c_void_p(s.cuda_stream)))
 
     def reset(self, stream=None):
         torch = self.torch

@@ -255,15 +255,24 @@ def _executor(key, progfn, backend, n_inst):
     return hit
 
 
+def ref_stats(tmpl, backend, item_elapsed=None):
+    """One BucketStats per reference bucket (elimination order).  A merged
+    device item's time is reported on its final bucket (0 on the buckets it
+    absorbed)."""
+    if item_elapsed is None:
+        el = np.zeros(len(tmpl.ref_w), np.int64)
+    else:
+        el = np.where(tmpl.ref_last == 1, item_elapsed[tmpl.ref_item], 0)
+    return [BucketStats(width=int(w), elapsed_ns=int(e), backend_used=backend.route(int(w)))
+            for w, e in zip(tmpl.ref_w, el)]
+
+
 def _stats(tmpl, ex, backend, inst=0):
     if backend.profile:
         t0, t1 = ex.fetch_timing()
         gids = ex.prog.bucket_gid[inst]
-        el = np.maximum(t1[gids] - t0[gids], 0)
-    else:
-        el = np.zeros(len(tmpl.w), np.int64)
-    return [BucketStats(width=int(w), elapsed_ns=int(e), backend_used=backend.route(int(w)))
-            for w, e in zip(tmpl.w, el)]
+        return ref_stats(tmpl, backend, np.maximum(t1[gids] - t0[gids], 0))
+    return ref_stats(tmpl, backend)
 
 
 def contract_network(tn: TensorNetwork, order, backend: Backend = None, mem_cap: int = DEFAULT_MEM_CAP):

@@ -227,62 +227,64 @@ def _device_permute(t: DeviceTensor, new_order, dtype) -> DeviceTensor:
 
 class _BucketLauncher:
     """Single-bucket program (no arena: member and result offsets are absolute
-    device addresses / element size)."""
-
-    _grid = {}
+    device addresses / element size), launched as one node: the K1
+    large-item kernel variant for vector-sized tiles, else a one-item K2
+    stage."""
 
     @classmethod
     def run(cls, members, masks, out, w, dtype):
         import torch
         dev = out.device
         esz = E.ELEM_BYTES[dtype]
-        lmax = E.TILE_BITS[dtype]
-        L = min(w, lmax)
-        while True:
-            low = (1 << L) - 1
-            st = sum(2 << bin(m & low).count("1") for m in masks if (m & low) != low)
-            if st * esz <= E.SMEM_BUDGET or L == 0:
-                break
-            L -= 1
+        smasks = [1] * len(masks)
+        L, st = E._tile_bits(w, masks, smasks, dtype)
+        small = (1 << L) < E.VEC[dtype] * E.NT
+        stm = 0 if small else E._step_mask(L, masks, dtype)
+        mcls = E.member_classes(w, 1, L, stm, masks)
+        variant = E.kernel_variant(w, 1, L, mcls, dtype)
         B = np.zeros(1, N.BUCKET_DT)
         B["out_off"] = out.data_ptr() // esz
         B["w"] = w
+        B["k"] = 1
         B["tile_bits"] = L
         B["n_mem"] = len(members)
         B["n_tiles"] = 1 << (w - L)
         B["slot"] = -1
         B["smem_elems"] = st
+        B["stmask"] = stm
         M = np.zeros(len(members), N.MEMBER_DT)
-        for k, (m, msk) in enumerate(zip(members, masks)):
-            M[k] = (m.data_ptr() // esz, msk)
-        blob = np.zeros(48 + 16 * N.MAX_MEMBERS + 16 + 16, np.uint8)
-        blob[0:48] = np.frombuffer(B.tobytes(), np.uint8)
-        blob[48:48 + M.nbytes] = np.frombuffer(M.tobytes(), np.uint8)
-        tb_off = 48 + 16 * N.MAX_MEMBERS          # tick_begin[0] = 0, then ctrl[3] = 0
+        for k, (m, msk, c) in enumerate(zip(members, masks, mcls)):
+            M[k] = (m.data_ptr() // esz, msk, 1, c)
+        bsz, msz = N.BUCKET_DT.itemsize, N.MEMBER_DT.itemsize
+        tb_off = bsz + msz * N.MAX_MEMBERS          # tick_begin[0] = 0, then ctrl[3] = 0
+        blob = np.zeros(tb_off + 32, np.uint8)
+        blob[0:bsz] = np.frombuffer(B.tobytes(), np.uint8)
+        blob[bsz:bsz + M.nbytes] = np.frombuffer(M.tobytes(), np.uint8)
         dtab = torch.from_numpy(blob).to(dev)
         base = dtab.data_ptr()
-        key = (dtype, st * esz, dev.index)
-        if key not in cls._grid:
-            cls._grid[key] = N.program_grid(E.DTYPE_CODE[dtype], _smem_bytes(st * esz))
         c = N.ProgramC()
         c.dtype = E.DTYPE_CODE[dtype]
         c.n_buckets = 1
-        c.n_tickets = 1 << (w - L)
-        c.smem_bytes = _smem_bytes(st * esz)
-        c.grid = min(cls._grid[key], c.n_tickets)
+        c.n_nodes = 1
         c.buckets = base
-        c.members = base + 48
-        c.deps = base + 48
+        c.members = base + bsz
+        c.deps = base + bsz
         c.tick_begin = base + tb_off
         c.ctrl = base + tb_off + 4
         c.arena = None
         c.results = None
         c.timing = None
+        node = np.zeros(1, N.NODE_DT)
+        if small:
+            node[0] = (N.QTN_NODE_SMALL, 0, 1, 1 << (w - L), 0, 0, 0, E.SMALL_PROD_ELEMS * esz)
+        else:
+            node[0] = (N.QTN_NODE_LARGE, 0, 1, 0, variant, 0, 0, _smem_bytes(st * esz))
         stream = torch.cuda.current_stream(dev)
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
-        N.check(N.load().qtn_program_launch(ctypes.byref(c), ctypes.c_void_p(stream.cuda_stream)))
+        N.check(N.load().qtn_node_launch(ctypes.byref(c), node.ctypes.data_as(ctypes.c_void_p), 0,
+                                         ctypes.c_void_p(stream.cuda_stream)))
         ev1.record(stream)
         # keep the table alive until the launch has consumed it
         ev1.synchronize()

@@ -36,16 +36,17 @@ for gid in range(prog.n_buckets):
     if b["w"] < 0:
         continue
     mem = prog.members[b["mem_begin"]: b["mem_begin"] + b["n_mem"]]
-    by = (1 << int(b["w"])) + sum(1 << (1 + bin(int(m["mask"])).count("1")) for m in mem)
+    by = (1 << int(b["w"])) + sum(1 << (bin(int(m["smask"])).count("1") + bin(int(m["mask"])).count("1")) for m in mem)
     rows.append((t0[gid] - origin, t1[gid] - origin, int(b["w"]), int(b["tile_bits"]), int(b["n_tiles"]),
-                 int(b["n_mem"]), by * esz))
+                 int(b["n_mem"]), by * esz, int(b["k"])))
 rows.sort()
 tot = t1.max() - origin
 print(f"total {tot/1e3:.1f} us, buckets {len(rows)}")
 small = [r for r in rows if r[2] < 12]
 print(f"small (w<12): {len(small)} buckets, span {max(r[1] for r in small)/1e3:.1f} us")
-print(" start_us   end_us   dur_us  w  L  tiles nmem   MB    GB/s")
+print(f"algorithmic {prog.algorithmic_bytes()/1e9:.3f} GB, executed {prog.executed_bytes()/1e9:.3f} GB, {prog.describe()}")
+print(" start_us   end_us   dur_us  w  k  L  tiles nmem   MB    GB/s")
 for r in rows:
-    if r[2] >= 12:
+    if r[2] >= 12 or r[7] > 1:
         d = r[1] - r[0]
-        print(f"{r[0]/1e3:8.1f} {r[1]/1e3:8.1f} {d/1e3:8.1f} {r[2]:2d} {r[3]:2d} {r[4]:6d} {r[5]:3d} {r[6]/1e6:7.1f} {r[6]/max(d,1):7.0f}")
+        print(f"{r[0]/1e3:8.1f} {r[1]/1e3:8.1f} {d/1e3:8.1f} {r[2]:2d} {r[7]:2d} {r[3]:2d} {r[4]:6d} {r[5]:3d} {r[6]/1e6:7.1f} {r[6]/max(d,1):7.0f}")

@@ -2,7 +2,7 @@
 
 Executes the planner's tables with the exact semantics the CUDA program
 kernel implements (csrc/qtn_b200.cu): buckets in ticket order, member offset
-off + b * 2^popc(mask) + pext(r, mask), out = prod_i(b=0) + prod_i(b=1),
+off + (pext(s, smask) << popc(mask)) + pext(r, mask), out = sum_s prod_i,
 finaliser = product of rank-0 values.  Lets the planner be checked on CPU."""
 import numpy as np
 
@@ -28,30 +28,38 @@ def run_program(prog, raw_parts):
         A = A.astype(np.complex64)
     res = np.zeros(len(prog.instances), np.complex128)
     B = prog.buckets
-    order = np.argsort(B["tick_begin"], kind="stable")
     done = set()
-    for g in order:
-        b = B[g]
-        for d in prog.deps[b["dep_begin"]: b["dep_begin"] + b["n_dep"]]:
-            assert int(d["bucket"]) in done, "dependency not satisfied in ticket order"
-        mem = prog.members[b["mem_begin"]: b["mem_begin"] + b["n_mem"]]
-        if b["w"] == N.QTN_FINALIZE:
-            v = 1 + 0j
-            for m in mem:
-                v *= complex(A[int(m["off"])])
-            res[int(b["slot"])] = v
-        else:
-            w = int(b["w"])
-            r = np.arange(1 << w, dtype=np.int64)
-            p = [None, None]
-            for m in mem:
-                mask = int(m["mask"])
-                pc = bin(mask).count("1")
-                idx = int(m["off"]) + pext_vec(r, mask)
-                for bb in (0, 1):
-                    x = A[idx + (bb << pc)]
-                    p[bb] = x.copy() if p[bb] is None else p[bb] * x
-            o = int(b["out_off"])
-            A[o: o + (1 << w)] = p[0] + p[1]
-        done.add(int(g))
+    node_done = set()
+    for ni, nd in enumerate(prog.nodes):
+        for d in prog.node_deps[nd["dep_begin"]: nd["dep_begin"] + nd["n_dep"]]:
+            assert int(d) in node_done and int(d) < ni, "graph dependency not earlier"
+        items = range(int(nd["first"]), int(nd["first"]) + int(nd["count"]))
+        if nd["kind"] == N.QTN_NODE_SMALL:
+            items = sorted(items, key=lambda g: int(B[g]["tick_begin"]))
+        for g in items:
+            b = B[g]
+            for d in prog.deps[b["dep_begin"]: b["dep_begin"] + b["n_dep"]]:
+                assert int(d["bucket"]) in done, "dependency not satisfied in ticket order"
+            mem = prog.members[b["mem_begin"]: b["mem_begin"] + b["n_mem"]]
+            if b["w"] == N.QTN_FINALIZE:
+                v = 1 + 0j
+                for m in mem:
+                    v *= complex(A[int(m["off"])])
+                res[int(b["slot"])] = v
+            else:
+                w, k = int(b["w"]), int(b["k"])
+                r = np.arange(1 << w, dtype=np.int64)
+                acc = None
+                for s in range(1 << k):
+                    p = None
+                    for m in mem:
+                        mask, smask = int(m["mask"]), int(m["smask"])
+                        pc = bin(mask).count("1")
+                        x = A[int(m["off"]) + (int(pext_vec(np.array([s]), smask)[0]) << pc) + pext_vec(r, mask)]
+                        p = x.copy() if p is None else p * x
+                    acc = p if acc is None else acc + p
+                o = int(b["out_off"])
+                A[o: o + (1 << w)] = acc
+            done.add(int(g))
+        node_done.add(ni)
     return res

@@ -20,14 +20,15 @@ def test_header_symbols_exported():
 
 
 def test_struct_layouts_match_header():
-    assert N.BUCKET_DT.itemsize == 48
-    assert N.MEMBER_DT.itemsize == 16
+    assert N.BUCKET_DT.itemsize == 56
+    assert N.MEMBER_DT.itemsize == 24
     assert ctypes.sizeof(N.ProgramC) == 6 * 4 + 8 * 8
+    assert N.NODE_DT.itemsize == 32
 
 
 def test_errors_cross_abi_as_codes():
     lib = N.load()
-    assert lib.qtn_program_launch(None, None) == N.QTN_E_INVALID
+    assert lib.qtn_node_launch(None, None, 0, None) == N.QTN_E_INVALID
     assert b"null program" in lib.qtn_last_error()
     n = ctypes.c_int(-1)
     assert lib.qtn_device_count(ctypes.byref(n)) == 0 and n.value >= 0

@@ -41,7 +41,7 @@ def test_network_orders_and_values(k):
         assert list(Q.dry_run(tn, order).per_bucket_widths) == rec[f"widths_{h}"]
     v, t, _ = _emulate(tn, rec["order_minfill"])
     assert abs(v - complex(*rec["value"])) < 1e-12
-    assert list(t.w) == [w for w in rec["widths_minfill"]][: len(t.w)]
+    assert list(t.ref_w) == rec["widths_minfill"]
     if "suggest" in rec:
         assert Q.suggest_slicing(tn, rec["order_minfill"], rec["slice_target"]) == rec["suggest"]
     # sliced: sum of emulated slices
@@ -162,6 +162,7 @@ def test_plan_masks_follow_canonical_layout():
         full = (1 << int(t.w[b])) - 1
         for k in range(t.mem_ptr[b], t.mem_ptr[b + 1]):
             assert int(t.mem_mask[k]) & ~full == 0
+            assert int(t.mem_smask[k]) >> int(t.k[b]) == 0
     # algorithmic bytes of the cfg-2 cone (1.468 GB c64)
     gb = E.algorithmic_bytes(t, "complex64") / 1e9
     assert gb == pytest.approx(1.468, abs=0.01)
