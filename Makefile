@@ -16,6 +16,10 @@ $(LIB): $(SRC) include/qtn_b200.h
 variant:
 	$(NVCC) $(NVFLAGS) -o paper_2210_15874_b200/lib/libqtn_b200_mb$(MINB).so $(SRC)
 
+# bounds-checked build (device asserts), for GPU debugging without compute-sanitizer
+debug:
+	$(NVCC) $(NVFLAGS) -DQTN_DEBUG -o paper_2210_15874_b200/lib/libqtn_b200_debug.so $(SRC)
+
 sass: $(LIB)
 	cuobjdump -sass $(LIB) | grep -E "Function|LDG|STG|ATOM|RED" | head -50
 

@@ -40,7 +40,7 @@ WORKLOAD = "cfg2: 3-regular N=30 (seed 0), p=4 (seeded angles), tight lightcone 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -334,13 +334,16 @@ def run_ours(args):
                                       "(NumPy+CuPy mixed on V100, PAPER.md:64)", **side},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(args.dtype), "peak_source": peak_src,
-                     "kernel": "program_kernel<float>" if dtype == "complex64" else "program_kernel<double>"},
+                     "kernel": "one program graph per step: K2 small_kernel stages + K1 large_kernel variants "
+                               "(one cudaGraphLaunch); achieved = algorithmic bytes (SURVEY 8(d)) / device time",
+                     "achieved_executed": prog.executed_bytes() / (t_kern / args.steps) / 1e9},
         "cpu_baseline": cpu,
         "e2e": {"value": world * args.steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": n_in,
                 "d2h_bytes_per_step": 16, "s_per_lightcone": t_e2e / args.steps,
                 "call": "paper_2210_15874_b200.contract_network(tn, order, Backend.b200(...)) from host Tensors",
                 "zz": v_e2e.real},
-        "gpu_launches": args.steps,
+        "gpu_launches": args.steps * prog.n_nodes,
+        "gpu_launches_note": f"{prog.n_nodes} kernels per step, issued as one CUDA graph launch",
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)

@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define QTN_ABI_VERSION 4
+#define QTN_ABI_VERSION 5
 
 enum {
   QTN_OK = 0,
@@ -126,6 +126,8 @@ typedef struct {
                                    offsets are absolute addresses / elem size  */
   double* results;              /* 2 doubles per finaliser slot               */
   unsigned long long* timing;   /* optional: 2 per bucket (first start, last end, ns) */
+  int64_t arena_elems;          /* arena size in elements (bounds checks of the
+                                   QTN_DEBUG build; 0 = unchecked)             */
 } qtn_program_t;
 
 /* Execution node of a program graph.

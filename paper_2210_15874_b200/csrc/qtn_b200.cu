@@ -60,6 +60,26 @@ int cuda_err(cudaError_t e, const char* what) {
   return set_err(QTN_E_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
 }
 
+// QTN_DEBUG build: bounds-check every arena / shared-memory index (trap with
+// a message).  compute-sanitizer is unavailable on the target pool.
+#ifdef QTN_DEBUG
+#define QTN_CHECK(cond, ...)                                                     \
+  do {                                                                           \
+    if (!(cond)) {                                                               \
+      printf("QTN_CHECK %s:%d (block %d thread %d): ", __FILE__, __LINE__,      \
+             (int)blockIdx.x, (int)threadIdx.x);                                \
+      printf(__VA_ARGS__);                                                       \
+      printf("\n");                                                             \
+      __trap();                                                                  \
+    }                                                                            \
+  } while (0)
+#else
+#define QTN_CHECK(cond, ...) \
+  do {                       \
+  } while (0)
+#endif
+#define QTN_ARENA_OK(P, o) ((P).arena_elems == 0 || ((int64_t)(o) >= 0 && (int64_t)(o) < (P).arena_elems))
+
 constexpr int NT = 256;                 // threads per block
 constexpr int MAXM = QTN_MAX_MEMBERS;   // members per item
 constexpr int MAXS = 16;                // vector steps per tile: 2^L / (VEC * NT)
@@ -126,6 +146,11 @@ __device__ __forceinline__ uint64_t pext64(uint64_t x, uint64_t m) {
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+[[maybe_unused]] __device__ __forceinline__ uint32_t dyn_smem_bytes() {
+  uint32_t v;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(v));
   return v;
 }
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -270,6 +295,7 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
         double re = 1.0, im = 0.0;
         for (int i = 0; i < S.b.n_mem; ++i) {
           const qtn_member_t m = P.members[S.b.mem_begin + i];
+          QTN_CHECK(QTN_ARENA_OK(P, m.off), "finaliser member %d off %lld", i, (long long)m.off);
           const T v = __ldcg(A + m.off);
           const double vr = (double)v.x, vi = (double)v.y;
           const double nr = re * vr - im * vi;
@@ -305,6 +331,7 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
               const int e = u & (nelem - 1), sc = s0 + (u >> L);
               const uint64_t o = S.base[i] + ((uint64_t)S.sig[i][sc] << S.pc[i]) +
                                  (S.pclo[i] == L ? (uint64_t)e : (uint64_t)pext32((uint32_t)e, S.mlo[i]));
+              QTN_CHECK(QTN_ARENA_OK(P, o), "small item %d member %d off %lld", cur, i, (long long)o);
               x[j] = __ldcg(A + o);
             }
 #pragma unroll
@@ -312,13 +339,17 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
           }
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            if (u0 + j * NT < nu) sprod[u0 + j * NT] = prod[j];
+            if (u0 + j * NT < nu) {
+              QTN_CHECK((u0 + j * NT + 1) * (int)sizeof(T) <= (int)dyn_smem_bytes(), "sprod %d", u0 + j * NT);
+              sprod[u0 + j * NT] = prod[j];
+            }
         }
         __syncthreads();
         if (tid < nelem)
           for (int c = 0; c < cs; ++c) acc = (s0 + c == 0) ? sprod[c * nelem + tid] : cadd(acc, sprod[c * nelem + tid]);
         __syncthreads();
       }
+      QTN_CHECK(QTN_ARENA_OK(P, S.b.out_off + (uint64_t)h * nelem + nelem - 1), "small item %d out", cur);
       if (tid < nelem) out[tid] = acc;
     }
     __syncthreads();
@@ -435,6 +466,11 @@ __device__ __forceinline__ void large_prep(LargeCtx& S, const qtn_program_t& P, 
     S.has_u = hu;
     S.uoff = acc;
     S.nbulk = nb;
+    QTN_CHECK((acc + MAXNS) * (int)sizeof(T) <= (int)dyn_smem_bytes(), "item %d staged %d elems > smem %u B", item,
+              acc, dyn_smem_bytes());
+    QTN_CHECK(nv <= MAXM && (L >= 32 ? false : true), "item %d bad layout", item);
+    QTN_CHECK((1 << L) / (VEC * NT) <= MAXS, "item %d steps", item);
+    QTN_CHECK(QTN_ARENA_OK(P, S.b.out_off + ((uint64_t)S.b.n_tiles << L) - 1), "item %d out range", item);
   }
   __syncthreads();
   if (tid < nm * MAXS) {
@@ -450,7 +486,7 @@ __device__ __forceinline__ void large_prep(LargeCtx& S, const qtn_program_t& P, 
 // U[s] = product of the tile-uniform members.
 template <typename R>
 __device__ __forceinline__ void large_stage(LargeCtx& S, const typename Cx<R>::T* A, typename Cx<R>::T* sseg,
-                                            uint64_t* bar, uint32_t& phase, int h) {
+                                            uint64_t* bar, uint32_t& phase, int h, const qtn_program_t& P_arena) {
   using T = typename Cx<R>::T;
   const int tid = threadIdx.x;
   const int nm = S.b.n_mem;
@@ -466,6 +502,9 @@ __device__ __forceinline__ void large_stage(LargeCtx& S, const typename Cx<R>::T
       if (rb < 16) continue;
       const T* src = A + S.base[i];
       for (int r = 0; r < S.nsig[i]; ++r) {
+        QTN_CHECK(QTN_ARENA_OK(P_arena, S.base[i] + ((uint64_t)r << S.pc[i]) + S.seglen[i] - 1), "bulk src member %d run %d", i, r);
+        QTN_CHECK(((uintptr_t)(src + ((uint64_t)r << S.pc[i])) & 15) == 0 && ((S.seg[i] + r * S.seglen[i]) * (int)sizeof(T)) % 16 == 0,
+                  "bulk misaligned member %d run %d", i, r);
         bulk_g2s(sseg + S.seg[i] + r * S.seglen[i], src + ((uint64_t)r << S.pc[i]), rb, bar);
         bytes += rb;
       }
@@ -475,7 +514,10 @@ __device__ __forceinline__ void large_stage(LargeCtx& S, const typename Cx<R>::T
   for (int i = 0; i < nm; ++i) {
     if (S.seg[i] < 0 || S.seglen[i] * (int)sizeof(T) >= 16) continue;
     const T* src = A + S.base[i];
-    for (int q = tid; q < S.nsig[i]; q += NT) sseg[S.seg[i] + q] = __ldcg(src + ((uint64_t)q << S.pc[i]));
+    for (int q = tid; q < S.nsig[i]; q += NT) {
+      QTN_CHECK(QTN_ARENA_OK(P_arena, S.base[i] + ((uint64_t)q << S.pc[i])), "short run member %d", i);
+      sseg[S.seg[i] + q] = __ldcg(src + ((uint64_t)q << S.pc[i]));
+    }
   }
   if (S.nbulk) {
     mbar_wait(bar, phase);
@@ -525,6 +567,7 @@ __device__ __forceinline__ void large_compute(const LargeCtx& S, const typename 
   int64_t sro[NS];
   if (ST) {
     const int sm = S.s0m;
+    QTN_CHECK(sm >= 0, "ST variant without streamed member");
     sp = A + S.base[sm] + S.eth[tid];
 #pragma unroll
     for (int c = 0; c < NS; ++c) sro[c] = (int64_t)S.sig[sm][c] << S.pc[sm];
@@ -581,6 +624,9 @@ __device__ __forceinline__ void large_compute(const LargeCtx& S, const typename 
       const T* q = qv[j] + S.gs[vi[j]][st];
 #pragma unroll
       for (int c = 0; c < NS; ++c) {
+        QTN_CHECK((int)((q + ro[j][c]) - sseg) + VEC <= S.uoff + MAXNS &&
+                      S.gt[vi[j]][tid] + S.gs[vi[j]][st] + ro[j][c] < S.nsig[vi[j]] * S.seglen[vi[j]],
+                  "staged gather member %d", vi[j]);
         T x[VEC];
         if (VEC == 2) {
           if (b0[j]) {
@@ -604,6 +650,7 @@ __device__ __forceinline__ void large_compute(const LargeCtx& S, const typename 
 #pragma unroll
       for (int c = 1; c < NS; ++c) acc[v] = cadd(acc[v], prod[c][v]);
     }
+    QTN_CHECK(S.eth[tid] + est + VEC <= (1 << S.b.tile_bits), "tile offset %d", S.eth[tid] + est);
     *reinterpret_cast<V*>(out + S.eth[tid] + est) = join(acc);
   }
 }
@@ -679,7 +726,7 @@ __global__ void __launch_bounds__(NT) large_kernel(const qtn_program_t P, int32_
   const int ntiles = S.b.n_tiles;
   const uint64_t nelem = 1ull << S.b.tile_bits;
   for (int h = blockIdx.x; h < ntiles; h += gridDim.x) {
-    large_stage<R>(S, A, sseg, &bar, phase, h);
+    large_stage<R>(S, A, sseg, &bar, phase, h, P);
     T* out = Aw + S.b.out_off + (uint64_t)h * nelem;
     if (NS > 0)
       large_compute<R, (NS > 0 ? NS : 2), NV, ST>(S, A, sseg, out);

@@ -68,12 +68,13 @@ VEC = {"complex64": 2, "complex128": 1}
 # merge cost model (seconds), calibrated on the r01 per-bucket B200 timeline:
 # a dependency hop costs ~3 us of latency; streaming ~5.5 TB/s; one block
 # evaluates ~2.5e9 member-terms/s when every SM is shared by ~5 blocks; a
-# small-tile thread is L2-latency bound (~40 ns per dependent member load).
+# small-tile round is L2-latency bound (~0.65 us per dependent member load,
+# measured on the r01 K2 timeline).
 HOP_S = 5.0e-6
 BW_BPS = 5.5e12
 BLOCK_TERMS_PS = {"complex64": 2.5e9, "complex128": 1.2e9}
 RESIDENT_BLOCKS = {"complex64": 296, "complex128": 296}
-SMALL_LOAD_S = 40e-9
+SMALL_LOAD_S = 0.65e-6
 MIN_TILE_BITS = {"complex64": 9, "complex128": 8}   # vector path needs VEC*NT results
 # QTN_MERGE=0 disables chain merging (A/B measurements)
 MERGE_DEFAULT = os.environ.get("QTN_MERGE", "1") != "0"
@@ -211,7 +212,10 @@ def _item_cost(w, k, L, sizes, dtype):
     if nelem >= VEC[dtype] * NT:
         per_tile = (nelem << k) * nm / BLOCK_TERMS_PS[dtype]
     else:
-        per_tile = 1e-6 + -(-(nelem << k) // NT) * nm * SMALL_LOAD_S
+        # K2: each thread handles 4 (element, assignment) units per round and
+        # every member of a round is one dependent L2 round trip
+        rounds = -(-(nelem << k) // (4 * NT))
+        per_tile = 1e-6 + rounds * nm * SMALL_LOAD_S
     return HOP_S + max(byt / BW_BPS, waves * per_tile)
 
 
@@ -678,6 +682,7 @@ class Executor:
             c.arena = self.arena.data_ptr()
             c.results = self.results.data_ptr()
             c.timing = self.timing.data_ptr() if timing else None
+            c.arena_elems = prog.arena_elems
             self.c = c
             torch.cuda.synchronize(dev)
             g = ctypes.c_void_p()

@@ -1,0 +1,94 @@
+"""N > 1 path on CPU: LPT sharding of (cone, slice) units and the slot-vector
+all-reduce, world_size 2 over gloo.  Each rank executes its units with the
+numpy program interpreter (tests/emulator.py) in place of the device run, so
+the host logic (plan_units, lpt_assign, run_units, _combine) is exactly the
+product's.  Checks: energies equal the single-rank result bit for bit and the
+golden reference energy."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT, load_json
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _emulated_run_local(plan, mine, backend, device, budget_bytes=None):
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from emulator import run_program
+    from paper_2210_15874_b200 import engine as E
+    vals, stats = {}, {}
+    for u in mine:
+        unit = plan.units[u]
+        prog = E.Program([E.Instance(plan.templates[unit.cone], unit.assignment)], backend.dtype)
+        vals[u] = complex(run_program(prog, [plan.raws[unit.cone]])[0])
+    return vals, stats
+
+
+def _energy(world, rank, port, out, slice_target):
+    import paper_2210_15874_b200 as Q
+    from paper_2210_15874_b200 import distributed as D
+    if world > 1:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    D.run_local = _emulated_run_local
+    g = load_json("qaoa.json")["cfg1"]
+    graph = Q.Graph(g["n"], tuple(tuple(e) for e in g["edges"]))
+    params = Q.QaoaParams(g["p"], g["gammas"], g["betas"])
+    be = Q.Backend.b200(dtype="complex128")
+    c = Q.qaoa_maxcut_circuit(graph, params)
+    cones = [Q.extract_lightcone(c, e) for e in graph.edges]
+    plan = D.plan_units(cones, be, slice_target=slice_target)
+    vals, _ = D.run_units(plan, be)
+    e = sum(0.5 * (1.0 - v.real) for v in vals)
+    owner = D.lpt_assign([u.cost for u in plan.units], max(world, 1))
+    out[rank] = (e, len(plan.units), owner)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _worker(rank, world, port, out, slice_target):
+    _energy(world, rank, port, out, slice_target)
+
+
+@pytest.mark.parametrize("slice_target", [None, 2])
+def test_gloo_world2_matches_single_rank(slice_target):
+    single = {}
+    _energy(1, 0, 0, single, slice_target)
+    e1, n_units, _ = single[0]
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    mp.spawn(_worker, args=(2, port, out, slice_target), nprocs=2, join=True)
+    g = load_json("qaoa.json")["cfg1"]
+    for r in (0, 1):
+        e, n, owner = out[r]
+        assert n == n_units
+        assert e == e1                         # bitwise: one contributor per slot
+        assert set(owner) == {0, 1}            # both ranks got work
+    assert abs(e1 - g["energy"]) < 1e-10
+    if slice_target is not None:
+        assert n_units > len(g["cones"])       # some cones were sliced
+
+
+def test_lpt_assignment_balanced_and_deterministic():
+    from paper_2210_15874_b200 import distributed as D
+    rng = np.random.default_rng(0)
+    costs = [int(x) for x in rng.integers(1, 1000, size=45)]
+    for n in (1, 2, 4, 8):
+        own = D.lpt_assign(costs, n)
+        assert own == D.lpt_assign(costs, n)
+        loads = [sum(c for c, o in zip(costs, own) if o == r) for r in range(n)]
+        assert max(loads) - min(loads) <= max(costs)
