@@ -225,8 +225,9 @@ PLAN_CACHE = _PlanCache()
 
 
 def _raw_inputs(tn: TensorNetwork) -> np.ndarray:
-    parts = [np.asarray(t.data, dtype=np.complex128).ravel() for t in tn.tensors]
-    return np.concatenate(parts) if parts else np.zeros(0, np.complex128)
+    parts = [t.data.ravel() for t in tn.tensors]
+    raw = np.concatenate(parts) if parts else np.zeros(0, np.complex128)
+    return raw if raw.dtype == np.complex128 else raw.astype(np.complex128)
 
 
 def _template(tn, order, backend, fixed=()):
@@ -267,12 +268,21 @@ def ref_stats(tmpl, backend, item_elapsed=None):
             for w, e in zip(tmpl.ref_w, el)]
 
 
+_NOPROFILE_STATS = {}
+
+
 def _stats(tmpl, ex, backend, inst=0):
     if backend.profile:
         t0, t1 = ex.fetch_timing()
         gids = ex.prog.bucket_gid[inst]
         return ref_stats(tmpl, backend, np.maximum(t1[gids] - t0[gids], 0))
-    return ref_stats(tmpl, backend)
+    # widths are fixed by the plan; BucketStats are immutable, so the list is
+    # built once per (template, threshold) and copied
+    key = (id(tmpl), backend.threshold)
+    hit = _NOPROFILE_STATS.get(key)
+    if hit is None or hit[0] is not tmpl:
+        hit = _NOPROFILE_STATS[key] = (tmpl, ref_stats(tmpl, backend))
+    return list(hit[1])
 
 
 def contract_network(tn: TensorNetwork, order, backend: Backend = None, mem_cap: int = DEFAULT_MEM_CAP):
@@ -285,10 +295,7 @@ def contract_network(tn: TensorNetwork, order, backend: Backend = None, mem_cap:
     backend = backend or Backend()
     if tn.open_indices:
         raise ValueError("contract_network requires a closed network")
-    missing = tn.all_indices() - set(order)
-    if missing:
-        raise ValueError(f"order is missing indices: {sorted(missing)}")
-    key, tmpl = _template(tn, order, backend)
+    key, tmpl = _template(tn, order, backend)   # raises for indices missing from the order
     _check_cap(tmpl, backend, mem_cap)
     ex, lock = _executor(key, lambda: E.Program([E.Instance(tmpl)], backend.dtype), backend, 1)
     raw = _raw_inputs(tn)
