@@ -39,6 +39,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -148,6 +149,13 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// Programmatic dependent launch (PDL): a kernel lets its graph successors
+// launch as soon as all of its blocks are running, and a successor waits for
+// its predecessors' completion (and memory) only where it first reads their
+// outputs — launch latency and table prologues overlap the predecessor.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 [[maybe_unused]] __device__ __forceinline__ uint32_t dyn_smem_bytes() {
   uint32_t v;
   asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(v));
@@ -219,6 +227,8 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
   uint32_t pend_cnt = 0;   // thread 0: finished, unpublished tiles of pend_item
   int pend_item = 0;
 
+  pdl_launch_dependents();
+  pdl_wait();   // predecessor nodes' outputs (and this stage's ctrl reset) visible
   if (tid == 0) S.next = (int)atomicAdd(&ctl[0], 1u);
   for (;;) {
     __syncthreads();
@@ -314,35 +324,47 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
       if (tid < nm) S.base[tid] = S.off[tid] + (pext64((uint64_t)h, S.mhi[tid]) << S.pclo[tid]);
       __syncthreads();
       T* out = Aw + S.b.out_off + (uint64_t)h * (uint64_t)nelem;
-      // threads cover (element, assignment) pairs, 4 per thread per round with
-      // every member load issued before the multiplies
+      // threads cover (element, assignment) pairs, UJ per thread per round;
+      // every member's loads of a round are issued before any multiply (one
+      // L2 round trip per round instead of one per member)
+      constexpr int UJ = 2;
       const int chunk = max(1, min(ns, SMALL_PROD_ELEMS / nelem));
       T acc = T{};
       for (int s0 = 0; s0 < ns; s0 += chunk) {
         const int cs = min(chunk, ns - s0);
         const int nu = cs * nelem;
-        for (int u0 = tid; u0 < nu; u0 += 4 * NT) {
-          T prod[4];
-          for (int i = 0; i < nm; ++i) {
-            T x[4];
+        for (int u0 = tid; u0 < nu; u0 += UJ * NT) {
+          int ue[UJ], us[UJ];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int u = min(u0 + j * NT, nu - 1);
-              const int e = u & (nelem - 1), sc = s0 + (u >> L);
-              const uint64_t o = S.base[i] + ((uint64_t)S.sig[i][sc] << S.pc[i]) +
-                                 (S.pclo[i] == L ? (uint64_t)e : (uint64_t)pext32((uint32_t)e, S.mlo[i]));
-              QTN_CHECK(QTN_ARENA_OK(P, o), "small item %d member %d off %lld", cur, i, (long long)o);
-              x[j] = __ldcg(A + o);
+          for (int j = 0; j < UJ; ++j) {
+            const int u = min(u0 + j * NT, nu - 1);
+            ue[j] = u & (nelem - 1);
+            us[j] = s0 + (u >> L);
+          }
+          T x[MAXM][UJ];
+#pragma unroll
+          for (int i = 0; i < MAXM; ++i) {
+            if (i < nm) {
+#pragma unroll
+              for (int j = 0; j < UJ; ++j) {
+                const uint64_t o = S.base[i] + ((uint64_t)S.sig[i][us[j]] << S.pc[i]) +
+                                   (S.pclo[i] == L ? (uint64_t)ue[j] : (uint64_t)pext32((uint32_t)ue[j], S.mlo[i]));
+                QTN_CHECK(QTN_ARENA_OK(P, o), "small item %d member %d off %lld", cur, i, (long long)o);
+                x[i][j] = __ldcg(A + o);
+              }
             }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) prod[j] = (i == 0) ? x[j] : cmul(prod[j], x[j]);
           }
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
+          for (int j = 0; j < UJ; ++j) {
+            T prod = x[0][j];
+#pragma unroll
+            for (int i = 1; i < MAXM; ++i)
+              if (i < nm) prod = cmul(prod, x[i][j]);
             if (u0 + j * NT < nu) {
               QTN_CHECK((u0 + j * NT + 1) * (int)sizeof(T) <= (int)dyn_smem_bytes(), "sprod %d", u0 + j * NT);
-              sprod[u0 + j * NT] = prod[j];
+              sprod[u0 + j * NT] = prod;
             }
+          }
         }
         __syncthreads();
         if (tid < nelem)
@@ -715,11 +737,13 @@ __global__ void __launch_bounds__(NT) large_kernel(const qtn_program_t P, int32_
   const T* A = reinterpret_cast<const T*>(P.arena);
   T* Aw = reinterpret_cast<T*>(P.arena);
   const int tid = threadIdx.x;
+  pdl_launch_dependents();
   if (tid == 0) {
     mbar_init(&bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  large_prep<R>(S, P, item);
+  large_prep<R>(S, P, item);   // static tables only
+  pdl_wait();                  // predecessors complete: their outputs are readable
   unsigned long long t_start = 0;
   if (P.timing && tid == 0) t_start = globaltimer();
   uint32_t phase = 0;
@@ -934,6 +958,8 @@ int qtn_graph_create(const qtn_program_t* p, const qtn_node_t* nodes, int32_t n_
   }
   std::vector<cudaGraphNode_t> gn(n_nodes);
   std::vector<LaunchSpec> specs(n_nodes);
+  const char* pdl_env = getenv("QTN_PDL");
+  const bool use_pdl = !(pdl_env && pdl_env[0] == '0');
   for (int i = 0; i < n_nodes; ++i) {
     const qtn_node_t& nd = nodes[i];
     if (nd.kind == QTN_NODE_LARGE && (nd.first < 0 || nd.first >= p->n_buckets)) {
@@ -961,10 +987,22 @@ int qtn_graph_create(const qtn_program_t* p, const qtn_node_t* nodes, int32_t n_
     kp.blockDim = dim3(NT);
     kp.sharedMemBytes = specs[i].smem;
     kp.kernelParams = specs[i].args;
-    e = cudaGraphAddKernelNode(&gn[i], g->graph, deps.empty() ? nullptr : deps.data(), deps.size(), &kp);
+    e = cudaGraphAddKernelNode(&gn[i], g->graph, nullptr, 0, &kp);
     if (e != cudaSuccess) {
       qtn_graph_destroy(g);
       return cuda_err(e, "cudaGraphAddKernelNode");
+    }
+    // programmatic edges (PDL): the kernels call griddepcontrol.wait before
+    // reading predecessor outputs
+    for (cudaGraphNode_t from : deps) {
+      cudaGraphEdgeData ed = {};
+      ed.from_port = use_pdl ? cudaGraphKernelNodePortProgrammatic : cudaGraphKernelNodePortDefault;
+      ed.type = use_pdl ? cudaGraphDependencyTypeProgrammatic : cudaGraphDependencyTypeDefault;
+      e = cudaGraphAddDependencies_v2(g->graph, &from, &gn[i], &ed, 1);
+      if (e != cudaSuccess) {
+        qtn_graph_destroy(g);
+        return cuda_err(e, "cudaGraphAddDependencies_v2");
+      }
     }
   }
   e = cudaGraphInstantiate(&g->exec, g->graph, 0);

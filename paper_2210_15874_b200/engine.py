@@ -70,12 +70,15 @@ VEC = {"complex64": 2, "complex128": 1}
 # evaluates ~2.5e9 member-terms/s when every SM is shared by ~5 blocks; a
 # small-tile round is L2-latency bound (~0.65 us per dependent member load,
 # measured on the r01 K2 timeline).
-HOP_S = 5.0e-6
+HOP_S = 5.0e-6            # K1 graph node
+HOP_K2_S = 1.5e-6         # item inside a K2 stage
 BW_BPS = 5.5e12
 BLOCK_TERMS_PS = {"complex64": 2.5e9, "complex128": 1.2e9}
 RESIDENT_BLOCKS = {"complex64": 296, "complex128": 296}
 SMALL_LOAD_S = 0.65e-6
 MIN_TILE_BITS = {"complex64": 9, "complex128": 8}   # vector path needs VEC*NT results
+SMALL_ITER_BITS = int(os.environ.get("QTN_SMALL_ITER", "12"))  # items with w + k <= this run in K2
+SMALL_TILE_BITS = {"complex64": 8, "complex128": 7}  # K2 tiles: below one vector step
 # QTN_MERGE=0 disables chain merging (A/B measurements)
 MERGE_DEFAULT = os.environ.get("QTN_MERGE", "1") != "0"
 
@@ -201,9 +204,10 @@ def kernel_variant(w, k, L, cls, dtype):
     return VARIANT_GENERIC
 
 
-def _item_cost(w, k, L, sizes, dtype):
+def _item_cost(w, k, L, sizes, dtype, hop=None):
     """Estimated device time of one item: dependency hop + max(streaming,
     per-tile term evaluation x waves of tiles)."""
+    hop = HOP_S if hop is None else hop
     nm = max(1, len(sizes))
     byt = ELEM_BYTES[dtype] * ((1 << w) + sum(sizes))
     tiles = 1 << (w - L)
@@ -212,16 +216,20 @@ def _item_cost(w, k, L, sizes, dtype):
     if nelem >= VEC[dtype] * NT:
         per_tile = (nelem << k) * nm / BLOCK_TERMS_PS[dtype]
     else:
-        # K2: each thread handles 4 (element, assignment) units per round and
-        # every member of a round is one dependent L2 round trip
-        rounds = -(-(nelem << k) // (4 * NT))
-        per_tile = 1e-6 + rounds * nm * SMALL_LOAD_S
-    return HOP_S + max(byt / BW_BPS, waves * per_tile)
+        # K2: each thread handles 2 (element, assignment) units per round; all
+        # member loads of a round are in flight together (one L2 round trip)
+        rounds = -(-(nelem << k) // (2 * NT))
+        per_tile = 1e-6 + rounds * SMALL_LOAD_S
+    return hop + max(byt / BW_BPS, waves * per_tile)
 
 
 def _cost_of(it, dtype):
     masks, smasks = _masks(it["members"], it["X"], it["R"])
-    L, _ = _tile_bits(len(it["R"]), masks, smasks, dtype)
+    w, k = len(it["R"]), len(it["X"])
+    if w + k <= SMALL_ITER_BITS:
+        L = min(w, SMALL_TILE_BITS[dtype])
+        return _item_cost(w, k, L, [1 << len(s2) for _, _, s2 in it["members"]], dtype, hop=HOP_K2_S)
+    L, _ = _tile_bits(w, masks, smasks, dtype)
     return _item_cost(len(it["R"]), len(it["X"]), L, [1 << len(s2) for _, _, s2 in it["members"]], dtype)
 
 
@@ -321,11 +329,13 @@ def plan_template(index_sets, order, dtype, fixed=(), merge=None):
                 if len(X2) > KMAX or len(mem2) > N.MAX_MEMBERS:
                     continue
                 w = len(R)
-                masks, smasks = _masks(mem2, X2, R)
-                L, _ = _tile_bits(w, masks, smasks, dtype)
-                if L < min(w, MIN_TILE_BITS[dtype]):
-                    continue
-                c2 = _item_cost(w, len(X2), L, [1 << len(s2) for _, _, s2 in mem2], dtype)
+                cand = {"X": X2, "R": R, "members": mem2}
+                if w + len(X2) > SMALL_ITER_BITS:
+                    masks, smasks = _masks(mem2, X2, R)
+                    L, _ = _tile_bits(w, masks, smasks, dtype)
+                    if L < min(w, MIN_TILE_BITS[dtype]):
+                        continue
+                c2 = _cost_of(cand, dtype)
                 if c2 >= it["cost"] + p_["cost"]:
                     continue
                 it["X"], it["members"], it["cost"] = X2, mem2, c2
@@ -348,7 +358,12 @@ def plan_template(index_sets, order, dtype, fixed=(), merge=None):
         R, X = it["R"], it["X"]
         w, k = len(R), len(X)
         masks, smasks = _masks(it["members"], X, R)
-        L, st = _tile_bits(w, masks, smasks, dtype)
+        if w + k <= SMALL_ITER_BITS:
+            # small iteration space: K2 stage, scalar-path tiles (latency-bound
+            # work; a K2 dependency hop costs ~1.5 us against ~7 us for a K1 node)
+            L, st = min(w, SMALL_TILE_BITS[dtype]), 0
+        else:
+            L, st = _tile_bits(w, masks, smasks, dtype)
         lv = 0
         for (k_, r_, _), m, sm in zip(it["members"], masks, smasks):
             if k_ == 1:

@@ -50,3 +50,36 @@ for r in rows:
     if r[2] >= 12 or r[7] > 1:
         d = r[1] - r[0]
         print(f"{r[0]/1e3:8.1f} {r[1]/1e3:8.1f} {d/1e3:8.1f} {r[2]:2d} {r[7]:2d} {r[3]:2d} {r[4]:6d} {r[5]:3d} {r[6]/1e6:7.1f} {r[6]/max(d,1):7.0f}")
+
+# ---- critical path: walk back from the last-finishing item through the
+# producer that finished last ----
+gid_rows = {}
+for gid in range(prog.n_buckets):
+    gid_rows[gid] = (t0[gid] - origin, t1[gid] - origin)
+node_of = {}
+for ni, nd in enumerate(prog.nodes):
+    for gg in range(int(nd["first"]), int(nd["first"]) + int(nd["count"])):
+        node_of[gg] = (ni, int(nd["kind"]), int(nd["variant"]))
+# producers per item (global ids) from the member offsets
+out_of = {}
+for gid in range(prog.n_buckets):
+    b = B[gid]
+    if b["w"] >= 0:
+        out_of[int(b["out_off"])] = gid
+def producers(gid):
+    b = B[gid]
+    mem = prog.members[b["mem_begin"]: b["mem_begin"] + b["n_mem"]]
+    return [out_of[int(m["off"])] for m in mem if int(m["off"]) in out_of]
+cur = max(gid_rows, key=lambda g: gid_rows[g][1])
+path = []
+while cur is not None:
+    path.append(cur)
+    ps = producers(cur)
+    cur = max(ps, key=lambda g: gid_rows[g][1]) if ps else None
+print("critical path (first -> last): start end dur | w k L tiles nmem | node kind variant")
+for gid in reversed(path):
+    b = B[gid]
+    s_, e_ = gid_rows[gid]
+    ni, kind, var = node_of[gid]
+    print(f"  {s_/1e3:7.1f} {e_/1e3:7.1f} {(e_-s_)/1e3:6.1f} | {int(b['w']):3d} {int(b['k'])} {int(b['tile_bits']):2d} "
+          f"{int(b['n_tiles']):5d} {int(b['n_mem'])} | node {ni:3d} {'K2' if kind == 0 else 'K1'} {var:#x}")
