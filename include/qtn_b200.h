@@ -138,7 +138,8 @@ typedef struct {
  *    specialised by `variant`. */
 enum { QTN_NODE_SMALL = 0, QTN_NODE_LARGE = 1 };
 #define QTN_VARIANT_GENERIC (-1)
-/* variant = log2(2^k) | (varying staged members) << 4 | (one streamed member) << 8,
+/* variant = log2(2^k) | (varying staged members) << 4 | (one streamed member) << 8
+ *         | (varying members carrying result bit 0, complex64) << 12,
  * for k <= 3 and at most 4 varying members; otherwise QTN_VARIANT_GENERIC. */
 typedef struct {
   int32_t kind;

@@ -435,7 +435,7 @@ struct LargeCtx {
 // mapping (v -> bit 0 for c64, lane -> the next 5 bits for coalesced warp
 // stores, warp and step bits -> the rest; step bits = the item's stmask).
 template <typename R>
-__device__ __forceinline__ void large_prep(LargeCtx& S, const qtn_program_t& P, int item) {
+__device__ __forceinline__ void large_prep(LargeCtx& S, const qtn_program_t& P, int item, int nb0_expected) {
   using T = typename Cx<R>::T;
   constexpr int VEC = Cx<R>::VEC;
   constexpr int EPV = 16 / (int)sizeof(T);
@@ -482,7 +482,21 @@ __device__ __forceinline__ void large_prep(LargeCtx& S, const qtn_program_t& P, 
         if (S.seglen[i] * (int)sizeof(T) >= 16) nb += S.nsig[i];
       }
       if (c == QTN_CLS_UNIFORM) hu = 1;
-      if (c == QTN_CLS_VARYING) S.vlist[nv++] = i;
+    }
+    // varying members, those carrying result bit 0 first (their v pairs are
+    // adjacent in smem: one 16-byte gather; c64 only)
+    int nb0 = 0;
+    for (int pass = 0; pass < 2; ++pass)
+      for (int i = 0; i < nm; ++i)
+        if (S.cls[i] == QTN_CLS_VARYING && (int)(S.mlo[i] & 1u) == 1 - pass) {
+          S.vlist[nv++] = i;
+          nb0 += 1 - pass;
+        }
+    // planner / kernel contract (always checked, once per block): the
+    // specialisation must match the item's varying-member layout
+    if (nb0_expected >= 0 && VEC == 2 && nb0 != nb0_expected) {
+      printf("qtn_b200: item %d has %d bit-0 varying members, kernel variant expects %d\n", item, nb0, nb0_expected);
+      __trap();
     }
     S.s0m = sm;
     S.has_u = hu;
@@ -563,7 +577,7 @@ __device__ __forceinline__ void large_stage(LargeCtx& S, const typename Cx<R>::T
 // Compute tile h (after large_stage): fully unrolled over the NS summed
 // assignments and the NV varying members; per-thread smem addresses and run
 // offsets live in registers.
-template <typename R, int NS, int NV, int ST>
+template <typename R, int NS, int NV, int ST, int NB0>
 __device__ __forceinline__ void large_compute(const LargeCtx& S, const typename Cx<R>::T* __restrict__ A,
                                               const typename Cx<R>::T* sseg, typename Cx<R>::T* out) {
   using T = typename Cx<R>::T;
@@ -574,14 +588,13 @@ __device__ __forceinline__ void large_compute(const LargeCtx& S, const typename 
   const int nst = (1 << S.b.tile_bits) / (VEC * NT);
   const T* qv[NV > 0 ? NV : 1];
   int ro[NV > 0 ? NV : 1][NS];
-  int b0[NV > 0 ? NV : 1];
   int vi[NV > 0 ? NV : 1];
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
     const int i = S.vlist[j];
     vi[j] = i;
     qv[j] = sseg + S.seg[i] + S.gt[i][tid];
-    b0[j] = (int)(S.mlo[i] & 1u);
+    QTN_CHECK(VEC == 1 || (int)(S.mlo[i] & 1u) == (j < NB0 ? 1 : 0), "vlist/NB0 mismatch item member %d", i);
 #pragma unroll
     for (int c = 0; c < NS; ++c) ro[j][c] = S.sig[i][c] << S.pclo[i];
   }
@@ -650,15 +663,11 @@ __device__ __forceinline__ void large_compute(const LargeCtx& S, const typename 
                       S.gt[vi[j]][tid] + S.gs[vi[j]][st] + ro[j][c] < S.nsig[vi[j]] * S.seglen[vi[j]],
                   "staged gather member %d", vi[j]);
         T x[VEC];
-        if (VEC == 2) {
-          if (b0[j]) {
-            split(*reinterpret_cast<const V*>(q + ro[j][c]), x);
-          } else {
-            x[0] = q[ro[j][c]];
-            x[VEC - 1] = x[0];
-          }
+        if (VEC == 2 && j < NB0) {
+          split(*reinterpret_cast<const V*>(q + ro[j][c]), x);   // adjacent v pair
         } else {
-          x[0] = q[ro[j][c]];
+          x[0] = q[ro[j][c]];                                     // member constant in v
+          x[VEC - 1] = x[0];
         }
 #pragma unroll
         for (int v = 0; v < VEC; ++v) prod[c][v] = started ? cmul(prod[c][v], x[v]) : x[v];
@@ -727,7 +736,7 @@ __device__ __forceinline__ void large_compute_generic(const LargeCtx& S, const t
 }
 
 // NS < 0: generic compute.
-template <typename R, int NS, int NV, int ST>
+template <typename R, int NS, int NV, int ST, int NB0>
 __global__ void __launch_bounds__(NT) large_kernel(const qtn_program_t P, int32_t item) {
   using T = typename Cx<R>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -742,7 +751,7 @@ __global__ void __launch_bounds__(NT) large_kernel(const qtn_program_t P, int32_
     mbar_init(&bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  large_prep<R>(S, P, item);   // static tables only
+  large_prep<R>(S, P, item, NS > 0 ? NB0 : -1);   // static tables only
   pdl_wait();                  // predecessors complete: their outputs are readable
   unsigned long long t_start = 0;
   if (P.timing && tid == 0) t_start = globaltimer();
@@ -753,7 +762,7 @@ __global__ void __launch_bounds__(NT) large_kernel(const qtn_program_t P, int32_
     large_stage<R>(S, A, sseg, &bar, phase, h, P);
     T* out = Aw + S.b.out_off + (uint64_t)h * nelem;
     if (NS > 0)
-      large_compute<R, (NS > 0 ? NS : 2), NV, ST>(S, A, sseg, out);
+      large_compute<R, (NS > 0 ? NS : 2), NV, ST, NB0>(S, A, sseg, out);
     else
       large_compute_generic<R>(S, A, sseg, out);
     __syncthreads();
@@ -789,28 +798,42 @@ __global__ void permute_kernel(const typename Cx<RS>::T* __restrict__ src, int64
 // =========================================================================
 using LargeFn = void (*)(const qtn_program_t, int32_t);
 
+template <typename R, int NS, int NV, int ST>
+LargeFn large_fn_nb0(int nb0) {
+  if (Cx<R>::VEC == 1) return large_kernel<R, NS, NV, ST, 0>;
+  switch (nb0) {
+    case 0: return large_kernel<R, NS, NV, ST, 0>;
+    case 1: return NV >= 1 ? large_kernel<R, NS, NV, ST, (NV >= 1 ? 1 : 0)> : nullptr;
+    case 2: return NV >= 2 ? large_kernel<R, NS, NV, ST, (NV >= 2 ? 2 : 0)> : nullptr;
+    case 3: return NV >= 3 ? large_kernel<R, NS, NV, ST, (NV >= 3 ? 3 : 0)> : nullptr;
+    case 4: return NV >= 4 ? large_kernel<R, NS, NV, ST, (NV >= 4 ? 4 : 0)> : nullptr;
+    default: return nullptr;
+  }
+}
+
+template <typename R, int NS, int ST>
+LargeFn large_fn_nv(int nv, int nb0) {
+  switch (nv) {
+    case 0: return large_fn_nb0<R, NS, 0, ST>(nb0);
+    case 1: return large_fn_nb0<R, NS, 1, ST>(nb0);
+    case 2: return large_fn_nb0<R, NS, 2, ST>(nb0);
+    case 3: return large_fn_nb0<R, NS, 3, ST>(nb0);
+    case 4: return large_fn_nb0<R, NS, 4, ST>(nb0);
+    default: return nullptr;
+  }
+}
+
+// variant = log2(2^k) | nv << 4 | streamed << 8 | nb0 << 12 (see qtn_b200.h)
 template <typename R>
 LargeFn large_fn(int variant) {
-  if (variant < 0) return large_kernel<R, -1, 0, 0>;
-  const int ks = variant & 15, nv = (variant >> 4) & 15, st = (variant >> 8) & 1;
-#define QTN_NV_CASES(NS, ST)                   \
-  switch (nv) {                                \
-    case 0: return large_kernel<R, NS, 0, ST>; \
-    case 1: return large_kernel<R, NS, 1, ST>; \
-    case 2: return large_kernel<R, NS, 2, ST>; \
-    case 3: return large_kernel<R, NS, 3, ST>; \
-    case 4: return large_kernel<R, NS, 4, ST>; \
-    default: return large_kernel<R, -1, 0, 0>; \
+  LargeFn f = nullptr;
+  if (variant >= 0) {
+    const int ks = variant & 15, nv = (variant >> 4) & 15, st = (variant >> 8) & 1, nb0 = (variant >> 12) & 15;
+    if (ks == 1) f = st ? large_fn_nv<R, 2, 1>(nv, nb0) : large_fn_nv<R, 2, 0>(nv, nb0);
+    else if (ks == 2) f = st ? large_fn_nv<R, 4, 1>(nv, nb0) : large_fn_nv<R, 4, 0>(nv, nb0);
+    else if (ks == 3) f = st ? large_fn_nv<R, 8, 1>(nv, nb0) : large_fn_nv<R, 8, 0>(nv, nb0);
   }
-  if (ks == 1) {
-    if (st) { QTN_NV_CASES(2, 1) } else { QTN_NV_CASES(2, 0) }
-  } else if (ks == 2) {
-    if (st) { QTN_NV_CASES(4, 1) } else { QTN_NV_CASES(4, 0) }
-  } else if (ks == 3) {
-    if (st) { QTN_NV_CASES(8, 1) } else { QTN_NV_CASES(8, 0) }
-  }
-#undef QTN_NV_CASES
-  return large_kernel<R, -1, 0, 0>;
+  return f ? f : large_kernel<R, -1, 0, 0, 0>;
 }
 
 int sm_count() {

@@ -192,7 +192,7 @@ def member_classes(w, k, L, stm, masks):
     return out
 
 
-def kernel_variant(w, k, L, cls, dtype):
+def kernel_variant(w, k, L, cls, dtype, masks=()):
     """K2 small stage for tiles below one vector step; otherwise the K1
     specialisation (2^k, varying members, streamed) or the generic kernel."""
     if (1 << L) < VEC[dtype] * NT:
@@ -200,7 +200,9 @@ def kernel_variant(w, k, L, cls, dtype):
     nv = sum(1 for c in cls if c == CLS_VARYING)
     nst = sum(1 for c in cls if c == CLS_STREAMED)
     if k <= 3 and nv <= 4 and nst <= 1:
-        return k | (nv << 4) | (nst << 8)
+        # varying members carrying result bit 0 (c64: 16-byte v-pair gathers)
+        nb0 = sum(1 for c, m in zip(cls, masks) if c == CLS_VARYING and m & 1) if VEC[dtype] == 2 else 0
+        return k | (nv << 4) | (nst << 8) | (nb0 << 12)
     return VARIANT_GENERIC
 
 
@@ -335,6 +337,8 @@ def plan_template(index_sets, order, dtype, fixed=(), merge=None):
                     L, _ = _tile_bits(w, masks, smasks, dtype)
                     if L < min(w, MIN_TILE_BITS[dtype]):
                         continue
+                if w + len(X2) > SMALL_ITER_BITS and len(X2) > 3:
+                    continue   # would need the generic K1 kernel (no k > 3 specialisation)
                 c2 = _cost_of(cand, dtype)
                 if c2 >= it["cost"] + p_["cost"]:
                     continue
@@ -381,7 +385,7 @@ def plan_template(index_sets, order, dtype, fixed=(), merge=None):
         stm.append(sm_)
         cls_ = member_classes(w, k, L, sm_, masks)
         mcls.extend(cls_)
-        var.append(kernel_variant(w, k, L, cls_, dtype))
+        var.append(kernel_variant(w, k, L, cls_, dtype, masks))
         inter += size
         for r_ in it["refs"]:
             ref_item[r_] = new

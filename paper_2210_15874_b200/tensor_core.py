@@ -241,7 +241,7 @@ class _BucketLauncher:
         small = (1 << L) < E.VEC[dtype] * E.NT
         stm = 0 if small else E._step_mask(L, masks, dtype)
         mcls = E.member_classes(w, 1, L, stm, masks)
-        variant = E.kernel_variant(w, 1, L, mcls, dtype)
+        variant = E.kernel_variant(w, 1, L, mcls, dtype, masks)
         B = np.zeros(1, N.BUCKET_DT)
         B["out_off"] = out.data_ptr() // esz
         B["w"] = w

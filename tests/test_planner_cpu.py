@@ -166,3 +166,26 @@ def test_plan_masks_follow_canonical_layout():
     # algorithmic bytes of the cfg-2 cone (1.468 GB c64)
     gb = E.algorithmic_bytes(t, "complex64") / 1e9
     assert gb == pytest.approx(1.468, abs=0.01)
+
+
+def test_kernel_variants_match_member_layout():
+    """The K1 specialisation encoded by the planner must agree with the member
+    classes the kernel derives (a mismatch would make the kernel gather wrong
+    values; the kernel also traps on it)."""
+    g, graph, params = _cfg("cfg2")
+    c = Q.qaoa_maxcut_circuit(graph, params)
+    for dtype in ("complex64", "complex128"):
+        for edge in [(0, 15), (0, 11)]:
+            lc = Q.extract_lightcone(c, edge, cone="tight")
+            t = E.plan_template([x.indices for x in lc.network.tensors], Q.greedy_order(lc.network), dtype)
+            for i in range(t.n_items):
+                v = int(t.variant[i])
+                if v < 0:
+                    continue
+                cls = [int(t.mem_cls[j]) for j in range(t.mem_ptr[i], t.mem_ptr[i + 1])]
+                masks = [int(t.mem_mask[j]) for j in range(t.mem_ptr[i], t.mem_ptr[i + 1])]
+                assert v & 15 == int(t.k[i])
+                assert (v >> 4) & 15 == sum(1 for x in cls if x == E.CLS_VARYING)
+                assert (v >> 8) & 1 == sum(1 for x in cls if x == E.CLS_STREAMED)
+                nb0 = sum(1 for x, m in zip(cls, masks) if x == E.CLS_VARYING and m & 1)
+                assert (v >> 12) & 15 == (nb0 if dtype == "complex64" else 0)
