@@ -94,7 +94,9 @@ def _batches(units, plan, backend, budget_bytes):
     cur, cur_b = [], 0
     for ui in units:
         t = plan.templates[plan.units[ui].cone]
-        b = (t.n_in_elems + t.n_inter_elems) * esz + 4096
+        if not hasattr(t, "_peak"):
+            t._peak = E.template_peak_elems(t)
+        b = (t.n_in_elems + t._peak) * esz + 4096
         if cur and cur_b + b > budget_bytes:
             yield cur
             cur, cur_b = [], 0
@@ -102,6 +104,44 @@ def _batches(units, plan, backend, budget_bytes):
         cur_b += b
     if cur:
         yield cur
+
+
+@dataclass
+class Prepared:
+    """Executors for one rank's units, built once (plans, graphs, HBM) and
+    re-run many times (bench loop / parameter sweeps over the same structure)."""
+    batches: list          # [(Executor, [unit ids])]
+    raws: list
+
+
+def prepare_local(plan: UnitPlan, mine, backend: Backend, device: int, budget_bytes=None) -> Prepared:
+    import torch
+    if budget_bytes is None:
+        free, _ = torch.cuda.mem_get_info(device)
+        budget_bytes = int(0.6 * free)
+    be = Backend(backend.kind, backend.threshold, backend.dtype, device, backend.profile)
+    out = []
+    for batch in _batches(mine, plan, be, budget_bytes):
+        insts = [E.Instance(plan.templates[plan.units[u].cone], plan.units[u].assignment) for u in batch]
+        ex = E.Executor(E.Program(insts, be.dtype), device=device, timing=be.profile)
+        ex.stage_inputs([plan.raws[plan.units[u].cone] for u in batch])
+        out.append((ex, batch))
+    return Prepared(out, plan.raws)
+
+
+def launch_prepared(prep: Prepared, stream=None):
+    """Launch every batch (inputs already resident)."""
+    for ex, _ in prep.batches:
+        ex.launch(stream)
+
+
+def collect_prepared(prep: Prepared, stream=None) -> dict:
+    vals = {}
+    for ex, batch in prep.batches:
+        res = ex.fetch_results(stream)
+        for k, u in enumerate(batch):
+            vals[u] = complex(res[k])
+    return vals
 
 
 def run_local(plan: UnitPlan, mine, backend: Backend, device: int, budget_bytes=None):

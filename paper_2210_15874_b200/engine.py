@@ -39,6 +39,10 @@ DTYPE_CODE = {"complex64": N.QTN_C64, "complex128": N.QTN_C128}
 # tile bits: 2^L results per tile (4096 c64 / 2048 c128 = 32 KiB of output)
 TILE_BITS = {"complex64": 12, "complex128": 11}
 SMEM_BUDGET = 48 * 1024
+# intermediate-memory reuse (liveness + WAR dependencies): only for programs
+# whose no-reuse footprint exceeds this, and only for blocks >= REUSE_MIN_ELEMS
+REUSE_ABOVE_BYTES = int(float(os.environ.get("QTN_REUSE_ABOVE_GB", "16")) * (1 << 30))
+REUSE_MIN_ELEMS = 1 << 20
 NT = 256
 
 
@@ -444,6 +448,74 @@ def executed_bytes(t: Template, dtype) -> int:
     return tot * ELEM_BYTES[norm_dtype(dtype)]
 
 
+class _Pool:
+    """Best-fit arena allocator over element offsets with free-block
+    coalescing.  A freed block remembers the items that last READ it; an
+    allocation that reuses any of its memory inherits them as write-after-read
+    dependencies."""
+
+    def __init__(self, base):
+        self.top = base
+        self.free = []          # [start, size, readers(set)] sorted by start, coalesced
+
+    def alloc(self, size, align):
+        size = _align(size, align)
+        best = None
+        for bi, (st, sz, _) in enumerate(self.free):
+            a = _align(st, align)
+            if a + size <= st + sz and (best is None or sz < self.free[best][1]):
+                best = bi
+        if best is not None:
+            st, sz, rd = self.free.pop(best)
+            a = _align(st, align)
+            if a > st:
+                self._insert(st, a - st, set(rd))
+            if a + size < st + sz:
+                self._insert(a + size, st + sz - a - size, set(rd))
+            return a, set(rd)
+        if self.free and self.free[-1][0] + self.free[-1][1] == self.top:
+            st, sz, rd = self.free.pop()      # extend the top free block
+            a = _align(st, align)
+            if a > st:
+                self._insert(st, a - st, set(rd))
+            self.top = a + size
+            return a, set(rd)
+        a = _align(self.top, align)
+        self.top = a + size
+        return a, set()
+
+    def release(self, start, size, reader):
+        self._insert(start, size, {reader})
+
+    def _insert(self, st, sz, rd):
+        self.free.append([st, sz, rd])
+        self.free.sort(key=lambda blk: blk[0])
+        merged = []
+        for blk in self.free:
+            if merged and merged[-1][0] + merged[-1][1] == blk[0]:
+                merged[-1][1] += blk[1]
+                merged[-1][2] = merged[-1][2] | blk[2]
+            else:
+                merged.append(blk)
+        self.free = merged
+
+
+def template_peak_elems(t: Template) -> int:
+    """Peak intermediate elements of one instance under the liveness-based
+    reuse of Program (same allocator, items in level order)."""
+    order = sorted(range(t.n_items), key=lambda b: (int(t.level[b]), b))
+    pool = _Pool(0)
+    off = {}
+    for b in order:
+        size = 1 << int(t.w[b])
+        off[b], _ = pool.alloc(size, _tensor_align(size))
+        for j in range(t.mem_ptr[b], t.mem_ptr[b + 1]):
+            if t.mem_kind[j] == 1:
+                r = int(t.mem_ref[j])
+                pool.release(off[r], 1 << int(t.w[r]), b)
+    return pool.top
+
+
 @dataclass
 class Instance:
     template: Template
@@ -462,7 +534,7 @@ class Program:
     (that would be a cycle); dependencies inside a stage are per-item
     completion counters, across nodes they are graph edges."""
 
-    def __init__(self, instances, dtype):
+    def __init__(self, instances, dtype, reuse_above=None):
         self.dtype = norm_dtype(dtype)
         self.instances = list(instances)
         esz = ELEM_BYTES[self.dtype]
@@ -472,15 +544,8 @@ class Program:
             in_base.append(n_in)
             n_in += inst.template.n_in_elems
         n_in = _align(n_in, 32)
-        inter = n_in
-        inter_base = []
-        for inst in self.instances:
-            inter_base.append(inter)
-            inter += inst.template.n_inter_elems
         self.n_input_elems = n_in
-        self.arena_elems = max(_align(inter, 32), 32)
         self.in_base = in_base
-        self.inter_base = inter_base
 
         # ---- global item order (topological) ----
         keys = []
@@ -504,6 +569,38 @@ class Program:
                 ps = [order_gid[(i, int(r))] for kd, r in zip(t.fin_kind, t.fin_ref) if kd == 1]
             prods.append(ps)
 
+        # ---- intermediates: liveness-based reuse in item order ----
+        # An item's output is allocated before its inputs are released; a
+        # block freed by its reader R and reused by writer W makes W depend on
+        # R (write-after-read), folded into the graph / stage dependencies.
+        # Reuse costs concurrency (WAR edges), so it is used only when the
+        # program would not fit otherwise, and only for large blocks.
+        no_reuse = sum(inst.template.n_inter_elems for inst in self.instances) * esz
+        self.reuse = (REUSE_ABOVE_BYTES if reuse_above is None else reuse_above) < no_reuse
+        pool = _Pool(n_in)
+        small_pool = _Pool(0)   # never reused; placed after the reusable pool
+        out_elem, war = {}, [set() for _ in keys]
+        wid, in_small = {}, set()
+        for g, (_, i, b) in enumerate(keys):
+            if b >= 0:
+                size = 1 << int(self.instances[i].template.w[b])
+                wid[g] = size
+                if self.reuse and size >= REUSE_MIN_ELEMS:
+                    off, readers = pool.alloc(size, _tensor_align(size))
+                    war[g] = readers - {g}
+                else:
+                    off, _ = small_pool.alloc(size, _tensor_align(size))
+                    in_small.add(g)
+                out_elem[g] = off
+            for p_ in prods[g]:
+                if p_ not in in_small:
+                    pool.release(out_elem[p_], wid[p_], g)
+        small_base = _align(pool.top, 32)
+        for g in in_small:
+            out_elem[g] += small_base
+        self.arena_elems = max(_align(small_base + small_pool.top, 32), 32)
+        deps_all = [sorted(set(prods[g]) | war[g]) for g in range(len(keys))]
+
         # ---- nodes: large items alone, small items in stages ----
         def is_small(q):
             _, i, b = q
@@ -513,7 +610,7 @@ class Program:
         nodes = []           # dict(kind, items, deps:set)
         open_stage = -1
         for g, q in enumerate(keys):
-            ext = {node_of[p] for p in prods[g]}
+            ext = {node_of[p] for p in deps_all[g]}
             if is_small(q):
                 # join the open stage unless a producer is a node created after it
                 if open_stage >= 0 and all(n <= open_stage for n in ext):
@@ -564,7 +661,7 @@ class Program:
             for gid in gids:
                 (_, i, b), g = item_keys[gid]
                 t = self.instances[i].template
-                ib, xb = in_base[i], inter_base[i]
+                ib = in_base[i]
                 rec = B[gid]
                 rec["tick_begin"] = tick if nd["kind"] == N.QTN_NODE_SMALL else 0
                 rec["n_tiles"] = ntiles[gid]
@@ -572,7 +669,7 @@ class Program:
                 rec["dep_begin"] = len(deps)
                 if b >= 0:
                     rec["w"], rec["k"], rec["tile_bits"] = t.w[b], t.k[b], t.L[b]
-                    rec["out_off"] = xb + t.out_off[b]
+                    rec["out_off"] = out_elem[g]
                     rec["slot"] = -1
                     rec["smem_elems"] = t.smem_elems[b]
                     rec["stmask"] = t.stmask[b]
@@ -581,10 +678,7 @@ class Program:
                         if kind == 0:
                             off = ib + int(t.in_off[ref])
                         else:
-                            pg = new_of[order_gid[(i, ref)]]
-                            off = xb + int(t.out_off[ref])
-                            if node_of[order_gid[(i, ref)]] == ni:
-                                deps.append((pg, ntiles[pg]))
+                            off = out_elem[order_gid[(i, ref)]]
                         members.append((off, int(t.mem_mask[j]), int(t.mem_smask[j]), int(t.mem_cls[j])))
                     rec["n_mem"] = t.mem_ptr[b + 1] - t.mem_ptr[b]
                     if nd["kind"] == N.QTN_NODE_LARGE:
@@ -598,12 +692,14 @@ class Program:
                         if kd == 0:
                             off = ib + int(t.in_off[ref])
                         else:
-                            pg = new_of[order_gid[(i, int(ref))]]
-                            off = xb + int(t.out_off[int(ref)])
-                            if node_of[order_gid[(i, int(ref))]] == ni:
-                                deps.append((pg, ntiles[pg]))
+                            off = out_elem[order_gid[(i, int(ref))]]
                         members.append((off, 0, 0, 0))
                     rec["n_mem"] = len(t.fin_kind)
+                # completion dependencies inside this stage (RAW + WAR)
+                for dg in deps_all[g]:
+                    if node_of[dg] == ni:
+                        pg = new_of[dg]
+                        deps.append((pg, ntiles[pg]))
                 rec["n_dep"] = len(deps) - rec["dep_begin"]
                 tick += int(ntiles[gid])
             smem_max = max(smem_max, node_smem)

@@ -153,3 +153,27 @@ def test_rank0_and_scalar_inputs():
     v, st = Q.contract_network(tn, [0], C128)
     assert abs(v - (2 + 1j) * (3 + 8j)) < 1e-12
     assert [s.width for s in st] == [0]
+
+
+def test_forced_memory_reuse_on_device(monkeypatch):
+    """Liveness reuse with WAR dependencies forced on every block: graph edges
+    and in-stage counters must order writers after readers on the device."""
+    from paper_2210_15874_b200 import engine as E
+    monkeypatch.setattr(E, "REUSE_MIN_ELEMS", 1)
+    g, graph, params = _cfg("cfg2")
+    c = Q.qaoa_maxcut_circuit(graph, params)
+    for dtype, tol in (("complex64", 1e-5), ("complex128", 1e-10)):
+        insts, raws, want = [], [], []
+        for rec in g["cones"]:
+            lc = Q.extract_lightcone(c, tuple(rec["edge"]), cone="tight")
+            t = E.plan_template([x.indices for x in lc.network.tensors], rec["order"], dtype)
+            insts.append(E.Instance(t))
+            raws.append(np.concatenate([np.asarray(x.data).ravel() for x in lc.network.tensors]))
+            want.append(rec["zz"][0])
+        prog = E.Program(insts, dtype, reuse_above=0)
+        assert prog.reuse
+        ex = E.Executor(prog)
+        for _ in range(2):
+            vals = ex.run(raws)
+            for v, w in zip(vals, want):
+                assert abs(v.real - w) <= tol

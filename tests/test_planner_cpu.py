@@ -189,3 +189,38 @@ def test_kernel_variants_match_member_layout():
                 assert (v >> 8) & 1 == sum(1 for x in cls if x == E.CLS_STREAMED)
                 nb0 = sum(1 for x, m in zip(cls, masks) if x == E.CLS_VARYING and m & 1)
                 assert (v >> 12) & 15 == (nb0 if dtype == "complex64" else 0)
+
+
+@pytest.mark.parametrize("k", range(6))
+def test_memory_reuse_programs_emulate_correctly(k, monkeypatch):
+    """Forced liveness reuse (every block, WAR dependencies) keeps the
+    results: the emulator executes nodes in order and asserts every
+    dependency precedes its dependent."""
+    monkeypatch.setattr(E, "REUSE_MIN_ELEMS", 1)
+    rec = load_json("networks.json")[k]
+    c = Q.Circuit(rec["n"], _gates(rec))
+    tn = Q.amplitude_network(c, rec["bits"])
+    t = E.plan_template([x.indices for x in tn.tensors], rec["order_minfill"], "complex128")
+    prog = E.Program([E.Instance(t), E.Instance(t)], "complex128", reuse_above=0)
+    assert prog.reuse
+    raw = np.concatenate([np.asarray(x.data).ravel() for x in tn.tensors])
+    vals = run_program(prog, [raw, raw])
+    for v in vals:
+        assert abs(v - complex(*rec["value"])) < 1e-12
+    no = E.Program([E.Instance(t), E.Instance(t)], "complex128", reuse_above=1 << 62)
+    assert prog.arena_elems <= no.arena_elems
+
+
+def test_memory_reuse_cfg1_batched(monkeypatch):
+    monkeypatch.setattr(E, "REUSE_MIN_ELEMS", 1)
+    g, graph, params = _cfg("cfg1")
+    c = Q.qaoa_maxcut_circuit(graph, params)
+    insts, raws = [], []
+    for rec in g["cones"]:
+        tn = Q.extract_lightcone(c, tuple(rec["edge"])).network
+        insts.append(E.Instance(E.plan_template([x.indices for x in tn.tensors], rec["order"], "complex128")))
+        raws.append(np.concatenate([np.asarray(x.data).ravel() for x in tn.tensors]))
+    prog = E.Program(insts, "complex128", reuse_above=0)
+    vals = run_program(prog, raws)
+    for v, rec in zip(vals, g["cones"]):
+        assert abs(v.real - rec["zz"][0]) < 1e-12
