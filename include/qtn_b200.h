@@ -173,6 +173,15 @@ int qtn_graph_create(const qtn_program_t* prog, const qtn_node_t* nodes, int32_t
 /* Launch the instantiated graph (one call per program execution). */
 int qtn_graph_launch(qtn_graph_t* g, void* stream);
 int qtn_graph_destroy(qtn_graph_t* g);
+/* Host planning (no device needed): the greedy min-fill (heuristic 0) or
+ * min-degree (1) elimination order of a network given as CSR index lists
+ * (tensor t holds tensor_idx[tensor_ptr[t] .. tensor_ptr[t+1])); open indices
+ * are never eliminated.  Same heap discipline and smallest-id tie-breaks as
+ * the reference's greedy_order (src/ordering.py:26-94), hence the same order.
+ * order_out must hold every distinct index id; *n_out = entries written. */
+int qtn_greedy_order(int32_t n_tensors, const int32_t* tensor_ptr, const int64_t* tensor_idx,
+                     int32_t n_open, const int64_t* open_idx, int32_t heuristic,
+                     int64_t* order_out, int32_t* n_out);
 /* dst[e] = convert(src[sum_j bit_j(e) * src_strides[j]]) for e < 2^rank,
  * j = 0 the fastest dst axis; src/dst element types given separately
  * (complex128 -> complex64 narrowing allowed).  General axis permutation +

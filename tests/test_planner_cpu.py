@@ -224,3 +224,22 @@ def test_memory_reuse_cfg1_batched(monkeypatch):
     vals = run_program(prog, raws)
     for v, rec in zip(vals, g["cones"]):
         assert abs(v.real - rec["zz"][0]) < 1e-12
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_native_greedy_order_matches_python(seed):
+    """csrc/planner.cpp (qtn_greedy_order) == the Python restatement, both
+    heuristics, with and without open indices."""
+    from paper_2210_15874_b200 import ordering as OR
+    rng = np.random.default_rng(seed)
+    c = Q.Circuit(7, [Q.Gate(k, tuple(q), a) for k, q, a in
+                      [("H", (int(rng.integers(7)),), None) if rng.random() < 0.3 else
+                       ("ZZ", tuple(int(x) for x in rng.choice(7, 2, replace=False)), 0.3) if rng.random() < 0.5 else
+                       ("CX", tuple(int(x) for x in rng.choice(7, 2, replace=False)), None) for _ in range(40)]])
+    tn = Q.amplitude_network(c, [0] * 7)
+    for h in ("minfill", "mindegree"):
+        assert Q.greedy_order(tn, h) == OR.greedy_order_py(tn, h)
+    ids = sorted(tn.all_indices())
+    opened = Q.TensorNetwork(tn.tensors, open_indices=tuple(ids[:: 7]))
+    for h in ("minfill", "mindegree"):
+        assert Q.greedy_order(opened, h) == OR.greedy_order_py(opened, h)
