@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define QTN_ABI_VERSION 5
+#define QTN_ABI_VERSION 6
 
 enum {
   QTN_OK = 0,
@@ -190,6 +190,42 @@ int qtn_greedy_order(int32_t n_tensors, const int32_t* tensor_ptr, const int64_t
 int qtn_permute(int32_t src_dtype, const void* src, int64_t src_offset,
                 int32_t dst_dtype, void* dst, int32_t rank,
                 const int64_t* src_strides, void* stream);
+
+/* ---- K3: one standalone bucket, members in any axis order ----
+ * The process-bucket call of the reference, contract_bucket(Bucket, Backend)
+ * (src/tensor_core.py:167-188) with the fast_kernel body
+ * (src/tensor_core.py:148-164), for members that are NOT in the program's
+ * canonical layout (arbitrary index permutations, strided slices): no member
+ * is transposed in HBM first.  Iteration bit b < w is result axis b of the
+ * sorted result (b = 0 the LAST sorted index, i.e. the fastest axis of the C
+ * order output, src/tensor_core.py:117-122); bit w is the bucket index.
+ *     out[r] = sum_{s=0,1} prod_i data_i[sum_b bit_b(r, s) * strides_i[b]]
+ * members multiplied in order, s = 0 then s = 1.  Every member must carry
+ * the bucket index (strides[w] > 0, reference: Bucket validation,
+ * src/tensor_core.py:86-90); w <= 31, member rank <= 32. */
+typedef struct {
+  const void* data;                   /* device pointer (element aligned)           */
+  int64_t strides[QTN_MAX_WIDTH + 1]; /* element stride per iteration bit, 0 = absent */
+} qtn_bmember_t;
+
+typedef struct {
+  int32_t dtype;   /* QTN_C64 / QTN_C128 (members and output)                   */
+  int32_t w;       /* result rank                                               */
+  int32_t n_mem;   /* 1..QTN_MAX_MEMBERS                                        */
+  int32_t reserved;
+  void* out;       /* 2^w elements, C order over the sorted result indices      */
+  qtn_bmember_t mem[QTN_MAX_MEMBERS];
+} qtn_bucket_desc_t;
+
+/* Launch K3 on `stream` (asynchronous; buffers must stay alive until the
+ * stream is synchronised).  Errors: QTN_E_INVALID (bad descriptor),
+ * QTN_E_UNSUPPORTED (w > 31, rank > 32), QTN_E_CUDA. */
+int qtn_bucket(const qtn_bucket_desc_t* desc, void* stream);
+/* Plan only (no device), info[8]: [0] tile bits, [1] staged elements per
+ * tile, [2] shared-memory bytes per block, [3] tiles, [4] staged members
+ * (-1 = every member staged, generic kernel), [5] members folded into the
+ * per-tile product table, [6] product-table bits. */
+int qtn_bucket_plan(const qtn_bucket_desc_t* desc, int32_t* info);
 
 #ifdef __cplusplus
 }

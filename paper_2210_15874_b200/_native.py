@@ -26,7 +26,7 @@ QTN_FINALIZE = -1
 MAX_MEMBERS = 8
 MAX_WIDTH = 40
 MAX_SUMMED = 6
-ABI_VERSION = 5
+ABI_VERSION = 6
 QTN_NODE_SMALL = 0
 QTN_NODE_LARGE = 1
 QTN_VARIANT_GENERIC = -1
@@ -43,6 +43,8 @@ EXPORTS = (
     "qtn_graph_destroy",
     "qtn_permute",
     "qtn_greedy_order",
+    "qtn_bucket",
+    "qtn_bucket_plan",
 )
 
 BUCKET_DT = np.dtype([
@@ -78,6 +80,16 @@ class ProgramC(ctypes.Structure):
     ]
 
 
+class BMemberC(ctypes.Structure):
+    _fields_ = [("data", ctypes.c_void_p), ("strides", ctypes.c_int64 * (MAX_WIDTH + 1))]
+
+
+class BucketDescC(ctypes.Structure):
+    """qtn_bucket_desc_t: one standalone bucket, members in any axis order."""
+    _fields_ = [("dtype", ctypes.c_int32), ("w", ctypes.c_int32), ("n_mem", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("out", ctypes.c_void_p), ("mem", BMemberC * MAX_MEMBERS)]
+
+
 _lib = None
 
 
@@ -110,6 +122,10 @@ def load(path: str = LIB_PATH):
     lib.qtn_greedy_order.argtypes = [i32, vp, vp, i32, vp, i32, vp, ctypes.POINTER(i32)]
     lib.qtn_permute.restype = ctypes.c_int
     lib.qtn_permute.argtypes = [i32, vp, i64, i32, vp, i32, ctypes.POINTER(i64), vp]
+    lib.qtn_bucket.restype = ctypes.c_int
+    lib.qtn_bucket.argtypes = [ctypes.POINTER(BucketDescC), vp]
+    lib.qtn_bucket_plan.restype = ctypes.c_int
+    lib.qtn_bucket_plan.argtypes = [ctypes.POINTER(BucketDescC), ctypes.POINTER(i32)]
     if lib.qtn_abi_version() != ABI_VERSION:
         raise NativeUnavailable(f"ABI mismatch: library {lib.qtn_abi_version()} != {ABI_VERSION}")
     _lib = lib
@@ -157,3 +173,31 @@ def permute(src_dtype, src_ptr, src_offset, dst_dtype, dst_ptr, rank, strides, s
     arr = (ctypes.c_int64 * max(1, rank))(*[int(s) for s in strides])
     check(lib.qtn_permute(src_dtype, ctypes.c_void_p(src_ptr), int(src_offset), dst_dtype,
                           ctypes.c_void_p(dst_ptr), int(rank), arr, ctypes.c_void_p(stream)))
+
+
+def bucket_desc(dtype_code, w, out_ptr, members):
+    """members: [(device_ptr, {iteration_bit: element_stride})]; bit w = summed index."""
+    d = BucketDescC()
+    d.dtype = dtype_code
+    d.w = w
+    d.n_mem = len(members)
+    d.out = out_ptr
+    for i, (ptr, strides) in enumerate(members):
+        d.mem[i].data = ptr
+        for b, st in strides.items():
+            d.mem[i].strides[b] = int(st)
+    return d
+
+
+def bucket_plan(desc):
+    """(tile bits, staged elements per tile, smem bytes, tiles, staged members
+    (-1: v1 kernel), folded members, product-table bits, invariant operand) — no device needed."""
+    lib = load()
+    info = (ctypes.c_int32 * 8)()
+    check(lib.qtn_bucket_plan(ctypes.byref(desc), info))
+    return tuple(info)
+
+
+def bucket_launch(desc, stream):
+    lib = require_device()
+    check(lib.qtn_bucket(ctypes.byref(desc), ctypes.c_void_p(stream)))

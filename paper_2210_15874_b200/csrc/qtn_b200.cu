@@ -911,6 +911,8 @@ int make_launch(const qtn_program_t* p, const qtn_node_t* nd, int ni, int32_t n_
 
 }  // namespace
 
+int qtn_internal_set_error(int code, const char* msg) { return set_err(code, "%s", msg); }
+
 struct qtn_graph {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;

@@ -13,8 +13,6 @@ storage); `.data` copies it back lazily.
 """
 from __future__ import annotations
 
-import ctypes
-import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -225,85 +223,34 @@ def _device_permute(t: DeviceTensor, new_order, dtype) -> DeviceTensor:
     return DeviceTensor(new_order, out)
 
 
-class _BucketLauncher:
-    """Single-bucket program (no arena: member and result offsets are absolute
-    device addresses / element size), launched as one node: the K1
-    large-item kernel variant for vector-sized tiles, else a one-item K2
-    stage."""
-
-    @classmethod
-    def run(cls, members, masks, out, w, dtype):
-        import torch
-        dev = out.device
-        esz = E.ELEM_BYTES[dtype]
-        smasks = [1] * len(masks)
-        L, st = E._tile_bits(w, masks, smasks, dtype)
-        small = (1 << L) < E.VEC[dtype] * E.NT
-        stm = 0 if small else E._step_mask(L, masks, dtype)
-        mcls = E.member_classes(w, 1, L, stm, masks)
-        variant = E.kernel_variant(w, 1, L, mcls, dtype, masks)
-        B = np.zeros(1, N.BUCKET_DT)
-        B["out_off"] = out.data_ptr() // esz
-        B["w"] = w
-        B["k"] = 1
-        B["tile_bits"] = L
-        B["n_mem"] = len(members)
-        B["n_tiles"] = 1 << (w - L)
-        B["slot"] = -1
-        B["smem_elems"] = st
-        B["stmask"] = stm
-        M = np.zeros(len(members), N.MEMBER_DT)
-        for k, (m, msk, c) in enumerate(zip(members, masks, mcls)):
-            M[k] = (m.data_ptr() // esz, msk, 1, c)
-        bsz, msz = N.BUCKET_DT.itemsize, N.MEMBER_DT.itemsize
-        tb_off = bsz + msz * N.MAX_MEMBERS          # tick_begin[0] = 0, then ctrl[3] = 0
-        blob = np.zeros(tb_off + 32, np.uint8)
-        blob[0:bsz] = np.frombuffer(B.tobytes(), np.uint8)
-        blob[bsz:bsz + M.nbytes] = np.frombuffer(M.tobytes(), np.uint8)
-        dtab = torch.from_numpy(blob).to(dev)
-        base = dtab.data_ptr()
-        c = N.ProgramC()
-        c.dtype = E.DTYPE_CODE[dtype]
-        c.n_buckets = 1
-        c.n_nodes = 1
-        c.buckets = base
-        c.members = base + bsz
-        c.deps = base + bsz
-        c.tick_begin = base + tb_off
-        c.ctrl = base + tb_off + 4
-        c.arena = None
-        c.results = None
-        c.timing = None
-        node = np.zeros(1, N.NODE_DT)
-        if small:
-            node[0] = (N.QTN_NODE_SMALL, 0, 1, 1 << (w - L), 0, 0, 0, E.SMALL_PROD_ELEMS * esz)
-        else:
-            node[0] = (N.QTN_NODE_LARGE, 0, 1, 0, variant, 0, 0, _smem_bytes(st * esz))
-        stream = torch.cuda.current_stream(dev)
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        ev0.record(stream)
-        N.check(N.load().qtn_node_launch(ctypes.byref(c), node.ctypes.data_as(ctypes.c_void_p), 0,
-                                         ctypes.c_void_p(stream.cuda_stream)))
-        ev1.record(stream)
-        # keep the table alive until the launch has consumed it
-        ev1.synchronize()
-        del dtab
-        return int(ev0.elapsed_time(ev1) * 1e6)
-
-
-def _smem_bytes(n):
-    return (n + 15) // 16 * 16
+def bucket_strides(b: Bucket, res):
+    """Iteration strides of every member of `b` for K3 (include/qtn_b200.h,
+    qtn_bucket_desc_t): bit j < w is result axis j counted from the LAST
+    sorted index (src/tensor_core.py:117-122), bit w the bucket index; a
+    member in C order over its own indices has stride 2^(rank-1-axis)."""
+    w = len(res)
+    bit = {a: w - 1 - j for j, a in enumerate(res)}
+    bit[b.bucket_index] = w
+    out = []
+    for t in b.tensors:
+        r = len(t.indices)
+        out.append({bit[a]: 1 << (r - 1 - ax) for ax, a in enumerate(t.indices)})
+    return out
 
 
 def contract_bucket(b: Bucket, backend: Backend = None):
     """Process-bucket: sum `bucket_index` out of the product of the members
-    (src/tensor_core.py:167-188), on the B200.
+    (src/tensor_core.py:167-188), on the B200, in ONE fused kernel (K3,
+    csrc/bucket_strided.cu) that reads every member in its own axis order —
+    no member is transposed first (the reference's fast_kernel transposes and
+    broadcasts each member, src/tensor_core.py:148-164).
 
     Returns (result, BucketStats).  The result's indices are the sorted union
     minus the bucket index (src/tensor_core.py:117-122).  Host members give a
     host `Tensor`; if any member is a `DeviceTensor` the result stays on the
-    device as a `DeviceTensor`."""
+    device as a `DeviceTensor` (members in another dtype are converted on
+    the device first).  BucketStats.elapsed_ns is the kernel's device time
+    (CUDA events), like the reference's kernel-only timing (185-187)."""
     import torch
     backend = backend or Backend()
     if not b.tensors:
@@ -315,26 +262,32 @@ def contract_bucket(b: Bucket, backend: Backend = None):
         raise ValueError(f"bucket has {len(b.tensors)} members; at most {N.MAX_MEMBERS} supported")
     dtype = backend.dtype
     dev = torch.device("cuda", backend.device)
+    tdt = torch.complex64 if dtype == "complex64" else torch.complex128
+    npdt = np.complex64 if dtype == "complex64" else np.complex128
     any_dev = any(isinstance(t, DeviceTensor) for t in b.tensors)
-    bit = {a: w - 1 - j for j, a in enumerate(res)}
-    members, masks = [], []
+    strides = bucket_strides(b, res)
     with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev)
+        members = []
         for t in b.tensors:
-            canon = (b.bucket_index,) + tuple(i for i in res if i in t.indices)
-            dt = t if isinstance(t, DeviceTensor) else DeviceTensor.from_host(t, "complex128", backend.device)
-            dt = _device_permute(dt, canon, dtype)
-            st = dt.storage
-            if not st.is_contiguous() or st.data_ptr() % 16:
-                st = st.contiguous().clone()   # vector loads need 16-byte alignment
+            if isinstance(t, DeviceTensor):
+                st = t.storage if t.storage.device == dev else t.storage.to(dev)
+                if st.dtype != tdt or not st.is_contiguous():
+                    st = st.to(tdt).contiguous()
+            else:   # host member: narrowed on the host, one pinned upload
+                h = torch.from_numpy(np.ascontiguousarray(np.asarray(t.data, dtype=npdt)).reshape(-1))
+                st = h.pin_memory().to(dev, non_blocking=True)
             members.append(st)
-            m = 0
-            for a in t.indices:
-                if a != b.bucket_index:
-                    m |= 1 << bit[a]
-            masks.append(m)
-        tdt = torch.complex64 if dtype == "complex64" else torch.complex128
-        out = torch.empty(max(1 << w, 2), dtype=tdt, device=dev)[: 1 << w]
-        elapsed = _BucketLauncher.run(members, masks, out, w, dtype)
+        out = torch.empty(1 << w, dtype=tdt, device=dev)
+        desc = N.bucket_desc(E.DTYPE_CODE[dtype], w, out.data_ptr(),
+                             [(m.data_ptr(), s) for m, s in zip(members, strides)])
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        N.bucket_launch(desc, stream.cuda_stream)
+        ev1.record(stream)
+        ev1.synchronize()
+        elapsed = int(ev0.elapsed_time(ev1) * 1e6)
     result = DeviceTensor(res, out)
     if not any_dev:
         result = result.to_host()
