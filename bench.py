@@ -47,9 +47,10 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=2, help="oracle contractions for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=150.0)
-    ap.add_argument("--workload", default="lightcone", choices=["lightcone", "graph"],
+    ap.add_argument("--workload", default="lightcone", choices=["lightcone", "graph", "bucket"],
                     help="lightcone: cfg-2 single lightcone per rank (weak); graph: all 45 N=30 p=4 "
-                         "tight lightcones sharded over ranks by LPT + slot all-reduce (strong)")
+                         "tight lightcones sharded over ranks by LPT + slot all-reduce (strong); bucket: "
+                         "cfg-5 synthetic bucket microbench through K3 (fused permutation-aware kernel)")
     return ap.parse_args()
 
 
@@ -449,6 +450,107 @@ def run_graph(args):
     return 0
 
 
+BUCKET_CASES = [(w, cls, k) for w in (24, 26, 28) for cls, k in (("A", 3), ("A", 6), ("B", 2))]
+
+
+def run_bucket(args):
+    """cfg 5 (BASELINE.json configs[4]): synthetic buckets of random complex
+    tensors over binary indices in random axis permutations, one bucket index
+    contracted by K3 (csrc/bucket_strided.cu).  A step = one launch per case
+    of BUCKET_CASES; value = algorithmic bytes of all cases / device time
+    (every member read once, result written once; inputs > L2 and L2
+    flushed between launches)."""
+    import torch
+    import paper_2210_15874_b200 as Q
+    from paper_2210_15874_b200 import _native as N
+    from paper_2210_15874_b200 import engine as E
+    from paper_2210_15874_b200 import workloads as W
+
+    rank, world, local = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    dtype = "complex64" if args.dtype == "c64" else "complex128"
+    esz = E.ELEM_BYTES[dtype]
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    cases = []
+    for w, cls, k in BUCKET_CASES:
+        mem = W.synthetic_bucket_device(w, k, cls, 0, dtype, device=local)
+        b = Q.Bucket(W.BUCKET, [Q.DeviceTensor(i, t) for i, t in mem])
+        st = Q.tensor_core.bucket_strides(b, tuple(range(1, w + 1)))
+        out = torch.empty(1 << w, dtype=mem[0][1].dtype, device="cuda")
+        d = N.bucket_desc(E.DTYPE_CODE[dtype], w, out.data_ptr(), [(t.data_ptr(), x) for (_, t), x in zip(mem, st)])
+        cases.append({"w": w, "cls": cls, "k": k, "desc": d, "keep": (mem, out), "bytes": W.bucket_bytes(mem, w, esz),
+                      "plan": N.bucket_plan(d), "t": 0.0})
+    for _ in range(max(3, args.warmup)):
+        for c in cases:
+            N.bucket_launch(c["desc"], stream.cuda_stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    evs = []
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            for c in cases:
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                N.bucket_launch(c["desc"], stream.cuda_stream)
+                e1.record(stream)
+                evs.append((c, e0, e1))
+        torch.cuda.synchronize()
+    for c, e0, e1 in evs:
+        c["t"] += e0.elapsed_time(e1) / 1e3
+    t_dev = max_over_ranks(sum(c["t"] for c in cases), world)
+    tot_bytes = sum(c["bytes"] for c in cases) * args.steps
+    # e2e: the public call with host Tensors (upload members, download result)
+    we, ke = 22, 3
+    host = [Q.Tensor(i, d) for i, d in W.synthetic_bucket(we, ke, "A", 0)]
+    be = Q.Backend.b200(dtype=dtype, device=local, profile=False)
+    bh = Q.Bucket(W.BUCKET, host)
+    Q.contract_bucket(bh, be)
+    n_e2e = max(2, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(n_e2e):
+        res, _ = Q.contract_bucket(bh, be)
+    t_e2e = max_over_ranks((time.perf_counter() - t0) / n_e2e, world)
+    e2e_bytes = (sum(1 << len(t.indices) for t in host) + (1 << we)) * esz
+    if rank != 0:
+        return 0
+    peak, peak_src = peak_hbm()
+    value = world * tot_bytes / t_dev / 1e9
+    cpu = None
+    if not args.no_cpu_baseline:
+        from oracle import qtn_oracle as O   # CPU baseline only
+        mem = W.synthetic_bucket(20, 3, "A", 0)
+        t0 = time.perf_counter()
+        O.bucket_fast(W.BUCKET, mem)
+        dt = time.perf_counter() - t0
+        cpu = {"value": W.bucket_bytes(mem, 20, 16) / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "port",
+               "sample": "one w=20 class-A k=3 bucket through the oracle port of fast_kernel (numpy complex128)"}
+    sweep = [{"w": c["w"], "class": c["cls"], "k": c["k"], "GBps": round(c["bytes"] * args.steps / c["t"] / 1e9, 1),
+              "frac": round(c["bytes"] * args.steps / c["t"] / 1e9 / peak, 3), "tile_bits": c["plan"][0],
+              "staged": c["plan"][4], "folded": c["plan"][5], "invariant": c["plan"][7]} for c in cases]
+    line = {
+        "metric": "GB/s (cfg-5 synthetic bucket contraction, K3)", "value": value, "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": 1e3 * t_dev / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+        "data": "synthetic (seeded standard complex normal entries, random index permutations)",
+        "config": {"workload": "cfg5: buckets w in {24,26,28} x {class A k=3, class A k=6, class B k=2}, one bucket "
+                               "index contracted, members in random axis order",
+                   "l2": "inputs > L2 and flushed (256 MiB write) before every launch", "sweep": sweep},
+        "roofline": {"bound": "hbm", "achieved": value, "peak": peak, "unit": "GB/s", "frac": value / peak,
+                     "traffic": None, "peak_source": peak_src, "kernel": "k3v2_kernel (csrc/bucket_strided.cu)"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_bytes / t_e2e / 1e9, "unit": "GB/s", "h2d_bytes_per_step": e2e_bytes - (1 << we) * esz,
+                "d2h_bytes_per_step": (1 << we) * esz, "call": f"contract_bucket(Bucket of host Tensors), w={we} class A k={ke}"},
+        "gpu_launches": args.steps * len(cases),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def E_alg(plan, dtype):
     from paper_2210_15874_b200 import engine as E
     return [E.algorithmic_bytes(plan.templates[u.cone], dtype) for u in plan.units]
@@ -460,6 +562,8 @@ def main():
         return run_reference(args)
     if args.workload == "graph":
         return run_graph(args)
+    if args.workload == "bucket":
+        return run_bucket(args)
     return run_ours(args)
 
 

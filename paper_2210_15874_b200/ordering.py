@@ -10,6 +10,7 @@ per batch; the get-result scalar is the program's finaliser slot.
 from __future__ import annotations
 
 import heapq
+import operator
 import threading
 from collections import OrderedDict
 from dataclasses import dataclass
@@ -236,18 +237,61 @@ class _PlanCache:
 PLAN_CACHE = _PlanCache()
 
 
+class _NetworkInputs:
+    """Per-network host staging cache: the structure key (index tuples) and
+    the raw concatenation of the tensor data, valid while `tn.tensors` holds
+    the very same Tensor objects (Tensors are immutable — read-only data —
+    so identical objects mean identical values).  A network whose tensor list
+    was changed, or a new network (e.g. the next point of a parameter sweep),
+    is re-read.  Small LRU keyed by id(tn)."""
+
+    def __init__(self, cap=16):
+        self.cap = cap
+        self.d = OrderedDict()
+        self.lock = threading.Lock()
+
+    def get(self, tn):
+        ts = tn.tensors
+        with self.lock:
+            hit = self.d.get(id(tn))
+            if hit is not None and hit[0] is tn and len(hit[1]) == len(ts) and all(map(operator.is_, hit[1], ts)):
+                self.d.move_to_end(id(tn))
+                return hit[2], hit[3], hit[4]
+        snap = tuple(ts)
+        struct = tuple(t.indices for t in snap)
+        parts = [t.data.ravel() for t in snap]
+        raw = np.concatenate(parts) if parts else np.zeros(0, np.complex128)
+        if raw.dtype != np.complex128:
+            raw = raw.astype(np.complex128)
+        raw.setflags(write=False)
+        plans = {}   # (order, fixed, dtype) -> (key, template) for this network
+        with self.lock:
+            self.d[id(tn)] = (tn, snap, struct, raw, plans)
+            self.d.move_to_end(id(tn))
+            while len(self.d) > self.cap:
+                self.d.popitem(last=False)
+        return struct, raw, plans
+
+
+NETWORK_INPUTS = _NetworkInputs()
+
+
 def _raw_inputs(tn: TensorNetwork) -> np.ndarray:
-    parts = [t.data.ravel() for t in tn.tensors]
-    raw = np.concatenate(parts) if parts else np.zeros(0, np.complex128)
-    return raw if raw.dtype == np.complex128 else raw.astype(np.complex128)
+    return NETWORK_INPUTS.get(tn)[1]
 
 
 def _template(tn, order, backend, fixed=()):
-    key = ("tmpl", tuple(t.indices for t in tn.tensors), tuple(order), tuple(fixed), backend.dtype)
+    struct, _, plans = NETWORK_INPUTS.get(tn)
+    okey = (tuple(order), tuple(fixed), backend.dtype)
+    got = plans.get(okey)
+    if got is not None:
+        return got
+    key = ("tmpl", struct) + okey
     hit = PLAN_CACHE.get(key)
     if hit is None:
-        hit = E.plan_template([t.indices for t in tn.tensors], order, backend.dtype, fixed)
+        hit = E.plan_template(list(struct), order, backend.dtype, fixed)
         PLAN_CACHE.put(key, hit)
+    plans[okey] = (key, hit)
     return key, hit
 
 
@@ -309,8 +353,12 @@ def contract_network(tn: TensorNetwork, order, backend: Backend = None, mem_cap:
         raise ValueError("contract_network requires a closed network")
     key, tmpl = _template(tn, order, backend)   # raises for indices missing from the order
     _check_cap(tmpl, backend, mem_cap)
-    ex, lock = _executor(key, lambda: E.Program([E.Instance(tmpl)], backend.dtype), backend, 1)
-    raw = _raw_inputs(tn)
+    struct, raw, plans = NETWORK_INPUTS.get(tn)
+    xkey = ("exec", tuple(order), backend.dtype, backend.device, backend.profile)
+    got = plans.get(xkey)
+    if got is None:
+        got = plans[xkey] = _executor(key, lambda: E.Program([E.Instance(tmpl)], backend.dtype), backend, 1)
+    ex, lock = got
     with lock:
         vals = ex.run([raw])
         stats = _stats(tmpl, ex, backend)
