@@ -631,58 +631,79 @@ __device__ __forceinline__ void large_compute(const LargeCtx& S, const typename 
   T U[NS];
 #pragma unroll
   for (int c = 0; c < NS; ++c) U[c] = hu ? sseg[S.uoff + c] : T{};
-  for (int st = 0; st < nst; ++st) {
-    const int est = S.est[st];
-    T prod[NS][VEC];
-    bool started = false;
+  // streamed loads of UNR steps are issued together before any of their
+  // stores (the compiler cannot hoist them: loads and stores share the arena),
+  // so each thread keeps UNR * NS 16-byte loads in flight
+  constexpr int UNR = ST ? (NS <= 2 ? 4 : (NS == 4 ? 2 : 1)) : 1;
+  for (int st0 = 0; st0 < nst; st0 += UNR) {
+    T pre[UNR][NS][VEC];
     if (ST) {
 #pragma unroll
-      for (int c = 0; c < NS; ++c) split(__ldcg(reinterpret_cast<const V*>(sp + est + sro[c])), prod[c]);
-      started = true;
-    }
-    if (hu) {
+      for (int u = 0; u < UNR; ++u)
+        if (st0 + u < nst) {
+          const int est = S.est[st0 + u];
 #pragma unroll
-      for (int c = 0; c < NS; ++c)
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) prod[c][v] = started ? cmul(prod[c][v], U[c]) : U[c];
-      started = true;
-    }
-    if (NS == 2 && haveP) {
-#pragma unroll
-      for (int c = 0; c < NS; ++c)
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) prod[c][v] = started ? cmul(prod[c][v], P[c][v]) : P[c][v];
-      started = true;
-    }
-#pragma unroll
-    for (int j = 0; j < NV; ++j) {
-      const T* q = qv[j] + S.gs[vi[j]][st];
-#pragma unroll
-      for (int c = 0; c < NS; ++c) {
-        QTN_CHECK((int)((q + ro[j][c]) - sseg) + VEC <= S.uoff + MAXNS &&
-                      S.gt[vi[j]][tid] + S.gs[vi[j]][st] + ro[j][c] < S.nsig[vi[j]] * S.seglen[vi[j]],
-                  "staged gather member %d", vi[j]);
-        T x[VEC];
-        if (VEC == 2 && j < NB0) {
-          split(*reinterpret_cast<const V*>(q + ro[j][c]), x);   // adjacent v pair
-        } else {
-          x[0] = q[ro[j][c]];                                     // member constant in v
-          x[VEC - 1] = x[0];
+          for (int c = 0; c < NS; ++c) split(__ldcg(reinterpret_cast<const V*>(sp + est + sro[c])), pre[u][c]);
         }
+    }
 #pragma unroll
-        for (int v = 0; v < VEC; ++v) prod[c][v] = started ? cmul(prod[c][v], x[v]) : x[v];
+    for (int u = 0; u < UNR; ++u) {
+      const int st = st0 + u;
+      if (st >= nst) break;
+      const int est = S.est[st];
+      T prod[NS][VEC];
+      bool started = false;
+      if (ST) {
+#pragma unroll
+        for (int c = 0; c < NS; ++c)
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) prod[c][v] = pre[u][c][v];
+        started = true;
       }
-      started = true;
-    }
-    T acc[VEC];
+      if (hu) {
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) {
-      acc[v] = prod[0][v];
+        for (int c = 0; c < NS; ++c)
 #pragma unroll
-      for (int c = 1; c < NS; ++c) acc[v] = cadd(acc[v], prod[c][v]);
+          for (int v = 0; v < VEC; ++v) prod[c][v] = started ? cmul(prod[c][v], U[c]) : U[c];
+        started = true;
+      }
+      if (NS == 2 && haveP) {
+#pragma unroll
+        for (int c = 0; c < NS; ++c)
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) prod[c][v] = started ? cmul(prod[c][v], P[c][v]) : P[c][v];
+        started = true;
+      }
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const T* q = qv[j] + S.gs[vi[j]][st];
+#pragma unroll
+        for (int c = 0; c < NS; ++c) {
+          QTN_CHECK((int)((q + ro[j][c]) - sseg) + VEC <= S.uoff + MAXNS &&
+                        S.gt[vi[j]][tid] + S.gs[vi[j]][st] + ro[j][c] < S.nsig[vi[j]] * S.seglen[vi[j]],
+                    "staged gather member %d", vi[j]);
+          T x[VEC];
+          if (VEC == 2 && j < NB0) {
+            split(*reinterpret_cast<const V*>(q + ro[j][c]), x);   // adjacent v pair
+          } else {
+            x[0] = q[ro[j][c]];                                     // member constant in v
+            x[VEC - 1] = x[0];
+          }
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) prod[c][v] = started ? cmul(prod[c][v], x[v]) : x[v];
+        }
+        started = true;
+      }
+      T acc[VEC];
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        acc[v] = prod[0][v];
+#pragma unroll
+        for (int c = 1; c < NS; ++c) acc[v] = cadd(acc[v], prod[c][v]);
+      }
+      QTN_CHECK(S.eth[tid] + est + VEC <= (1 << S.b.tile_bits), "tile offset %d", S.eth[tid] + est);
+      *reinterpret_cast<V*>(out + S.eth[tid] + est) = join(acc);
     }
-    QTN_CHECK(S.eth[tid] + est + VEC <= (1 << S.b.tile_bits), "tile offset %d", S.eth[tid] + est);
-    *reinterpret_cast<V*>(out + S.eth[tid] + est) = join(acc);
   }
 }
 

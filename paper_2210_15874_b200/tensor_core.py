@@ -134,7 +134,9 @@ class DeviceTensor:
     @property
     def data(self) -> np.ndarray:
         if self._host is None:
-            h = self.storage.detach().cpu().numpy().astype(np.complex128).reshape((2,) * self.rank)
+            import torch
+            # widen on the device (one D2H copy, no host conversion pass)
+            h = self.storage.detach().to(torch.complex128).cpu().numpy().reshape((2,) * self.rank)
             h.setflags(write=False)
             object.__setattr__(self, "_host", h)
         return self._host
@@ -223,6 +225,17 @@ def _device_permute(t: DeviceTensor, new_order, dtype) -> DeviceTensor:
     return DeviceTensor(new_order, out)
 
 
+def _upload(arr, dev):
+    """Host ndarray -> flat device tensor (read-only arrays are copied by the
+    H2D transfer itself; torch only warns that it cannot write to them)."""
+    import torch
+    import warnings
+    a = np.ascontiguousarray(arr).reshape(-1)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)
+        return torch.from_numpy(a).to(dev)
+
+
 def bucket_strides(b: Bucket, res):
     """Iteration strides of every member of `b` for K3 (include/qtn_b200.h,
     qtn_bucket_desc_t): bit j < w is result axis j counted from the LAST
@@ -263,7 +276,6 @@ def contract_bucket(b: Bucket, backend: Backend = None):
     dtype = backend.dtype
     dev = torch.device("cuda", backend.device)
     tdt = torch.complex64 if dtype == "complex64" else torch.complex128
-    npdt = np.complex64 if dtype == "complex64" else np.complex128
     any_dev = any(isinstance(t, DeviceTensor) for t in b.tensors)
     strides = bucket_strides(b, res)
     with torch.cuda.device(dev):
@@ -274,9 +286,10 @@ def contract_bucket(b: Bucket, backend: Backend = None):
                 st = t.storage if t.storage.device == dev else t.storage.to(dev)
                 if st.dtype != tdt or not st.is_contiguous():
                     st = st.to(tdt).contiguous()
-            else:   # host member: narrowed on the host, one pinned upload
-                h = torch.from_numpy(np.ascontiguousarray(np.asarray(t.data, dtype=npdt)).reshape(-1))
-                st = h.pin_memory().to(dev, non_blocking=True)
+            else:   # host member: uploaded as is (complex128), narrowed on the device
+                st = _upload(t.data, dev)
+                if st.dtype != tdt:
+                    st = st.to(tdt)
             members.append(st)
         out = torch.empty(1 << w, dtype=tdt, device=dev)
         desc = N.bucket_desc(E.DTYPE_CODE[dtype], w, out.data_ptr(),
