@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=2, help="oracle contractions for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=150.0)
+    ap.add_argument("--simplify", action="store_true",
+                    help="graph workload: simplify each lightcone network before ordering (tn_build.simplify_network)")
     ap.add_argument("--workload", default="lightcone", choices=["lightcone", "graph", "bucket"],
                     help="lightcone: cfg-2 single lightcone per rank (weak); graph: all 45 N=30 p=4 "
                          "tight lightcones sharded over ranks by LPT + slot all-reduce (strong); bucket: "
@@ -373,7 +375,7 @@ def run_graph(args):
     be = Q.Backend.b200(dtype=dtype, device=local, profile=False)
     t0 = time.perf_counter()
     c = Q.qaoa_maxcut_circuit(g, params)
-    cones = [Q.extract_lightcone(c, e, cone="tight") for e in g.edges]
+    cones = [Q.extract_lightcone(c, e, cone="tight", simplify=args.simplify) for e in g.edges]
     plan = D.plan_units(cones, be)
     t_plan = time.perf_counter() - t0
     owner = D.lpt_assign([u.cost for u in plan.units], world)
@@ -417,7 +419,8 @@ def run_graph(args):
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
-    e_api = Q.qaoa_energy(g, params, be, cone="tight", group=dist.group.WORLD if world > 1 else None)
+    e_api = Q.qaoa_energy(g, params, be, cone="tight", group=dist.group.WORLD if world > 1 else None,
+                          simplify=args.simplify)
     torch.cuda.synchronize()
     t_api = max_over_ranks(time.perf_counter() - t0, world)
     if rank != 0:
@@ -440,7 +443,8 @@ def run_graph(args):
                      "peak_source": peak_src, "note": "per-GPU average"},
         "cpu_baseline": None,
         "e2e": {"value": len(cones) / t_api, "unit": UNIT, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
-                "call": "qaoa_energy(g, params, backend, cone='tight') incl. host ordering/planning", "energy": e_api},
+                "call": f"qaoa_energy(g, params, backend, cone='tight', simplify={args.simplify}) incl. host "
+                        "ordering/planning", "energy": e_api},
         "gpu_launches": args.steps * sum(ex.prog.n_nodes for ex, _ in prep.batches),
         "clocks": clk.summary(),
     }

@@ -55,7 +55,8 @@ def plan_units(cones, backend: Backend, heuristic="minfill", mem_cap=4 << 30, sl
         sliced = []
         if slice_target is not None and width > slice_target:
             sliced = suggest_slicing(tn, order, slice_target)
-        tmpl = E.plan_template([t.indices for t in tn.tensors], order, backend.dtype, fixed=sliced)
+        tmpl = E.plan_template([t.indices for t in tn.tensors], order, backend.dtype, fixed=sliced,
+                               small_iter_bits=E.small_iter_bits_for(backend.threshold))
         if memory_estimate(tmpl.max_width, backend.dtype) > mem_cap:
             raise MemoryCapError(tmpl.max_width, memory_estimate(tmpl.max_width, backend.dtype), mem_cap)
         raw = np.concatenate([np.asarray(t.data, np.complex128).ravel() for t in tn.tensors])

@@ -229,25 +229,37 @@ def _item_cost(w, k, L, sizes, dtype, hop=None):
     return hop + max(byt / BW_BPS, waves * per_tile)
 
 
-def _cost_of(it, dtype):
+def _cost_of(it, dtype, small_iter_bits=None):
+    sib = SMALL_ITER_BITS if small_iter_bits is None else small_iter_bits
     masks, smasks = _masks(it["members"], it["X"], it["R"])
     w, k = len(it["R"]), len(it["X"])
-    if w + k <= SMALL_ITER_BITS:
+    if w + k <= sib:
         L = min(w, SMALL_TILE_BITS[dtype])
         return _item_cost(w, k, L, [1 << len(s2) for _, _, s2 in it["members"]], dtype, hop=HOP_K2_S)
     L, _ = _tile_bits(w, masks, smasks, dtype)
     return _item_cost(len(it["R"]), len(it["X"]), L, [1 << len(s2) for _, _, s2 in it["members"]], dtype)
 
 
-def plan_template(index_sets, order, dtype, fixed=(), merge=None):
+def small_iter_bits_for(threshold):
+    """Backend.threshold (result width at or below which a bucket runs in the
+    batched small-bucket schedule, the analogue of the reference's Mixed
+    threshold, src/tensor_core.py:176-184) -> iteration bits (w + k) of the
+    K2 routing rule."""
+    return int(threshold) + 1
+
+
+def plan_template(index_sets, order, dtype, fixed=(), merge=None, small_iter_bits=None):
     """Replay contract_network's bucket assignment (src/ordering.py:165-187)
     over index sets only and freeze it into a Template.
 
     index_sets: per input tensor, its indices in its own storage order
     (before slicing).  `fixed` indices are sliced out (src/ordering.py:233-248).
     merge: fold chains of buckets into k-sum items when the cost model says
-    the saved hop latency / HBM round trip outweighs the extra multiplies."""
+    the saved hop latency / HBM round trip outweighs the extra multiplies.
+    small_iter_bits: items with w + k <= this run in a K2 small stage
+    (default SMALL_ITER_BITS = Backend threshold 11 + 1)."""
     dtype = norm_dtype(dtype)
+    sib = SMALL_ITER_BITS if small_iter_bits is None else int(small_iter_bits)
     merge = MERGE_DEFAULT if merge is None else merge
     fixed = set(int(f) for f in fixed)
     act = [int(i) for i in order if int(i) not in fixed]
@@ -327,7 +339,7 @@ def plan_template(index_sets, order, dtype, fixed=(), merge=None):
     for b, (x, mem, R) in enumerate(refs):
         it = {"X": [x], "R": R, "refs": [b],
               "members": [(k_, (item_of[r_] if k_ == 1 else r_), st) for k_, r_, st in mem]}
-        it["cost"] = _cost_of(it, dtype)
+        it["cost"] = _cost_of(it, dtype, sib)
         changed = merge
         while changed:
             changed = False
@@ -341,14 +353,14 @@ def plan_template(index_sets, order, dtype, fixed=(), merge=None):
                     continue
                 w = len(R)
                 cand = {"X": X2, "R": R, "members": mem2}
-                if w + len(X2) > SMALL_ITER_BITS:
+                if w + len(X2) > sib:
                     masks, smasks = _masks(mem2, X2, R)
                     L, _ = _tile_bits(w, masks, smasks, dtype)
                     if L < min(w, MIN_TILE_BITS[dtype]):
                         continue
-                if w + len(X2) > SMALL_ITER_BITS and len(X2) > 3:
+                if w + len(X2) > sib and len(X2) > 3:
                     continue   # would need the generic K1 kernel (no k > 3 specialisation)
-                c2 = _cost_of(cand, dtype)
+                c2 = _cost_of(cand, dtype, sib)
                 if c2 >= it["cost"] + p_["cost"]:
                     continue
                 it["X"], it["members"], it["cost"] = X2, mem2, c2
@@ -371,7 +383,7 @@ def plan_template(index_sets, order, dtype, fixed=(), merge=None):
         R, X = it["R"], it["X"]
         w, k = len(R), len(X)
         masks, smasks = _masks(it["members"], X, R)
-        if w + k <= SMALL_ITER_BITS:
+        if w + k <= sib:
             # small iteration space: K2 stage, scalar-path tiles (latency-bound
             # work; a K2 dependency hop costs ~1.5 us against ~7 us for a K1 node)
             L, st = min(w, SMALL_TILE_BITS[dtype]), 0

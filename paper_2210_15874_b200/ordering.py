@@ -282,14 +282,15 @@ def _raw_inputs(tn: TensorNetwork) -> np.ndarray:
 
 def _template(tn, order, backend, fixed=()):
     struct, _, plans = NETWORK_INPUTS.get(tn)
-    okey = (tuple(order), tuple(fixed), backend.dtype)
+    okey = (tuple(order), tuple(fixed), backend.dtype, backend.threshold)
     got = plans.get(okey)
     if got is not None:
         return got
     key = ("tmpl", struct) + okey
     hit = PLAN_CACHE.get(key)
     if hit is None:
-        hit = E.plan_template(list(struct), order, backend.dtype, fixed)
+        hit = E.plan_template(list(struct), order, backend.dtype, fixed,
+                              small_iter_bits=E.small_iter_bits_for(backend.threshold))
         PLAN_CACHE.put(key, hit)
     plans[okey] = (key, hit)
     return key, hit
@@ -320,8 +321,10 @@ def ref_stats(tmpl, backend, item_elapsed=None):
         el = np.zeros(len(tmpl.ref_w), np.int64)
     else:
         el = np.where(tmpl.ref_last == 1, item_elapsed[tmpl.ref_item], 0)
-    return [BucketStats(width=int(w), elapsed_ns=int(e), backend_used=backend.route(int(w)))
-            for w, e in zip(tmpl.ref_w, el)]
+    # the route a bucket actually took: its item's kernel (K2 small stage or K1)
+    small = tmpl.variant[tmpl.ref_item] == E.VARIANT_SMALL
+    return [BucketStats(width=int(w), elapsed_ns=int(e), backend_used="b200-small" if sm else "b200-large")
+            for w, e, sm in zip(tmpl.ref_w, el, small)]
 
 
 _NOPROFILE_STATS = {}
@@ -354,7 +357,7 @@ def contract_network(tn: TensorNetwork, order, backend: Backend = None, mem_cap:
     key, tmpl = _template(tn, order, backend)   # raises for indices missing from the order
     _check_cap(tmpl, backend, mem_cap)
     struct, raw, plans = NETWORK_INPUTS.get(tn)
-    xkey = ("exec", tuple(order), backend.dtype, backend.device, backend.profile)
+    xkey = ("exec", tuple(order), backend.dtype, backend.threshold, backend.device, backend.profile)
     got = plans.get(xkey)
     if got is None:
         got = plans[xkey] = _executor(key, lambda: E.Program([E.Instance(tmpl)], backend.dtype), backend, 1)

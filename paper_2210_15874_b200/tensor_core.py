@@ -29,10 +29,12 @@ KINDS = (B200,)
 class Backend:
     """Kernel policy.  `kind` is always "b200".
 
-    threshold: buckets with result width <= threshold are reported as the
-      small-bucket schedule ("b200-small"), wider ones as the fused large-bucket
-      path ("b200-large") — the B200 analogue of the reference's Mixed routing
-      (src/tensor_core.py:176-184); both run inside the same persistent launch.
+    threshold: buckets with result width <= threshold (w + k <= threshold + 1
+      for a merged item summing k indices) run in the batched small-bucket
+      schedule (K2 persistent stages, "b200-small"), wider ones in the fused
+      large-bucket kernels (K1, "b200-large") — the B200 analogue of the
+      reference's Mixed routing (src/tensor_core.py:176-184); both run inside
+      the same CUDA graph.  `tune-threshold` (tuning.py) picks it on the B200.
     dtype: "complex64" or "complex128" (the reference is complex128 only).
     device: CUDA device ordinal.
     profile: record per-bucket device time (BucketStats.elapsed_ns).

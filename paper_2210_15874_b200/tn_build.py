@@ -211,9 +211,10 @@ def zz_sandwich_network(c: Circuit, edge, prune: bool = True) -> TensorNetwork:
     return _sandwich(gates, edge, qubits)
 
 
-def extract_lightcone(c: Circuit, edge, cone: str = "reference") -> Lightcone:
+def extract_lightcone(c: Circuit, edge, cone: str = "reference", simplify: bool = False) -> Lightcone:
     """Lightcone network of edge (u, v) (src/tn_build.py:145-151).
-    cone="tight" uses the commutation-aware cone (QAOA MaxCut circuits only)."""
+    cone="tight" uses the commutation-aware cone (QAOA MaxCut circuits only);
+    simplify=True applies simplify_network (same value, fewer tensors)."""
     if cone not in CONES:
         raise ValueError(f"unknown cone mode {cone!r}")
     u, v = edge
@@ -223,8 +224,94 @@ def extract_lightcone(c: Circuit, edge, cone: str = "reference") -> Lightcone:
         gates, qubits = cone_gates(c, edge)
     else:
         gates, qubits = tight_cone_gates(c, edge)
-    return Lightcone(edge=tuple(edge), cone_qubits=qubits | set(edge),
-                     network=_sandwich(gates, edge, qubits))
+    net = _sandwich(gates, edge, qubits)
+    if simplify:
+        net = simplify_network(net)
+    return Lightcone(edge=tuple(edge), cone_qubits=qubits | set(edge), network=net)
+
+
+def simplify_network(tn: TensorNetwork, max_rank: int | None = None) -> TensorNetwork:
+    """Value-preserving network simplification before ordering (SURVEY §8(f)
+    row 2): repeatedly
+      * fold a tensor whose indices are a subset of another tensor's into it
+        (element-wise product; adjacent diagonal gates, Z / ket0 vectors),
+      * contract the two tensors sharing a closed index that no other tensor
+        holds when the result is no larger than the larger of the two (the
+        RX = H.RZ.H triplet of src/tn_build.py:57-66 becomes one rank-2
+        tensor and its middle wire disappears).
+    Only gate-sized host tensors are touched (rank <= max(max_rank, ranks
+    already present)); the contraction itself stays on the device.  The
+    network's value is unchanged up to rounding; its bucket structure is not
+    the reference's, so use it through qaoa_energy(simplify=True) /
+    extract_lightcone(simplify=True), not for bucket-level parity."""
+    import numpy as _np
+    opn = set(tn.open_indices)
+    ts = {i: (tuple(t.indices), _np.asarray(t.data, _np.complex128)) for i, t in enumerate(tn.tensors)}
+    lim = max_rank if max_rank is not None else max((len(ix) for ix, _ in ts.values()), default=0)
+    where = {}
+    for i, (ix, _) in ts.items():
+        for a in ix:
+            where.setdefault(a, set()).add(i)
+    nxt = len(ts)
+
+    def remove(i):
+        for a in ts[i][0]:
+            where[a].discard(i)
+        del ts[i]
+
+    def add(ix, d):
+        nonlocal nxt
+        ts[nxt] = (ix, d)
+        for a in ix:
+            where.setdefault(a, set()).add(nxt)
+        nxt += 1
+        return nxt - 1
+
+    def fold_into(small, big):
+        six, sd = ts[small]
+        bix, bd = ts[big]
+        sub = "".join(chr(97 + bix.index(a)) for a in six)
+        full = "".join(chr(97 + k) for k in range(len(bix)))
+        nd = _np.einsum(f"{full},{sub}->{full}", bd, sd) if six else bd * sd
+        remove(small)
+        remove(big)
+        return add(bix, nd)
+
+    changed = True
+    while changed:
+        changed = False
+        # subset folds (smallest tensors first, deterministic)
+        for i in sorted(ts, key=lambda k: (len(ts[k][0]), k)):
+            if i not in ts:
+                continue
+            ix = ts[i][0]
+            if not ix:
+                continue
+            cands = set.intersection(*(where[a] for a in ix)) - {i}
+            cands = [j for j in cands if len(ts[j][0]) >= len(ix)]
+            if cands:
+                j = min(cands, key=lambda k: (len(ts[k][0]), k))
+                fold_into(i, j)
+                changed = True
+        # rank-non-increasing pair contractions over closed indices
+        for a in sorted(where):
+            holders = where.get(a, ())
+            if a in opn or len(holders) != 2:
+                continue
+            i, j = sorted(holders)
+            aix, ad = ts[i]
+            bix, bd = ts[j]
+            out = tuple(x for x in aix if x != a) + tuple(x for x in bix if x != a and x not in aix)
+            if len(out) > max(len(aix), len(bix), 0) or len(out) > lim:
+                continue
+            letters = {x: chr(97 + k) for k, x in enumerate(dict.fromkeys(aix + bix))}
+            nd = _np.einsum("".join(letters[x] for x in aix) + "," + "".join(letters[x] for x in bix) + "->" +
+                            "".join(letters[x] for x in out), ad, bd)
+            remove(i)
+            remove(j)
+            add(out, nd)
+            changed = True
+    return TensorNetwork([Tensor(ix, d) for _, (ix, d) in sorted(ts.items())], tn.open_indices)
 
 
 def _check_residue(edge, value, dtype="complex128"):
@@ -246,6 +333,7 @@ def qaoa_energy_detailed(
     slice_target: int | None = None,
     n_gpus: int | None = None,
     group=None,
+    simplify: bool = False,
 ):
     """Per-edge <Z_u Z_v> and bucket stats, one lightcone per edge
     (src/tn_build.py:166-186).
@@ -260,7 +348,7 @@ def qaoa_energy_detailed(
     from . import distributed as D
     backend = backend or Backend()
     circuit = qaoa_maxcut_circuit(g, params)
-    cones = [extract_lightcone(circuit, e, cone=cone) for e in g.edges]
+    cones = [extract_lightcone(circuit, e, cone=cone, simplify=simplify) for e in g.edges]
     plan = D.plan_units(cones, backend, heuristic=heuristic, mem_cap=mem_cap,
                         slice_target=slice_target, n_workers=n_workers)
     values, stats = D.run_units(plan, backend, group=group, n_gpus=n_gpus)

@@ -243,3 +243,34 @@ def test_native_greedy_order_matches_python(seed):
     opened = Q.TensorNetwork(tn.tensors, open_indices=tuple(ids[:: 7]))
     for h in ("minfill", "mindegree"):
         assert Q.greedy_order(opened, h) == OR.greedy_order_py(opened, h)
+
+
+def test_simplify_network_preserves_value():
+    """simplify_network: same value through the oracle,
+    fewer tensors, RX triplets folded."""
+    from paper_2210_15874_b200 import tn_build as T
+    from oracle import qtn_oracle as O
+    g = Q.random_regular_graph(12, 3, seed=1)
+    c = Q.qaoa_maxcut_circuit(g, Q.QaoaParams.seeded(2, 3))
+    for e in g.edges[:4]:
+        for cone in ("reference", "tight"):
+            lc = Q.extract_lightcone(c, e, cone=cone)
+            s = T.simplify_network(lc.network)
+            assert len(s.tensors) < len(lc.network.tensors)
+            v1, _ = O.contract_network([(t.indices, t.data) for t in lc.network.tensors], Q.greedy_order(lc.network))
+            v2, _ = O.contract_network([(t.indices, t.data) for t in s.tensors], Q.greedy_order(s))
+            assert abs(v1 - v2) < 1e-13
+    # amplitude networks (non-QAOA gates): value preserved
+    rng = np.random.default_rng(0)
+    gates = []
+    for _ in range(30):
+        a, b = (int(x) for x in rng.choice(5, 2, replace=False))
+        kind = ["H", "RX", "RZ", "ZZ", "CX"][int(rng.integers(5))]
+        ang = float(rng.uniform(0, 3)) if kind in ("RX", "RZ", "ZZ") else None
+        gates.append(Q.Gate(kind, (a, b) if kind in ("ZZ", "CX") else (a,), ang))
+    circ = Q.Circuit(5, gates)
+    tn = Q.amplitude_network(circ, [0, 1, 1, 0, 1])
+    s = T.simplify_network(tn)
+    v1, _ = O.contract_network([(t.indices, t.data) for t in tn.tensors], Q.greedy_order(tn))
+    v2, _ = O.contract_network([(t.indices, t.data) for t in s.tensors], Q.greedy_order(s))
+    assert abs(v1 - v2) < 1e-12 and len(s.tensors) < len(tn.tensors)
