@@ -4,7 +4,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 MINB ?= 2
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -cudart static -Iinclude -DQTN_MINB=$(MINB)
 LIB := paper_2210_15874_b200/lib/libqtn_b200.so
-SRC := paper_2210_15874_b200/csrc/qtn_b200.cu paper_2210_15874_b200/csrc/bucket_strided.cu paper_2210_15874_b200/csrc/planner.cpp
+SRC := paper_2210_15874_b200/csrc/qtn_b200.cu paper_2210_15874_b200/csrc/bucket_strided.cu paper_2210_15874_b200/csrc/planner.cpp paper_2210_15874_b200/csrc/plan_template.cpp
 
 all: $(LIB)
 

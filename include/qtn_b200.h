@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define QTN_ABI_VERSION 6
+#define QTN_ABI_VERSION 7
 
 enum {
   QTN_OK = 0,
@@ -182,6 +182,41 @@ int qtn_graph_destroy(qtn_graph_t* g);
 int qtn_greedy_order(int32_t n_tensors, const int32_t* tensor_ptr, const int64_t* tensor_idx,
                      int32_t n_open, const int64_t* open_idx, int32_t heuristic,
                      int64_t* order_out, int32_t* n_out);
+/* ---- Host program planner (no device needed) ----
+ * qtn_plan_build replays the bucket assignment of the reference's
+ * contract_network (src/ordering.py:165-187) over index sets only, merges
+ * bucket chains into k-sum items under the engine's cost model and lays the
+ * items out (tile bits, staging, step mask, member classes, kernel variant):
+ * the C++ restatement of engine.plan_template (identical output, tested).
+ * Input: CSR index lists in each tensor's own axis order, the elimination
+ * order, the sliced (fixed) indices and the cost-model parameters.
+ * Output arrays (int64, fetched by id after qtn_plan_array_len): */
+enum {
+  QTN_PLAN_W = 0, QTN_PLAN_K, QTN_PLAN_L, QTN_PLAN_LEVEL, QTN_PLAN_OUT_OFF, QTN_PLAN_MEM_PTR,
+  QTN_PLAN_MEM_KIND, QTN_PLAN_MEM_REF, QTN_PLAN_MEM_MASK, QTN_PLAN_MEM_SMASK, QTN_PLAN_SMEM,
+  QTN_PLAN_STMASK, QTN_PLAN_MEM_CLS, QTN_PLAN_VARIANT, QTN_PLAN_REF_W, QTN_PLAN_REF_ITEM,
+  QTN_PLAN_REF_LAST, QTN_PLAN_REF_ELEMS, QTN_PLAN_BUCKET_INDEX, QTN_PLAN_FIN_KIND, QTN_PLAN_FIN_REF,
+  QTN_PLAN_IN_OFF, QTN_PLAN_GDST, QTN_PLAN_GSRC, QTN_PLAN_GFIX, /* n_fixed rows of len(GDST) */
+  QTN_PLAN_N_ARRAYS
+};
+typedef struct {
+  int32_t elem_bytes, tile_bits, small_tile_bits, min_tile_bits;
+  int32_t kmax, max_members, vec, nt;
+  int32_t small_iter_bits, merge, resident_blocks;
+  int64_t smem_budget;
+  double hop_s, hop_k2_s, bw_bps, block_terms_ps, small_load_s;
+} qtn_plan_params_t;
+typedef struct qtn_plan qtn_plan_t;
+int qtn_plan_build(int32_t n_tensors, const int32_t* tensor_ptr, const int64_t* tensor_idx,
+                   int32_t n_order, const int64_t* order, int32_t n_fixed, const int64_t* fixed,
+                   const qtn_plan_params_t* params, qtn_plan_t** out);
+/* s[0] = input elements, s[1] = intermediate elements, s[2] = raw source
+ * elements, s[3] = widest bucket. */
+int qtn_plan_scalars(const qtn_plan_t* plan, int64_t* s);
+int qtn_plan_array_len(const qtn_plan_t* plan, int32_t id, int64_t* len);
+int qtn_plan_array(const qtn_plan_t* plan, int32_t id, int64_t* dst);
+int qtn_plan_destroy(qtn_plan_t* plan);
+
 /* dst[e] = convert(src[sum_j bit_j(e) * src_strides[j]]) for e < 2^rank,
  * j = 0 the fastest dst axis; src/dst element types given separately
  * (complex128 -> complex64 narrowing allowed).  General axis permutation +

@@ -26,7 +26,7 @@ QTN_FINALIZE = -1
 MAX_MEMBERS = 8
 MAX_WIDTH = 40
 MAX_SUMMED = 6
-ABI_VERSION = 6
+ABI_VERSION = 7
 QTN_NODE_SMALL = 0
 QTN_NODE_LARGE = 1
 QTN_VARIANT_GENERIC = -1
@@ -45,7 +45,15 @@ EXPORTS = (
     "qtn_greedy_order",
     "qtn_bucket",
     "qtn_bucket_plan",
+    "qtn_plan_build",
+    "qtn_plan_scalars",
+    "qtn_plan_array_len",
+    "qtn_plan_array",
+    "qtn_plan_destroy",
 )
+PLAN_ARRAYS = ("w", "k", "L", "level", "out_off", "mem_ptr", "mem_kind", "mem_ref", "mem_mask", "mem_smask",
+               "smem_elems", "stmask", "mem_cls", "variant", "ref_w", "ref_item", "ref_last", "ref_elems",
+               "bucket_index", "fin_kind", "fin_ref", "in_off", "gdst", "gsrc", "gfix")
 
 BUCKET_DT = np.dtype([
     ("out_off", "<u8"), ("w", "<i4"), ("tile_bits", "<i4"), ("k", "<i4"), ("mem_begin", "<i4"),
@@ -90,6 +98,16 @@ class BucketDescC(ctypes.Structure):
                 ("reserved", ctypes.c_int32), ("out", ctypes.c_void_p), ("mem", BMemberC * MAX_MEMBERS)]
 
 
+class PlanParamsC(ctypes.Structure):
+    """qtn_plan_params_t: the engine's cost-model constants."""
+    _fields_ = [("elem_bytes", ctypes.c_int32), ("tile_bits", ctypes.c_int32), ("small_tile_bits", ctypes.c_int32),
+                ("min_tile_bits", ctypes.c_int32), ("kmax", ctypes.c_int32), ("max_members", ctypes.c_int32),
+                ("vec", ctypes.c_int32), ("nt", ctypes.c_int32), ("small_iter_bits", ctypes.c_int32),
+                ("merge", ctypes.c_int32), ("resident_blocks", ctypes.c_int32), ("smem_budget", ctypes.c_int64),
+                ("hop_s", ctypes.c_double), ("hop_k2_s", ctypes.c_double), ("bw_bps", ctypes.c_double),
+                ("block_terms_ps", ctypes.c_double), ("small_load_s", ctypes.c_double)]
+
+
 _lib = None
 
 
@@ -126,6 +144,17 @@ def load(path: str = LIB_PATH):
     lib.qtn_bucket.argtypes = [ctypes.POINTER(BucketDescC), vp]
     lib.qtn_bucket_plan.restype = ctypes.c_int
     lib.qtn_bucket_plan.argtypes = [ctypes.POINTER(BucketDescC), ctypes.POINTER(i32)]
+    lib.qtn_plan_build.restype = ctypes.c_int
+    lib.qtn_plan_build.argtypes = [i32, vp, vp, i32, vp, i32, vp, ctypes.POINTER(PlanParamsC),
+                                   ctypes.POINTER(ctypes.c_void_p)]
+    lib.qtn_plan_scalars.restype = ctypes.c_int
+    lib.qtn_plan_scalars.argtypes = [vp, vp]
+    lib.qtn_plan_array_len.restype = ctypes.c_int
+    lib.qtn_plan_array_len.argtypes = [vp, i32, ctypes.POINTER(i64)]
+    lib.qtn_plan_array.restype = ctypes.c_int
+    lib.qtn_plan_array.argtypes = [vp, i32, vp]
+    lib.qtn_plan_destroy.restype = ctypes.c_int
+    lib.qtn_plan_destroy.argtypes = [vp]
     if lib.qtn_abi_version() != ABI_VERSION:
         raise NativeUnavailable(f"ABI mismatch: library {lib.qtn_abi_version()} != {ABI_VERSION}")
     _lib = lib
@@ -201,3 +230,38 @@ def bucket_plan(desc):
 def bucket_launch(desc, stream):
     lib = require_device()
     check(lib.qtn_bucket(ctypes.byref(desc), ctypes.c_void_p(stream)))
+
+
+def plan_build(index_lists, order, fixed, params):
+    """Run the native planner; returns (scalars, {name: int64 array})."""
+    lib = load()
+    ptr = np.zeros(len(index_lists) + 1, np.int32)
+    flat = []
+    for t, ids in enumerate(index_lists):
+        flat.extend(ids)
+        ptr[t + 1] = len(flat)
+    idx = np.asarray(flat, dtype=np.int64)
+    od = np.asarray([int(x) for x in order], dtype=np.int64)
+    fx = np.asarray([int(x) for x in fixed], dtype=np.int64)
+    h = ctypes.c_void_p()
+    rc = lib.qtn_plan_build(len(index_lists), ptr.ctypes.data_as(ctypes.c_void_p),
+                            idx.ctypes.data_as(ctypes.c_void_p) if len(idx) else None, len(od),
+                            od.ctypes.data_as(ctypes.c_void_p) if len(od) else None, len(fx),
+                            fx.ctypes.data_as(ctypes.c_void_p) if len(fx) else None, ctypes.byref(params),
+                            ctypes.byref(h))
+    if rc == QTN_E_INVALID:
+        raise ValueError(lib.qtn_last_error().decode(errors="replace"))
+    check(rc)
+    try:
+        sc = np.zeros(4, np.int64)
+        check(lib.qtn_plan_scalars(h, sc.ctypes.data_as(ctypes.c_void_p)))
+        out = {}
+        n = ctypes.c_int64(0)
+        for i, name in enumerate(PLAN_ARRAYS):
+            check(lib.qtn_plan_array_len(h, i, ctypes.byref(n)))
+            a = np.empty(n.value, np.int64)
+            check(lib.qtn_plan_array(h, i, a.ctypes.data_as(ctypes.c_void_p) if n.value else None))
+            out[name] = a
+        return sc, out
+    finally:
+        lib.qtn_plan_destroy(h)

@@ -46,17 +46,18 @@ class UnitPlan:
 
 def plan_units(cones, backend: Backend, heuristic="minfill", mem_cap=4 << 30, slice_target=None, n_workers=1):
     """Order every cone, slice the wide ones, build templates and units."""
-    from .ordering import MemoryCapError, dry_run, greedy_order, suggest_slicing
+    from .ordering import MemoryCapError, greedy_order, suggest_slicing
 
     def one(lc):
         tn = lc.network
         order = greedy_order(tn, heuristic)
-        width = dry_run(tn, order).contraction_width
+        ix = [t.indices for t in tn.tensors]
+        sib = E.small_iter_bits_for(backend.threshold)
+        tmpl = E.plan_template(ix, order, backend.dtype, small_iter_bits=sib)
         sliced = []
-        if slice_target is not None and width > slice_target:
+        if slice_target is not None and tmpl.max_width > slice_target:   # width = the dry run's
             sliced = suggest_slicing(tn, order, slice_target)
-        tmpl = E.plan_template([t.indices for t in tn.tensors], order, backend.dtype, fixed=sliced,
-                               small_iter_bits=E.small_iter_bits_for(backend.threshold))
+            tmpl = E.plan_template(ix, order, backend.dtype, fixed=sliced, small_iter_bits=sib)
         if memory_estimate(tmpl.max_width, backend.dtype) > mem_cap:
             raise MemoryCapError(tmpl.max_width, memory_estimate(tmpl.max_width, backend.dtype), mem_cap)
         raw = np.concatenate([np.asarray(t.data, np.complex128).ravel() for t in tn.tensors])

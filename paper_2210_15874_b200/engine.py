@@ -248,7 +248,41 @@ def small_iter_bits_for(threshold):
     return int(threshold) + 1
 
 
+def _plan_params(dtype, merge, sib):
+    return N.PlanParamsC(
+        elem_bytes=ELEM_BYTES[dtype], tile_bits=TILE_BITS[dtype], small_tile_bits=SMALL_TILE_BITS[dtype],
+        min_tile_bits=MIN_TILE_BITS[dtype], kmax=KMAX, max_members=N.MAX_MEMBERS, vec=VEC[dtype], nt=NT,
+        small_iter_bits=sib, merge=1 if merge else 0, resident_blocks=RESIDENT_BLOCKS[dtype],
+        smem_budget=SMEM_BUDGET, hop_s=HOP_S, hop_k2_s=HOP_K2_S, bw_bps=BW_BPS,
+        block_terms_ps=BLOCK_TERMS_PS[dtype], small_load_s=SMALL_LOAD_S)
+
+
 def plan_template(index_sets, order, dtype, fixed=(), merge=None, small_iter_bits=None):
+    """The symbolic plan of one network structure + order (+ sliced
+    indices), computed by the native planner (csrc/plan_template.cpp,
+    qtn_plan_build) — the C++ restatement of plan_template_py below, which
+    stays as its checker (tests compare the two array by array)."""
+    dtype = norm_dtype(dtype)
+    merge = MERGE_DEFAULT if merge is None else merge
+    sib = SMALL_ITER_BITS if small_iter_bits is None else int(small_iter_bits)
+    fixed = list(dict.fromkeys(int(f) for f in fixed))
+    sc, a = N.plan_build([tuple(int(i) for i in s) for s in index_sets], order, fixed, _plan_params(dtype, merge, sib))
+    ncanon = len(a["gdst"])
+    gfix = {f: a["gfix"][j * ncanon:(j + 1) * ncanon] for j, f in enumerate(fixed)}
+    return Template(
+        n_in_elems=int(sc[0]), n_inter_elems=int(sc[1]),
+        w=a["w"], k=a["k"], L=a["L"], level=a["level"], out_off=a["out_off"], mem_ptr=a["mem_ptr"],
+        mem_kind=a["mem_kind"], mem_ref=a["mem_ref"], mem_mask=a["mem_mask"].view(np.uint64),
+        mem_smask=a["mem_smask"].view(np.uint64), smem_elems=a["smem_elems"], stmask=a["stmask"],
+        mem_cls=a["mem_cls"], variant=a["variant"],
+        ref_w=a["ref_w"], ref_item=a["ref_item"], ref_last=a["ref_last"], ref_elems=a["ref_elems"],
+        bucket_index=a["bucket_index"], fin_kind=a["fin_kind"], fin_ref=a["fin_ref"],
+        in_off=a["in_off"], gdst=a["gdst"], gsrc=a["gsrc"], gfix=gfix, n_raw=int(sc[2]),
+        max_width=int(sc[3]),
+    )
+
+
+def plan_template_py(index_sets, order, dtype, fixed=(), merge=None, small_iter_bits=None):
     """Replay contract_network's bucket assignment (src/ordering.py:165-187)
     over index sets only and freeze it into a Template.
 

@@ -274,3 +274,47 @@ def test_simplify_network_preserves_value():
     v1, _ = O.contract_network([(t.indices, t.data) for t in tn.tensors], Q.greedy_order(tn))
     v2, _ = O.contract_network([(t.indices, t.data) for t in s.tensors], Q.greedy_order(s))
     assert abs(v1 - v2) < 1e-12 and len(s.tensors) < len(tn.tensors)
+
+
+def _same_template(a, b):
+    import dataclasses
+    for f in dataclasses.fields(a):
+        x, y = getattr(a, f.name), getattr(b, f.name)
+        if isinstance(x, np.ndarray):
+            assert x.shape == y.shape and np.array_equal(x, y), f.name
+        elif isinstance(x, dict):
+            assert x.keys() == y.keys() and all(np.array_equal(x[k], y[k]) for k in x), f.name
+        else:
+            assert x == y, f.name
+
+
+def test_native_planner_matches_python_planner():
+    """csrc/plan_template.cpp (qtn_plan_build) restates engine.plan_template_py:
+    identical templates on QAOA cones (both cone modes, both dtypes, merging
+    on/off, several K2 thresholds), sliced networks and random circuits."""
+    cases = []
+    g = Q.random_regular_graph(16, 3, seed=2)
+    c = Q.qaoa_maxcut_circuit(g, Q.QaoaParams.seeded(3, 1))
+    for e in g.edges[:6]:
+        for cone in ("reference", "tight"):
+            lc = Q.extract_lightcone(c, e, cone=cone)
+            cases.append((lc.network, Q.greedy_order(lc.network), ()))
+    for rec in load_json("networks.json"):
+        circ = Q.Circuit(rec["n"], [Q.Gate(a, tuple(b), x) for a, b, x in rec["gates"]])
+        tn = Q.amplitude_network(circ, rec["bits"])
+        cases.append((tn, rec["order_minfill"], tuple(rec["sliced"])))
+        cases.append((tn, rec["order_minfill"], ()))
+    for tn, order, fixed in cases:
+        ix = [t.indices for t in tn.tensors]
+        for dtype in ("complex64", "complex128"):
+            for merge, sib in ((True, 12), (False, 12), (True, 8), (True, 16)):
+                a = E.plan_template_py(ix, order, dtype, fixed, merge=merge, small_iter_bits=sib)
+                b = E.plan_template(ix, order, dtype, fixed, merge=merge, small_iter_bits=sib)
+                _same_template(a, b)
+
+
+def test_native_planner_errors():
+    tn = Q.amplitude_network(Q.Circuit(2, [Q.Gate("H", (0,)), Q.Gate("CX", (0, 1))]), [0, 0])
+    order = Q.greedy_order(tn)
+    with pytest.raises(ValueError, match="order is missing indices"):
+        E.plan_template([t.indices for t in tn.tensors], order[:-1], "complex64")
