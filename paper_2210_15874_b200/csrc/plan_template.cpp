@@ -404,7 +404,7 @@ int qtn_plan_build(int32_t n_tensors, const int32_t* tensor_ptr, const int64_t* 
         c = QTN_CLS_STREAMED;
       else if (lo == 0)
         c = QTN_CLS_UNIFORM;
-      else if (k == 1 && (lo & sm_) == 0)
+      else if (k <= 3 && (lo & sm_) == 0)
         c = QTN_CLS_INVARIANT;
       else
         c = QTN_CLS_VARYING;

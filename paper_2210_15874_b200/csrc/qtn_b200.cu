@@ -607,30 +607,36 @@ __device__ __forceinline__ void large_compute(const LargeCtx& S, const typename 
 #pragma unroll
     for (int c = 0; c < NS; ++c) sro[c] = (int64_t)S.sig[sm][c] << S.pc[sm];
   }
-  // thread-invariant members (k == 1): P[s] once per tile
+  // thread-invariant members (k <= 3): P[s] once per tile, with the
+  // tile-uniform product U[s] folded in
   T P[NS][VEC];
   bool haveP = false;
-  if (NS == 2) {
-    for (int i = 0; i < nm; ++i) {
-      if (S.cls[i] != QTN_CLS_INVARIANT) continue;
-      const T* q = sseg + S.seg[i] + S.gt[i][tid];
-      const int bb = (int)(S.mlo[i] & 1u);
+  for (int i = 0; i < nm; ++i) {
+    if (S.cls[i] != QTN_CLS_INVARIANT) continue;
+    const T* q = sseg + S.seg[i] + S.gt[i][tid];
+    const int bb = (int)(S.mlo[i] & 1u);
 #pragma unroll
-      for (int c = 0; c < NS; ++c) {
-        const T* qc = q + (S.sig[i][c] << S.pclo[i]);
+    for (int c = 0; c < NS; ++c) {
+      const T* qc = q + (S.sig[i][c] << S.pclo[i]);
 #pragma unroll
-        for (int v = 0; v < VEC; ++v) {
-          const T x = qc[v & bb];
-          P[c][v] = haveP ? cmul(P[c][v], x) : x;
-        }
+      for (int v = 0; v < VEC; ++v) {
+        const T x = qc[v & bb];
+        P[c][v] = haveP ? cmul(P[c][v], x) : x;
       }
-      haveP = true;
     }
+    haveP = true;
   }
-  const bool hu = S.has_u;
+  const bool hu0 = S.has_u;
   T U[NS];
 #pragma unroll
-  for (int c = 0; c < NS; ++c) U[c] = hu ? sseg[S.uoff + c] : T{};
+  for (int c = 0; c < NS; ++c) U[c] = hu0 ? sseg[S.uoff + c] : T{};
+  if (haveP && hu0) {
+#pragma unroll
+    for (int c = 0; c < NS; ++c)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) P[c][v] = cmul(U[c], P[c][v]);
+  }
+  const bool hu = hu0 && !haveP;
   // streamed loads of UNR steps are issued together before any of their
   // stores (the compiler cannot hoist them: loads and stores share the arena),
   // so each thread keeps UNR * NS 16-byte loads in flight
@@ -667,7 +673,7 @@ __device__ __forceinline__ void large_compute(const LargeCtx& S, const typename 
           for (int v = 0; v < VEC; ++v) prod[c][v] = started ? cmul(prod[c][v], U[c]) : U[c];
         started = true;
       }
-      if (NS == 2 && haveP) {
+      if (haveP) {
 #pragma unroll
         for (int c = 0; c < NS; ++c)
 #pragma unroll
@@ -865,8 +871,14 @@ int sm_count() {
 }
 
 int resident_grid(const void* fn, int smem, int* grid) {
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return cuda_err(e, "cudaFuncSetAttribute");
+  // the attribute only ever grows: other nodes of the same kernel may need more
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+  if (e != cudaSuccess) return cuda_err(e, "cudaFuncGetAttributes");
+  if (smem > fa.maxDynamicSharedSizeBytes) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return cuda_err(e, "cudaFuncSetAttribute");
+  }
   int nb = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, NT, smem);
   if (e != cudaSuccess) return cuda_err(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");

@@ -189,7 +189,7 @@ def member_classes(w, k, L, stm, masks):
             out.append(CLS_STREAMED)
         elif lo == 0:
             out.append(CLS_UNIFORM)
-        elif k == 1 and (lo & stm) == 0:
+        elif k <= 3 and (lo & stm) == 0:
             out.append(CLS_INVARIANT)
         else:
             out.append(CLS_VARYING)
