@@ -82,6 +82,7 @@ int cuda_err(cudaError_t e, const char* what) {
 #define QTN_ARENA_OK(P, o) ((P).arena_elems == 0 || ((int64_t)(o) >= 0 && (int64_t)(o) < (P).arena_elems))
 
 constexpr int NT = 256;                 // threads per block
+
 constexpr int MAXM = QTN_MAX_MEMBERS;   // members per item
 constexpr int MAXS = 16;                // vector steps per tile: 2^L / (VEC * NT)
 constexpr int MAXNS = 1 << QTN_MAX_SUMMED;
@@ -764,7 +765,7 @@ __device__ __forceinline__ void large_compute_generic(const LargeCtx& S, const t
 
 // NS < 0: generic compute.
 template <typename R, int NS, int NV, int ST, int NB0>
-__global__ void __launch_bounds__(NT) large_kernel(const qtn_program_t P, int32_t item) {
+__device__ __forceinline__ void large_body(const qtn_program_t& P, int32_t item) {
   using T = typename Cx<R>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sseg = reinterpret_cast<T*>(smem_raw);
@@ -800,6 +801,26 @@ __global__ void __launch_bounds__(NT) large_kernel(const qtn_program_t P, int32_
   }
 }
 
+// One kernel per element type so each gets its own register budget: complex64
+// runs best with the compiler's default allocation, complex128 with a cap
+// that keeps 3 blocks resident (measured on cfg-2: 0.671 -> 0.605 ms).
+template <int NS, int NV, int ST, int NB0>
+__global__ void __launch_bounds__(NT) large_kernel_c64(const qtn_program_t P, int32_t item) {
+  large_body<float, NS, NV, ST, NB0>(P, item);
+}
+template <int NS, int NV, int ST, int NB0>
+__global__ void __launch_bounds__(NT, 3) large_kernel_c128(const qtn_program_t P, int32_t item) {
+  large_body<double, NS, NV, ST, NB0>(P, item);
+}
+template <typename R, int NS, int NV, int ST, int NB0>
+struct LargeK {
+  static constexpr auto fn = large_kernel_c64<NS, NV, ST, NB0>;
+};
+template <int NS, int NV, int ST, int NB0>
+struct LargeK<double, NS, NV, ST, NB0> {
+  static constexpr auto fn = large_kernel_c128<NS, NV, ST, NB0>;
+};
+
 // ---- permutation (tensors entering a program in a non-canonical layout) ----
 struct PermStrides {
   int64_t s[QTN_MAX_WIDTH + 4];
@@ -827,13 +848,13 @@ using LargeFn = void (*)(const qtn_program_t, int32_t);
 
 template <typename R, int NS, int NV, int ST>
 LargeFn large_fn_nb0(int nb0) {
-  if (Cx<R>::VEC == 1) return large_kernel<R, NS, NV, ST, 0>;
+  if (Cx<R>::VEC == 1) return LargeK<R, NS, NV, ST, 0>::fn;
   switch (nb0) {
-    case 0: return large_kernel<R, NS, NV, ST, 0>;
-    case 1: return NV >= 1 ? large_kernel<R, NS, NV, ST, (NV >= 1 ? 1 : 0)> : nullptr;
-    case 2: return NV >= 2 ? large_kernel<R, NS, NV, ST, (NV >= 2 ? 2 : 0)> : nullptr;
-    case 3: return NV >= 3 ? large_kernel<R, NS, NV, ST, (NV >= 3 ? 3 : 0)> : nullptr;
-    case 4: return NV >= 4 ? large_kernel<R, NS, NV, ST, (NV >= 4 ? 4 : 0)> : nullptr;
+    case 0: return LargeK<R, NS, NV, ST, 0>::fn;
+    case 1: return NV >= 1 ? LargeK<R, NS, NV, ST, (NV >= 1 ? 1 : 0)>::fn : nullptr;
+    case 2: return NV >= 2 ? LargeK<R, NS, NV, ST, (NV >= 2 ? 2 : 0)>::fn : nullptr;
+    case 3: return NV >= 3 ? LargeK<R, NS, NV, ST, (NV >= 3 ? 3 : 0)>::fn : nullptr;
+    case 4: return NV >= 4 ? LargeK<R, NS, NV, ST, (NV >= 4 ? 4 : 0)>::fn : nullptr;
     default: return nullptr;
   }
 }
@@ -860,7 +881,7 @@ LargeFn large_fn(int variant) {
     else if (ks == 2) f = st ? large_fn_nv<R, 4, 1>(nv, nb0) : large_fn_nv<R, 4, 0>(nv, nb0);
     else if (ks == 3) f = st ? large_fn_nv<R, 8, 1>(nv, nb0) : large_fn_nv<R, 8, 0>(nv, nb0);
   }
-  return f ? f : large_kernel<R, -1, 0, 0, 0>;
+  return f ? f : LargeK<R, -1, 0, 0, 0>::fn;
 }
 
 int sm_count() {
