@@ -481,26 +481,35 @@ __global__ void __launch_bounds__(NT) k3v2_kernel(const __grid_constant__ Plan P
           i1 = *reinterpret_cast<const T*>(stb + off[0][0] + psb[0]);
         }
       }
+      // per member: the s = 0 and s = 1 planes as two base pointers, so each
+      // value is one shared load at [register offset + base]
+      const unsigned char* s1p[NB];
 #pragma unroll
-      for (int j = 0; j < NJ; ++j) {
-        if (j < nj) {
-          T p0 = i0, p1 = i1;
+      for (int b = 0; b < NB; ++b) s1p[b] = stb + psb[b];
+      auto result = [&](int j) {
+        T p0 = i0, p1 = i1;
 #pragma unroll
-          for (int b = B0; b < NB; ++b) {
-            const unsigned char* a = stb + off[b][j];
-            const T x0 = *reinterpret_cast<const T*>(a);
-            const T x1 = *reinterpret_cast<const T*>(a + psb[b]);
-            const bool first = !INV && b == 0;
-            p0 = first ? x0 : cmul(p0, x0);
-            p1 = first ? x1 : cmul(p1, x1);
-          }
-          if (HF && !INV) {
-            const T* f = reinterpret_cast<const T*>(Fb + offF[j]);
-            p0 = cmul(p0, f[0]);
-            p1 = cmul(p1, f[1]);
-          }
-          __stcs(out + oo[j], cadd(p0, p1));
+        for (int b = B0; b < NB; ++b) {
+          const T x0 = *reinterpret_cast<const T*>(stb + off[b][j]);
+          const T x1 = *reinterpret_cast<const T*>(s1p[b] + off[b][j]);
+          const bool first = !INV && b == 0;
+          p0 = first ? x0 : cmul(p0, x0);
+          p1 = first ? x1 : cmul(p1, x1);
         }
+        if (HF && !INV) {
+          const T* f = reinterpret_cast<const T*>(Fb + offF[j]);
+          p0 = cmul(p0, f[0]);
+          p1 = cmul(p1, f[1]);
+        }
+        __stcs(out + oo[j], cadd(p0, p1));
+      };
+      if (nj == NJ) {   // full tiles: no per-result guard
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) result(j);
+      } else {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+          if (j < nj) result(j);
       }
     }
     const int64_t hnn = h + 2 * G;
@@ -588,7 +597,8 @@ int make_plan(const qtn_bucket_desc_t* d, Plan* P, int* smem_bytes) {
   // ---- tile bits ----
   // A thread owns results tid + j * NT: tile bits 0..7 ("core") come from
   // tid, bits 8.. ("j bits") from j < NJ = 8 (c64) / 4 (c128).
-  const int tcap = d->dtype == QTN_C64 ? 11 : 10;
+  static const int tcap_env = getenv("QTN_K3_TCAP") ? atoi(getenv("QTN_K3_TCAP")) : 0;
+  const int tcap = std::min(d->dtype == QTN_C64 ? 11 : 10, tcap_env > 0 ? tcap_env : 99);
   const int nt_target = std::min(tcap, w);
   const int core = std::min(nt_target, 8);
   bool inT[64] = {};
