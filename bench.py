@@ -293,6 +293,34 @@ def run_ours(args):
     t_kern = max_over_ranks(t_kern, world)
 
     # c128 device time as a side figure (same program structure)
+    # live per-item breakdown: the same program with globaltimer stamps per
+    # item (first tile start -> last tile end), after warm-up, L2 flushed;
+    # algorithmic bytes per item = its reference buckets'
+    items = []
+    if rank == 0:
+        ext = E.Executor(prog, device=local, timing=True)
+        ext.stage_inputs([raw])
+        for _ in range(3):
+            ext.launch(stream)
+        acc = np.zeros(tmpl.n_items)
+        nrep = 20
+        for _ in range(nrep):
+            flush.zero_()
+            ext.launch(stream)
+            torch.cuda.synchronize()
+            t0_, t1_ = ext.fetch_timing()
+            g_ = prog.bucket_gid[0]
+            acc += np.maximum(t1_[g_] - t0_[g_], 0)
+        acc /= nrep
+        ibytes = np.zeros(tmpl.n_items)
+        np.add.at(ibytes, tmpl.ref_item, tmpl.ref_elems * E.ELEM_BYTES[dtype])
+        for it in np.argsort(-acc)[:3]:
+            items.append({"item": int(it), "w": int(tmpl.w[it]), "k": int(tmpl.k[it]),
+                          "kernel": "K2 small_kernel" if int(tmpl.variant[it]) == E.VARIANT_SMALL
+                          else f"K1 large_kernel variant {int(tmpl.variant[it]):#x}",
+                          "us": round(float(acc[it]) / 1e3, 1), "alg_MB": round(float(ibytes[it]) / 1e6, 1),
+                          "alg_GBps": round(float(ibytes[it]) / max(float(acc[it]), 1.0), 1)})
+        del ext
     side = {}
     if dtype == "complex64":
         tm2 = E.plan_template([t.indices for t in tn.tensors], order, "complex128")
@@ -342,7 +370,8 @@ def run_ours(args):
                      "frac": achieved / peak, "traffic": ncu_traffic(args.dtype), "peak_source": peak_src,
                      "kernel": "one program graph per step: K2 small_kernel stages + K1 large_kernel variants "
                                "(one cudaGraphLaunch); achieved = algorithmic bytes (SURVEY 8(d)) / device time",
-                     "achieved_executed": prog.executed_bytes() / (t_kern / args.steps) / 1e9},
+                     "achieved_executed": prog.executed_bytes() / (t_kern / args.steps) / 1e9,
+                     "top_items_live": items},
         "cpu_baseline": cpu,
         "e2e": {"value": world * args.steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": n_in,
                 "d2h_bytes_per_step": 16, "s_per_lightcone": t_e2e / args.steps,
