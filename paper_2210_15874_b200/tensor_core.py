@@ -97,6 +97,16 @@ class Tensor:
     def __setattr__(self, *a):
         raise AttributeError("Tensor is immutable")
 
+    @classmethod
+    def _trusted(cls, indices: tuple, data: np.ndarray) -> "Tensor":
+        """Internal constructor for the network builders: `indices` is a
+        tuple of distinct ints and `data` a read-only complex128 array of
+        shape (2,)*rank (shared gate arrays are safe: Tensors are immutable)."""
+        t = object.__new__(cls)
+        object.__setattr__(t, "indices", indices)
+        object.__setattr__(t, "data", data)
+        return t
+
     @property
     def rank(self) -> int:
         return len(self.indices)

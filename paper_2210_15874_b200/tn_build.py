@@ -59,31 +59,57 @@ class _WireIds:
         return self.counter - 1
 
 
+_GATE_DATA = {}   # (kind, angle, adjoint) -> read-only tensor data (shared by every network)
+
+
+def _gate_data(kind, qubits, angle, adjoint):
+    key = (kind, angle, adjoint, len(qubits))
+    d = _GATE_DATA.get(key)
+    if d is None:
+        g = Gate(kind, qubits, angle)
+        if g.is_diagonal:
+            d = gate_diagonal(g)
+            if adjoint:
+                d = d.conj()
+            d = np.array(d, dtype=np.complex128).reshape((2,) * g.arity)
+        else:
+            u = gate_unitary(g)
+            if adjoint:
+                u = u.conj().T
+            d = np.array(u, dtype=np.complex128).reshape((2,) * (2 * g.arity))
+        d.setflags(write=False)
+        if len(_GATE_DATA) < 4096:
+            _GATE_DATA[key] = d
+    return d
+
+
 def _add_gate(tensors, wires: _WireIds, g: Gate, adjoint: bool = False):
     """Gate -> tensor (src/tn_build.py:55-80).  RX(t) is lowered to H RZ(t) H so
     the rotation stays diagonal; diagonal gates reuse the live wire ids;
-    other gates get fresh output ids, tensor axes = outputs then inputs."""
+    other gates get fresh output ids, tensor axes = outputs then inputs.
+    Gate data arrays are computed once per (kind, angle, adjoint) and shared."""
     if g.kind == "RX":
-        q = g.qubits
-        _add_gate(tensors, wires, Gate("H", q))
-        _add_gate(tensors, wires, Gate("RZ", q, g.angle), adjoint)
-        _add_gate(tensors, wires, Gate("H", q))
+        (q,) = g.qubits
+        live = wires.live
+        h = _gate_data("H", (q,), None, False)
+        a = live[q]
+        b = wires.fresh()
+        tensors.append(Tensor._trusted((b, a), h))
+        tensors.append(Tensor._trusted((b,), _gate_data("RZ", (q,), g.angle, adjoint)))
+        c = wires.fresh()
+        tensors.append(Tensor._trusted((c, b), h))
+        live[q] = c
         return
+    d = _gate_data(g.kind, g.qubits, g.angle, adjoint)
     if g.is_diagonal:
-        d = gate_diagonal(g)
-        if adjoint:
-            d = d.conj()
-        tensors.append(Tensor(tuple(wires.live[q] for q in g.qubits), d.reshape((2,) * g.arity)))
+        tensors.append(Tensor._trusted(tuple(wires.live[q] for q in g.qubits), d))
         return
-    u = gate_unitary(g)
-    if adjoint:
-        u = u.conj().T
     ins = [wires.live[q] for q in g.qubits]
     outs = []
     for q in g.qubits:
         wires.live[q] = wires.fresh()
         outs.append(wires.live[q])
-    tensors.append(Tensor(tuple(outs) + tuple(ins), u.reshape((2,) * (2 * g.arity))))
+    tensors.append(Tensor._trusted(tuple(outs) + tuple(ins), d))
 
 
 def amplitude_network(c: Circuit, bitstring) -> TensorNetwork:
@@ -321,6 +347,9 @@ def _check_residue(edge, value, dtype="complex128"):
     return value.real
 
 
+_ENERGY_PLANS = {}   # structure key -> (UnitPlan, executor cache); insertion-ordered, 2 entries
+
+
 def qaoa_energy_detailed(
     g: Graph,
     params: QaoaParams,
@@ -345,13 +374,30 @@ def qaoa_energy_detailed(
     on algorithmic bytes and the unit values are combined with one
     all-reduce.  Accumulation is in sorted-edge then slice order, so the
     result is bitwise identical for any worker / GPU count."""
+    import dataclasses
     from . import distributed as D
     backend = backend or Backend()
     circuit = qaoa_maxcut_circuit(g, params)
     cones = [extract_lightcone(circuit, e, cone=cone, simplify=simplify) for e in g.edges]
-    plan = D.plan_units(cones, backend, heuristic=heuristic, mem_cap=mem_cap,
-                        slice_target=slice_target, n_workers=n_workers)
-    values, stats = D.run_units(plan, backend, group=group, n_gpus=n_gpus)
+    # the index structure of the cones does not depend on the angles: plans and
+    # device programs are reused across calls (angle sweeps), only the inputs
+    # are re-staged
+    struct = tuple(tuple(t.indices for t in lc.network.tensors) for lc in cones)
+    key = (struct, heuristic, mem_cap, slice_target, backend.dtype, backend.threshold, backend.profile,
+           n_gpus, id(group) if group is not None else None)
+    hit = _ENERGY_PLANS.get(key)
+    if hit is None:
+        plan = D.plan_units(cones, backend, heuristic=heuristic, mem_cap=mem_cap,
+                            slice_target=slice_target, n_workers=n_workers)
+        hit = _ENERGY_PLANS[key] = (plan, {})
+        while len(_ENERGY_PLANS) > 2:
+            _ENERGY_PLANS.pop(next(iter(_ENERGY_PLANS)))
+    else:
+        raws = [np.concatenate([np.asarray(t.data, np.complex128).ravel() for t in lc.network.tensors])
+                for lc in cones]
+        hit = (dataclasses.replace(hit[0], cones=list(cones), raws=raws), hit[1])
+    plan, cache = hit
+    values, stats = D.run_units(plan, backend, group=group, n_gpus=n_gpus, cache=cache)
     out = []
     for ci, lc in enumerate(cones):
         out.append((lc.edge, _check_residue(lc.edge, values[ci], backend.dtype), stats[ci]))

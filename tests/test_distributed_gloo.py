@@ -23,7 +23,7 @@ def _free_port():
     return p
 
 
-def _emulated_run_local(plan, mine, backend, device, budget_bytes=None):
+def _emulated_run_local(plan, mine, backend, device, budget_bytes=None, cache=None):
     import sys
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from emulator import run_program

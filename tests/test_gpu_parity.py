@@ -177,3 +177,26 @@ def test_forced_memory_reuse_on_device(monkeypatch):
             vals = ex.run(raws)
             for v, w in zip(vals, want):
                 assert abs(v.real - w) <= tol
+
+
+def test_energy_sweep_reuses_plans():
+    """qaoa_energy over an angle sweep: the second structure-identical call
+    reuses plans and device programs (only inputs re-staged) and still
+    matches the oracle for its own angles."""
+    import time
+    from paper_2210_15874_b200 import tn_build as T
+    g = Q.random_regular_graph(12, 3, seed=4)
+    vals = []
+    for seed in range(3):
+        params = Q.QaoaParams.seeded(2, seed)
+        e = Q.qaoa_energy(g, params, C128, cone="tight")
+        c = Q.qaoa_maxcut_circuit(g, params)
+        ref = 0.0
+        for edge in g.edges:
+            lc = Q.extract_lightcone(c, edge, cone="tight")
+            v, _ = O.contract_network([(t.indices, t.data) for t in lc.network.tensors], Q.greedy_order(lc.network))
+            ref += 0.5 * (1 - v.real)
+        assert abs(e - ref) <= 1e-10 * abs(ref)
+        vals.append(e)
+    assert len(set(vals)) == 3
+    assert any(len(cache) > 0 for _, cache in T._ENERGY_PLANS.values())
