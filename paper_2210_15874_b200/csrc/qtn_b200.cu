@@ -209,6 +209,7 @@ struct SmallCtx {
   int32_t tick;
   int32_t next;
   int32_t last;
+  int32_t item_end;   // first ticket after the current item
 };
 
 template <typename R>
@@ -261,7 +262,10 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
       }
       if (tid == 0) {
         S.item = lo;
-        if (lo != prepared) S.b = P.buckets[lo];
+        if (lo != prepared) {
+          S.b = P.buckets[lo];
+          S.item_end = lo < last_item ? __ldg(&P.tick_begin[lo + 1]) : n_tickets;
+        }
       }
     }
     __syncthreads();
@@ -382,6 +386,13 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
       if (P.timing) {
         atomicMin(&P.timing[2 * cur], t_start);
         atomicMax(&P.timing[2 * cur + 1], globaltimer());
+      }
+      // the prefetched next ticket belongs to another item: publish now (a
+      // dependent item may be waiting) instead of after the ticket search
+      if (S.next >= S.item_end) {
+        __threadfence();
+        atomicAdd(&done[pend_item], pend_cnt);
+        pend_cnt = 0;
       }
     }
   }
