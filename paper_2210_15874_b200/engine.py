@@ -69,15 +69,19 @@ def _tensor_align(size):
 KMAX = N.MAX_SUMMED
 SMALL_PROD_ELEMS = 1024   # smem products per round of a small tile (csrc)
 VEC = {"complex64": 2, "complex128": 1}
-# merge cost model (seconds), calibrated on the r01 per-bucket B200 timeline:
-# a dependency hop costs ~3 us of latency; streaming ~5.5 TB/s; one block
-# evaluates ~2.5e9 member-terms/s when every SM is shared by ~5 blocks; a
-# small-tile round is L2-latency bound (~0.65 us per dependent member load,
-# measured on the r01 K2 timeline).
-HOP_S = 5.0e-6            # K1 graph node
-HOP_K2_S = 1.5e-6         # item inside a K2 stage
-BW_BPS = 5.5e12
-BLOCK_TERMS_PS = {"complex64": 2.5e9, "complex128": 1.2e9}
+# merge cost model (seconds).  Effective constants, tuned end to end on the
+# B200 (sweep over hop cost and term rate, profiles/r01_configs.md): a K1
+# dependency hop (~3 us measured + the lost overlap of a serial node) is
+# charged 8 us, a hop inside a K2 stage 0.8 us; streaming ~5.5 TB/s; one
+# block evaluates ~5e9 member-terms/s (complex64); a small-tile round is
+# L2-latency bound (~0.65 us per dependent member load, r01 K2 timeline).
+# Tuned values: cfg-2 0.327 -> 0.318 ms, 45-cone graph 10.4 -> 9.5 ms, cfg-3
+# 0.286 -> 0.267 s.  QTN_* environment overrides are for A/B sweeps.
+HOP_S = float(os.environ.get("QTN_HOP_S", 8.0e-6))        # K1 graph node
+HOP_K2_S = float(os.environ.get("QTN_HOP_K2_S", 0.8e-6))   # item inside a K2 stage
+BW_BPS = float(os.environ.get("QTN_BW_BPS", 5.5e12))
+_TERMS_SCALE = float(os.environ.get("QTN_TERMS_SCALE", 1.0))
+BLOCK_TERMS_PS = {"complex64": 5.0e9 * _TERMS_SCALE, "complex128": 2.4e9 * _TERMS_SCALE}
 RESIDENT_BLOCKS = {"complex64": 296, "complex128": 296}
 SMALL_LOAD_S = 0.65e-6
 MIN_TILE_BITS = {"complex64": 9, "complex128": 8}   # vector path needs VEC*NT results
