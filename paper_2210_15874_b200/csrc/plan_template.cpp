@@ -81,9 +81,9 @@ struct Planner {
     }
   }
 
-  // engine._item_cost
-  double item_cost(int w, int k, int L, const vector<int64_t>& sizes, double hop) const {
-    const int64_t nm = std::max<int64_t>(1, (int64_t)sizes.size());
+  // engine._item_cost (nm_eff < 0: every member counts 1)
+  double item_cost(int w, int k, int L, const vector<int64_t>& sizes, double hop, double nm_eff = -1.0) const {
+    const int64_t nm_cnt = std::max<int64_t>(1, (int64_t)sizes.size());
     int64_t ssum = 0;
     for (int64_t s : sizes) ssum += s;
     const int64_t byt = (int64_t)P.elem_bytes * (((int64_t)1 << w) + ssum);
@@ -92,7 +92,10 @@ struct Planner {
     const int64_t nelem = (int64_t)1 << L;
     double per_tile;
     if (nelem >= (int64_t)P.vec * P.nt) {
-      per_tile = (double)((nelem << k) * nm) / P.block_terms_ps;
+      if (nm_eff < 0)
+        per_tile = (double)((nelem << k) * nm_cnt) / P.block_terms_ps;
+      else
+        per_tile = (double)(nelem << k) * nm_eff / P.block_terms_ps;
     } else {
       const int64_t rounds = ((nelem << k) + 2 * P.nt - 1) / (2 * P.nt);
       per_tile = 1e-6 + (double)rounds * P.small_load_s;
@@ -111,7 +114,18 @@ struct Planner {
     for (const Mem& mm : it.mem) sizes.push_back((int64_t)1 << mm.set.size());
     if (w + k <= sib) return item_cost(w, k, std::min(w, P.small_tile_bits), sizes, P.hop_k2_s);
     const int L = tile_bits(w, m, sm, nullptr);
-    return item_cost(w, k, L, sizes, P.hop_s);
+    double nm_eff = -1.0;
+    if (P.cheap_member_w != 1.0 && ((int64_t)1 << L) >= (int64_t)P.vec * P.nt) {
+      const uint64_t stm = step_mask(L, m);
+      const uint64_t full = (1ull << L) - 1;
+      int n_cheap = 0;
+      for (uint64_t x : m) {
+        const uint64_t lo = x & full;
+        if (lo != full && (lo == 0 || (k <= 3 && (lo & stm) == 0))) ++n_cheap;
+      }
+      nm_eff = std::max(1.0, (double)((int)m.size() - n_cheap) + P.cheap_member_w * (double)n_cheap);
+    }
+    return item_cost(w, k, L, sizes, P.hop_s, nm_eff);
   }
 
   // engine._step_mask: maximise (invariant staged members, mask)

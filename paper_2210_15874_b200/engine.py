@@ -81,6 +81,7 @@ HOP_S = float(os.environ.get("QTN_HOP_S", 8.0e-6))        # K1 graph node
 HOP_K2_S = float(os.environ.get("QTN_HOP_K2_S", 0.8e-6))   # item inside a K2 stage
 BW_BPS = float(os.environ.get("QTN_BW_BPS", 5.5e12))
 _TERMS_SCALE = float(os.environ.get("QTN_TERMS_SCALE", 1.0))
+CHEAP_MEMBER_W = float(os.environ.get("QTN_CHEAP_W", 1.0))   # per-result weight of uniform/invariant members
 BLOCK_TERMS_PS = {"complex64": 5.0e9 * _TERMS_SCALE, "complex128": 2.4e9 * _TERMS_SCALE}
 RESIDENT_BLOCKS = {"complex64": 296, "complex128": 296}
 SMALL_LOAD_S = 0.65e-6
@@ -214,11 +215,13 @@ def kernel_variant(w, k, L, cls, dtype, masks=()):
     return VARIANT_GENERIC
 
 
-def _item_cost(w, k, L, sizes, dtype, hop=None):
+def _item_cost(w, k, L, sizes, dtype, hop=None, nm_eff=None):
     """Estimated device time of one item: dependency hop + max(streaming,
-    per-tile term evaluation x waves of tiles)."""
+    per-tile term evaluation x waves of tiles).  nm_eff: members weighted by
+    their per-result cost (large items: uniform / invariant members count
+    CHEAP_MEMBER_W, see _cost_of)."""
     hop = HOP_S if hop is None else hop
-    nm = max(1, len(sizes))
+    nm = max(1, len(sizes)) if nm_eff is None else nm_eff
     byt = ELEM_BYTES[dtype] * ((1 << w) + sum(sizes))
     tiles = 1 << (w - L)
     waves = -(-tiles // RESIDENT_BLOCKS[dtype])
@@ -241,7 +244,14 @@ def _cost_of(it, dtype, small_iter_bits=None):
         L = min(w, SMALL_TILE_BITS[dtype])
         return _item_cost(w, k, L, [1 << len(s2) for _, _, s2 in it["members"]], dtype, hop=HOP_K2_S)
     L, _ = _tile_bits(w, masks, smasks, dtype)
-    return _item_cost(len(it["R"]), len(it["X"]), L, [1 << len(s2) for _, _, s2 in it["members"]], dtype)
+    nm_eff = None
+    if CHEAP_MEMBER_W != 1.0 and (1 << L) >= VEC[dtype] * NT:
+        stm = _step_mask(L, masks, dtype)
+        cls = member_classes(w, k, L, stm, masks)
+        n_cheap = sum(1 for c in cls if c in (CLS_UNIFORM, CLS_INVARIANT))
+        nm_eff = max(1.0, (len(cls) - n_cheap) + CHEAP_MEMBER_W * n_cheap)
+    return _item_cost(len(it["R"]), len(it["X"]), L, [1 << len(s2) for _, _, s2 in it["members"]], dtype,
+                      nm_eff=nm_eff)
 
 
 def small_iter_bits_for(threshold):
@@ -258,7 +268,7 @@ def _plan_params(dtype, merge, sib):
         min_tile_bits=MIN_TILE_BITS[dtype], kmax=KMAX, max_members=N.MAX_MEMBERS, vec=VEC[dtype], nt=NT,
         small_iter_bits=sib, merge=1 if merge else 0, resident_blocks=RESIDENT_BLOCKS[dtype],
         smem_budget=SMEM_BUDGET, hop_s=HOP_S, hop_k2_s=HOP_K2_S, bw_bps=BW_BPS,
-        block_terms_ps=BLOCK_TERMS_PS[dtype], small_load_s=SMALL_LOAD_S)
+        block_terms_ps=BLOCK_TERMS_PS[dtype], small_load_s=SMALL_LOAD_S, cheap_member_w=CHEAP_MEMBER_W)
 
 
 def plan_template(index_sets, order, dtype, fixed=(), merge=None, small_iter_bits=None):
