@@ -248,7 +248,9 @@ typedef struct {
   int32_t dtype;   /* QTN_C64 / QTN_C128 (members and output)                   */
   int32_t w;       /* result rank                                               */
   int32_t n_mem;   /* 1..QTN_MAX_MEMBERS                                        */
-  int32_t reserved;
+  int32_t k;       /* summed indices, iteration bits w .. w+k-1 (0 or 1: one
+                      bucket index; up to 3: a merged chain of buckets — the
+                      members then need not carry every summed index)       */
   void* out;       /* 2^w elements, C order over the sorted result indices      */
   qtn_bmember_t mem[QTN_MAX_MEMBERS];
 } qtn_bucket_desc_t;
@@ -257,6 +259,8 @@ typedef struct {
  * stream is synchronised).  Errors: QTN_E_INVALID (bad descriptor),
  * QTN_E_UNSUPPORTED (w > 31, rank > 32), QTN_E_CUDA. */
 int qtn_bucket(const qtn_bucket_desc_t* desc, void* stream);
+/* out[r] = sum over the 2^k assignments s of the summed bits (ascending) of
+ * prod_i data_i[...]; k > 1 is the program path's merged-chain form. */
 /* Plan only (no device), info[8]: [0] tile bits, [1] staged elements per
  * tile, [2] shared-memory bytes per block, [3] tiles, [4] staged members
  * (-1 = every member staged, generic kernel), [5] members folded into the

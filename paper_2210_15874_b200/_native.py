@@ -205,11 +205,13 @@ def permute(src_dtype, src_ptr, src_offset, dst_dtype, dst_ptr, rank, strides, s
                           ctypes.c_void_p(dst_ptr), int(rank), arr, ctypes.c_void_p(stream)))
 
 
-def bucket_desc(dtype_code, w, out_ptr, members):
-    """members: [(device_ptr, {iteration_bit: element_stride})]; bit w = summed index."""
+def bucket_desc(dtype_code, w, out_ptr, members, k=1):
+    """members: [(device_ptr, {iteration_bit: element_stride})]; bits w .. w+k-1
+    are the summed indices (k = 1: one reference bucket)."""
     d = BucketDescC()
     d.dtype = dtype_code
     d.w = w
+    d.reserved = k
     d.n_mem = len(members)
     d.out = out_ptr
     for i, (ptr, strides) in enumerate(members):

@@ -46,7 +46,8 @@ namespace qtn_k3 {
 
 constexpr int NT = 256;
 constexpr int MAXT = 12;              // tile bits
-constexpr int MAXL = MAXT + 1;        // local bits of a member (tile bits + s)
+constexpr int MAXKS = 3;              // summed bits (one bucket index, or a merged chain of up to 3)
+constexpr int MAXL = 14;              // local bits of a member (tile bits + summed bits <= 13)
 constexpr int MAXM = QTN_MAX_MEMBERS;
 constexpr int MAXN = QTN_MAX_WIDTH;   // non-tile result bits
 
@@ -56,12 +57,12 @@ struct Member {
   uint32_t lstride[MAXL];  // global stride of local bit q (ascending)
   uint16_t lphys[MAXL];    // shared-memory slot bits of local bit q (1<<q ^ swizzle)
   int8_t tq[MAXT];         // local bit of tile bit j, -1 if the member lacks it
-  int8_t sq;               // local bit of s
+  int8_t sq[MAXKS];        // local bit of summed bit i, -1 if the member lacks it
   int8_t nl;               // local bits
   int8_t vec;              // 2: stage stride-1 pairs with 16-byte copies (complex64)
   int32_t soff;            // element offset of the member's slots in a stage
   uint32_t fs[8];          // folded member: global stride of product-table bit b
-  int64_t sstride;         // global stride of s
+  int64_t sstride[MAXKS];  // global stride of summed bit i (0 = absent)
 };
 
 struct Plan {
@@ -69,6 +70,7 @@ struct Plan {
   int64_t onstride[MAXN];  // output stride of non-tile bit j (= 1 << bit)
   uint32_t otstride[MAXT]; // output stride of tile bit j
   int32_t w, nt, nn, nm;
+  int32_t k;               // summed bits (iteration bits w .. w+k-1)
   int32_t stage_elems;     // elements of one stage (all members)
   int32_t table_bytes;
   int64_t n_tiles;
@@ -80,6 +82,8 @@ struct Plan {
   int32_t f_off;           // byte offset of the two F buffers in dynamic smem
   int32_t bl_off;          // byte offset of the tile-base tables (v2)
   int32_t inv;             // v2: F (or big member 0) is the same for all of a thread's results
+  unsigned long long* timing;   // program item timing (first start, last end), or null
+  int32_t item;                 // program item id (timing slot)
   Member m[MAXM];
 };
 
@@ -105,8 +109,46 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
                : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Loads from the dynamic shared memory at byte offsets: indexing the
+// extern __shared__ array itself keeps the shared address space visible to
+// the compiler (LDS [reg + imm], no generic-window arithmetic per access).
+extern __shared__ __align__(16) unsigned char k3_dsmem[];
+#ifndef K3_LDS_ASM
+#define K3_LDS_ASM 1   // 0: C++ indexing (the compiler re-materialises the window base), 1: ld.shared
+#endif
+#if K3_LDS_ASM
+// ld.shared at a 32-bit shared address (K3_LDS_ASM=2: with a memory clobber)
+__device__ __forceinline__ uint32_t k3_smem_base() { return (uint32_t)__cvta_generic_to_shared(k3_dsmem); }
+#if K3_LDS_ASM == 2
+#define K3_CLOBBER : "memory"
+#else
+#define K3_CLOBBER
+#endif
+__device__ __forceinline__ float2 ld_sm(uint32_t a, float2*) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) K3_CLOBBER);
+  return v;
+}
+__device__ __forceinline__ double2 ld_sm(uint32_t a, double2*) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) K3_CLOBBER);
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T lds(uint32_t off) {
+  return ld_sm(off, static_cast<T*>(nullptr));
+}
+#else
+__device__ __forceinline__ uint32_t k3_smem_base() { return 0u; }
+template <typename T>
+__device__ __forceinline__ T lds(uint32_t off) {
+  return *reinterpret_cast<const T*>(k3_dsmem + off);
+}
+#endif
 
 // Per-member lookup tables in shared memory (built once per block).
 struct Tables {
@@ -246,7 +288,7 @@ __global__ void __launch_bounds__(NT) k3_kernel(const __grid_constant__ Plan P) 
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
     pl[i] = tab[i].PL[rl];
-    ps[i] = P.m[i].lphys[P.m[i].sq];
+    ps[i] = P.m[i].lphys[P.m[i].sq[0]];
   }
   const uint32_t ol = OL[rl];
   int buf = 0, ring = 0;
@@ -299,14 +341,15 @@ __global__ void __launch_bounds__(NT) k3_kernel(const __grid_constant__ Plan P) 
 // operand is loaded once per tile (INV).  Every shared-memory offset a thread
 // needs is tile-invariant and lives in registers; tile bases come from
 // 3 x 7-bit lookup tables.
-template <typename R>
+template <typename R, int MS>
 __device__ __forceinline__ void compute_F(const Plan& P, const uint32_t* FG, const int64_t* base,
                                           typename Cx<R>::T* F) {
   using T = typename Cx<R>::T;
-  const int n = 2 << P.nu;
+  const int k = MS ? P.k : 1;
+  const int n = (1 << k) << P.nu;
   for (int x = threadIdx.x; x < n; x += NT) {
-    const int u = x >> 1;
-    const bool s1 = x & 1;
+    const int u = x >> k;
+    const int s = x & ((1 << k) - 1);
     // all loads in flight before the first multiply (members in order)
     T v[MAXM];
 #pragma unroll
@@ -314,8 +357,15 @@ __device__ __forceinline__ void compute_F(const Plan& P, const uint32_t* FG, con
       if (f < P.nf) {
         const int i = P.fold[f];
         const Member& M = P.m[i];
+        int64_t so = 0;
+        if (MS) {
+          for (int q = 0; q < k; ++q)
+            if ((s >> q) & 1) so += M.sstride[q];
+        } else if (s) {
+          so = M.sstride[0];
+        }
         const T* src = reinterpret_cast<const T*>(M.ptr) + base[i] + FG[f * 32 + (u & 15)] +
-                       FG[f * 32 + 16 + (u >> 4)] + (s1 ? M.sstride : 0);
+                       FG[f * 32 + 16 + (u >> 4)] + so;
         v[f] = __ldg(src);
       }
     }
@@ -371,9 +421,10 @@ __device__ __forceinline__ void stage_big(const Plan& P, const StageRegs<R, NB>&
   cp_commit();
 }
 
-template <typename R, int NB, int HF, int INV>
+template <typename R, int NB, int HF, int INV, int MS>
 __global__ void __launch_bounds__(NT) k3v2_kernel(const __grid_constant__ Plan P) {
   using T = typename Cx<R>::T;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   constexpr int NJ = sizeof(R) == 4 ? 8 : 4;
   constexpr int B0 = (INV && !HF) ? 1 : 0;   // first big member read per result
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -416,6 +467,10 @@ __global__ void __launch_bounds__(NT) k3v2_kernel(const __grid_constant__ Plan P
   int64_t h = blockIdx.x;
   __syncthreads();
   if (h >= P.n_tiles) return;
+  // program graphs: inputs are predecessor outputs (PDL edge); standalone: no-op
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  unsigned long long t_start = 0;
+  if (P.timing && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   lut_bases(BL, nm + 1, h, sbase[0]);
   if (h + G < P.n_tiles) lut_bases(BL, nm + 1, h + G, sbase[1]);
   StageRegs<R, NB> SR;
@@ -431,8 +486,8 @@ __global__ void __launch_bounds__(NT) k3v2_kernel(const __grid_constant__ Plan P
   }
   __syncthreads();
   stage_big<R, NB>(P, SR, tab, sbase[0], stage0);
-  const int fbytes = (2 << P.nu) * (int)sizeof(T);
-  if (HF) compute_F<R>(P, FG, sbase[0], reinterpret_cast<T*>(F0));
+  const int fbytes = ((1 << P.k) << P.nu) * (int)sizeof(T);
+  if (HF) compute_F<R, MS>(P, FG, sbase[0], reinterpret_cast<T*>(F0));
 
   // tile-invariant per-thread offsets (bytes into a stage / F buffer; elements of out)
   const int ntile = 1 << P.nt;
@@ -446,11 +501,24 @@ __global__ void __launch_bounds__(NT) k3v2_kernel(const __grid_constant__ Plan P
       off[b][j] = ((uint32_t)(tab[b].PL[r & 63] ^ tab[b].PH[r >> 6]) + (uint32_t)P.m[P.big[b]].soff) * (uint32_t)sizeof(T);
     uint32_t u = 0;
     for (int b = 0; b < P.nu; ++b) u |= (uint32_t)((r >> P.fu[b]) & 1) << b;
-    offF[j] = u * 2u * (uint32_t)sizeof(T);
+    offF[j] = (u << P.k) * (uint32_t)sizeof(T);
     oo[j] = OL[r & 63] + OH[r >> 6];
   }
 #pragma unroll
-  for (int b = 0; b < NB; ++b) psb[b] = (uint32_t)P.m[P.big[b]].lphys[P.m[P.big[b]].sq] * (uint32_t)sizeof(T);
+  for (int b = 0; b < NB; ++b) {
+    const int8_t q0 = P.m[P.big[b]].sq[0];
+    psb[b] = q0 >= 0 ? (uint32_t)P.m[P.big[b]].lphys[q0] * (uint32_t)sizeof(T) : 0u;
+  }
+  // multi-sum (MS): byte offset of each summed bit's plane per big member
+  uint32_t sbit[NB][MAXKS];
+#pragma unroll
+  for (int b = 0; b < NB; ++b)
+#pragma unroll
+    for (int q = 0; q < MAXKS; ++q) {
+      const int8_t sq = q < P.k ? P.m[P.big[b]].sq[q] : (int8_t)-1;
+      sbit[b][q] = sq >= 0 ? (uint32_t)P.m[P.big[b]].lphys[sq] * (uint32_t)sizeof(T) : 0u;
+    }
+  const int NSr = 1 << P.k;
   const bool active = tid < ntile;
   const uint32_t stage_bytes = (uint32_t)P.stage_elems * (uint32_t)sizeof(T);
 
@@ -460,46 +528,85 @@ __global__ void __launch_bounds__(NT) k3v2_kernel(const __grid_constant__ Plan P
     const int rn = ring == 2 ? 0 : ring + 1;
     if (hn < P.n_tiles) {
       stage_big<R, NB>(P, SR, tab, sbase[rn], stage0 + (buf ^ 1) * stage_bytes);
-      if (HF) compute_F<R>(P, FG, sbase[rn], reinterpret_cast<T*>(F0 + (buf ^ 1) * fbytes));
+      if (HF) compute_F<R, MS>(P, FG, sbase[rn], reinterpret_cast<T*>(F0 + (buf ^ 1) * fbytes));
       cp_wait<1>();
     } else {
       cp_wait<0>();
     }
     __syncthreads();
-    const unsigned char* stb = stage0 + buf * stage_bytes;
-    const unsigned char* Fb = F0 + buf * fbytes;
+    const uint32_t stb = k3_smem_base() + (uint32_t)P.table_bytes + buf * stage_bytes;   // offsets into k3_dsmem
+    const uint32_t Fb = k3_smem_base() + (uint32_t)P.f_off + buf * (uint32_t)fbytes;
     T* out = reinterpret_cast<T*>(P.out) + sbase[ring][nm];
-    if (active) {
+    if (MS && active) {
+      // summed assignments s = 0 .. 2^k - 1 outermost (ascending, as the
+      // reference's bucket-by-bucket sums), a thread's NJ results inner
+      T acc[NJ];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) acc[j] = T{};
+      for (int s = 0; s < NSr; ++s) {
+        uint32_t sp[NB];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          uint32_t o = 0;
+#pragma unroll
+          for (int q = 0; q < MAXKS; ++q)
+            if ((s >> q) & 1) o += sbit[b][q];
+          sp[b] = stb + o;
+        }
+        T iv = T{};
+        if (INV) iv = HF ? lds<T>(Fb + offF[0] + s * (uint32_t)sizeof(T)) : lds<T>(sp[0] + off[0][0]);
+        auto term = [&](int j) {
+          T p = iv;
+#pragma unroll
+          for (int b = B0; b < NB; ++b) {
+            const T x = lds<T>(sp[b] + off[b][j]);
+            p = (!INV && b == 0) ? x : cmul(p, x);
+          }
+          if (HF && !INV) p = cmul(p, lds<T>(Fb + offF[j] + s * (uint32_t)sizeof(T)));
+          acc[j] = cadd(acc[j], p);   // acc starts at +0: s ascending, as the reference
+        };
+        if (nj == NJ) {
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) term(j);
+        } else {
+#pragma unroll
+          for (int j = 0; j < NJ; ++j)
+            if (j < nj) term(j);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+        if (j < nj) __stcs(out + oo[j], acc[j]);
+    }
+    if (!MS && active) {
       T i0 = T{}, i1 = T{};
       if (INV) {   // operand invariant across j: F, or big member 0
         if (HF) {
-          const T* f = reinterpret_cast<const T*>(Fb + offF[0]);
-          i0 = f[0];
-          i1 = f[1];
+          i0 = lds<T>(Fb + offF[0]);
+          i1 = lds<T>(Fb + offF[0] + (uint32_t)sizeof(T));
         } else {
-          i0 = *reinterpret_cast<const T*>(stb + off[0][0]);
-          i1 = *reinterpret_cast<const T*>(stb + off[0][0] + psb[0]);
+          i0 = lds<T>(stb + off[0][0]);
+          i1 = lds<T>(stb + off[0][0] + psb[0]);
         }
       }
-      // per member: the s = 0 and s = 1 planes as two base pointers, so each
+      // per member: the s = 0 and s = 1 planes as two base addresses, so each
       // value is one shared load at [register offset + base]
-      const unsigned char* s1p[NB];
+      uint32_t s1p[NB];
 #pragma unroll
       for (int b = 0; b < NB; ++b) s1p[b] = stb + psb[b];
       auto result = [&](int j) {
         T p0 = i0, p1 = i1;
 #pragma unroll
         for (int b = B0; b < NB; ++b) {
-          const T x0 = *reinterpret_cast<const T*>(stb + off[b][j]);
-          const T x1 = *reinterpret_cast<const T*>(s1p[b] + off[b][j]);
+          const T x0 = lds<T>(stb + off[b][j]);
+          const T x1 = lds<T>(s1p[b] + off[b][j]);
           const bool first = !INV && b == 0;
           p0 = first ? x0 : cmul(p0, x0);
           p1 = first ? x1 : cmul(p1, x1);
         }
         if (HF && !INV) {
-          const T* f = reinterpret_cast<const T*>(Fb + offF[j]);
-          p0 = cmul(p0, f[0]);
-          p1 = cmul(p1, f[1]);
+          p0 = cmul(p0, lds<T>(Fb + offF[j]));
+          p1 = cmul(p1, lds<T>(Fb + offF[j] + (uint32_t)sizeof(T)));
         }
         __stcs(out + oo[j], cadd(p0, p1));
       };
@@ -519,24 +626,31 @@ __global__ void __launch_bounds__(NT) k3v2_kernel(const __grid_constant__ Plan P
     buf ^= 1;
     ring = rn;
   }
+  if (P.timing && tid == 0) {
+    unsigned long long t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    atomicMin(&P.timing[2 * P.item], t_start);
+    atomicMax(&P.timing[2 * P.item + 1], t_end);
+  }
 }
 
 template <typename R, int NB, int HF>
-const void* k3v2_fn_inv(int inv) {
-  return inv ? (const void*)k3v2_kernel<R, NB, HF, 1> : (const void*)k3v2_kernel<R, NB, HF, 0>;
+const void* k3v2_fn_inv(int inv, int ms) {
+  if (ms) return inv ? (const void*)k3v2_kernel<R, NB, HF, 1, 1> : (const void*)k3v2_kernel<R, NB, HF, 0, 1>;
+  return inv ? (const void*)k3v2_kernel<R, NB, HF, 1, 0> : (const void*)k3v2_kernel<R, NB, HF, 0, 0>;
 }
 
 template <typename R>
-const void* k3v2_fn(int nb, int hf, int inv) {
+const void* k3v2_fn(int nb, int hf, int inv, int ms) {
   switch (nb * 2 + (hf ? 1 : 0)) {
-    case 2: return k3v2_fn_inv<R, 1, 0>(0);
-    case 3: return k3v2_fn_inv<R, 1, 1>(inv);
-    case 4: return k3v2_fn_inv<R, 2, 0>(inv);
-    case 5: return k3v2_fn_inv<R, 2, 1>(inv);
-    case 6: return k3v2_fn_inv<R, 3, 0>(inv);
-    case 7: return k3v2_fn_inv<R, 3, 1>(inv);
-    case 8: return k3v2_fn_inv<R, 4, 0>(inv);
-    case 9: return k3v2_fn_inv<R, 4, 1>(inv);
+    case 2: return k3v2_fn_inv<R, 1, 0>(0, ms);
+    case 3: return k3v2_fn_inv<R, 1, 1>(inv, ms);
+    case 4: return k3v2_fn_inv<R, 2, 0>(inv, ms);
+    case 5: return k3v2_fn_inv<R, 2, 1>(inv, ms);
+    case 6: return k3v2_fn_inv<R, 3, 0>(inv, ms);
+    case 7: return k3v2_fn_inv<R, 3, 1>(inv, ms);
+    case 8: return k3v2_fn_inv<R, 4, 0>(inv, ms);
+    case 9: return k3v2_fn_inv<R, 4, 1>(inv, ms);
     default: return nullptr;
   }
 }
@@ -575,17 +689,21 @@ int make_plan(const qtn_bucket_desc_t* d, Plan* P, int* smem_bytes) {
   if (!d->out) return fail(QTN_E_INVALID, "null output");
   const int esz = d->dtype == QTN_C64 ? 8 : 16;
   const int BB = d->dtype == QTN_C64 ? 4 : 3;   // slot bits of one 128-byte bank row
+  // summed bits: 1 (a reference bucket) or up to 3 (a merged chain, program items)
+  const int ks = d->k > 0 ? d->k : 1;
+  if (ks > MAXKS || w + ks > QTN_MAX_WIDTH + 1) return fail(QTN_E_UNSUPPORTED, "%d summed indices", ks);
   std::memset(P, 0, sizeof(*P));
   P->out = d->out;
   P->w = w;
+  P->k = ks;
   P->nm = nm;
   int rank[MAXM];
   for (int i = 0; i < nm; ++i) {
     const qtn_bmember_t& m = d->mem[i];
     if (!m.data) return fail(QTN_E_INVALID, "member %d: null data", i);
-    if (m.strides[w] <= 0) return fail(QTN_E_INVALID, "member %d does not carry the bucket index", i);
+    if (ks == 1 && m.strides[w] <= 0) return fail(QTN_E_INVALID, "member %d does not carry the bucket index", i);
     rank[i] = 0;
-    for (int b = 0; b <= w; ++b) {
+    for (int b = 0; b < w + ks; ++b) {
       if (m.strides[b] < 0) return fail(QTN_E_INVALID, "member %d: negative stride", i);
       if (m.strides[b]) ++rank[i];
     }
@@ -598,7 +716,8 @@ int make_plan(const qtn_bucket_desc_t* d, Plan* P, int* smem_bytes) {
   // A thread owns results tid + j * NT: tile bits 0..7 ("core") come from
   // tid, bits 8.. ("j bits") from j < NJ = 8 (c64) / 4 (c128).
   static const int tcap_env = getenv("QTN_K3_TCAP") ? atoi(getenv("QTN_K3_TCAP")) : 0;
-  const int tcap = std::min(d->dtype == QTN_C64 ? 11 : 10, tcap_env > 0 ? tcap_env : 99);
+  // local bits (tile + summed) stay <= 13: the staging tables are 6 + 7 bits
+  const int tcap = std::min(std::min(d->dtype == QTN_C64 ? 11 : 10, 13 - ks), tcap_env > 0 ? tcap_env : 99);
   const int nt_target = std::min(tcap, w);
   const int core = std::min(nt_target, 8);
   bool inT[64] = {};
@@ -609,7 +728,9 @@ int make_plan(const qtn_bucket_desc_t* d, Plan* P, int* smem_bytes) {
     int64_t tot = 0;
     for (int i = 0; i < nm; ++i) {
       if (!staged[i]) continue;
-      int nl = 1;
+      int nl = 0;
+      for (int q = 0; q < ks; ++q)
+        if (d->mem[i].strides[w + q]) ++nl;
       for (int j = 0; j < ntt; ++j)
         if (d->mem[i].strides[T[j]]) ++nl;
       tot += ((int64_t)1 << nl) + 1;   // +1: 16-byte aligned member slots
@@ -641,10 +762,10 @@ int make_plan(const qtn_bucket_desc_t* d, Plan* P, int* smem_bytes) {
     int64_t run = 1;
     while (run < run_target && nt < core) {
       int b = -1;   // the axis with stride == run
-      for (int c = 0; c <= w; ++c)
+      for (int c = 0; c < w + ks; ++c)
         if (m.strides[c] == run) b = c;
       if (b < 0) break;
-      if (b != w && !inT[b] && !add(b, true)) break;
+      if (b < w && !inT[b] && !add(b, true)) break;
       run *= 2;
     }
   }
@@ -681,6 +802,7 @@ int make_plan(const qtn_bucket_desc_t* d, Plan* P, int* smem_bytes) {
   int nb = 0, nf = 0;
   for (int i = 0; i < nm; ++i) nb += folded[i] ? 0 : 1, nf += folded[i] ? 1 : 0;
   P->v2 = (nb <= 4 && !v2_off) ? 1 : 0;
+  if (!P->v2 && ks > 1) return fail(QTN_E_UNSUPPORTED, "%d staged members with %d summed indices", nb, ks);
   if (!P->v2) {
     for (int i = 0; i < nm; ++i) folded[i] = false, staged[i] = true;
     nf = 0;
@@ -776,28 +898,34 @@ int make_plan(const qtn_bucket_desc_t* d, Plan* P, int* smem_bytes) {
     const qtn_bmember_t& m = d->mem[i];
     Member& M = P->m[i];
     M.ptr = m.data;
-    M.sstride = m.strides[w];
+    for (int q = 0; q < MAXKS; ++q) {
+      M.sstride[q] = q < ks ? m.strides[w + q] : 0;
+      M.sq[q] = -1;
+    }
     for (int j = 0; j < nn; ++j) M.nstride[j] = m.strides[N[j]];
     for (int b = 0; b < P->nu; ++b) M.fs[b] = (uint32_t)m.strides[T[P->fu[b]]];
-    // local bits: the member's bits in T u {s}, ascending stride
-    int lb[MAXL], nl = 0;   // iteration bit of local bit q (w = s)
+    // local bits: the member's bits in T u {summed bits}, ascending stride
+    int lb[MAXL], nl = 0;   // iteration bit of local bit q (>= w: summed)
     for (int j = 0; j < nt; ++j)
       if (m.strides[T[j]]) lb[nl++] = T[j];
-    lb[nl++] = w;
+    for (int q = 0; q < ks; ++q)
+      if (m.strides[w + q]) lb[nl++] = w + q;
     std::sort(lb, lb + nl, [&](int a, int b) { return m.strides[a] < m.strides[b]; });
     M.nl = (int8_t)nl;
     for (int q = 0; q < nl; ++q) M.lstride[q] = (uint32_t)m.strides[lb[q]];
     for (int j = 0; j < nt; ++j) M.tq[j] = -1;
+    uint32_t smask_local = 0;   // local bits of summed indices (never swizzle targets)
     for (int q = 0; q < nl; ++q) {
-      if (lb[q] == w) {
-        M.sq = (int8_t)q;
+      if (lb[q] >= w) {
+        M.sq[lb[q] - w] = (int8_t)q;
+        smask_local |= 1u << q;
       } else {
         for (int j = 0; j < nt; ++j)
           if (T[j] == lb[q]) M.tq[j] = (int8_t)q;
       }
     }
-    bool vec2 = esz == 8 && m.strides[lb[0]] == 1 && ((uintptr_t)m.data % 16) == 0;
-    for (int b = 0; b <= w; ++b)
+    bool vec2 = nl > 0 && esz == 8 && m.strides[lb[0]] == 1 && ((uintptr_t)m.data % 16) == 0;
+    for (int b = 0; b < w + ks; ++b)
       if (b != lb[0] && (m.strides[b] & 1)) vec2 = false;   // pairs stay 16-byte aligned
     M.vec = vec2 ? 2 : 1;
     // swizzle: local bits q >= BB that the compute-phase half-warp varies
@@ -813,7 +941,7 @@ int make_plan(const qtn_bucket_desc_t* d, Plan* P, int* smem_bytes) {
       const int q = M.tq[j];
       if (q < BB) continue;
       for (int b = lo_ok; b < BB; ++b)
-        if (b != M.sq && !((span >> b) & 1)) {
+        if (!((smask_local >> b) & 1) && !((span >> b) & 1)) {
           span |= 1u << b;
           M.lphys[q] ^= (uint16_t)(1u << b);
           break;
@@ -830,7 +958,7 @@ int make_plan(const qtn_bucket_desc_t* d, Plan* P, int* smem_bytes) {
   const int ntab = P->v2 ? nb : nm;
   P->table_bytes = (int32_t)(((int64_t)ntab * sizeof(Tables) + 128 * 4 + (int64_t)nf * 32 * 4 + 15) / 16 * 16);
   P->f_off = P->table_bytes + 2 * P->stage_elems * esz;
-  P->bl_off = P->f_off + (nf ? 2 * (2 << P->nu) * esz : 0);
+  P->bl_off = P->f_off + (nf ? 2 * ((1 << ks) << P->nu) * esz : 0);
   *smem_bytes = P->bl_off + (P->v2 ? (nm + 1) * 384 * 8 : 0);
   if (*smem_bytes > 227 * 1024) return fail(QTN_E_UNSUPPORTED, "bucket needs %d B of shared memory", *smem_bytes);
   return QTN_OK;
@@ -844,6 +972,37 @@ int sm_count() {
 }
 
 }  // namespace qtn_k3
+
+// Program-graph node for one item (called by qtn_graph_create, qtn_b200.cu):
+// plans K3 for `d` into `plan` (size qtn_k3_plan_bytes()) and returns the
+// kernel, grid and dynamic shared memory.
+size_t qtn_k3_plan_bytes() { return sizeof(qtn_k3::Plan); }
+
+int qtn_k3_node(const qtn_bucket_desc_t* d, unsigned long long* timing, int32_t item, void* plan, const void** fn,
+                int* grid, int* smem) {
+  using namespace qtn_k3;
+  Plan* P = reinterpret_cast<Plan*>(plan);
+  int rc = make_plan(d, P, smem);
+  if (rc) return rc;
+  if (!P->v2) return fail(QTN_E_UNSUPPORTED, "K3 node needs the staged/folded kernel");
+  P->timing = timing;
+  P->item = item;
+  *fn = d->dtype == QTN_C64 ? k3v2_fn<float>(P->nb, P->nf > 0, P->inv, P->k > 1)
+                            : k3v2_fn<double>(P->nb, P->nf > 0, P->inv, P->k > 1);
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, *fn);
+  if (e != cudaSuccess) return fail(QTN_E_CUDA, "cudaFuncGetAttributes: %s", cudaGetErrorString(e));
+  if (*smem > fa.maxDynamicSharedSizeBytes) {
+    e = cudaFuncSetAttribute(*fn, cudaFuncAttributeMaxDynamicSharedMemorySize, *smem);
+    if (e != cudaSuccess) return fail(QTN_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+  }
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, *fn, NT, *smem);
+  if (e != cudaSuccess) return fail(QTN_E_CUDA, "occupancy: %s", cudaGetErrorString(e));
+  if (per_sm < 1) return fail(QTN_E_UNSUPPORTED, "K3 cannot be resident with %d B smem", *smem);
+  *grid = (int)std::min<int64_t>(P->n_tiles, (int64_t)per_sm * sm_count());
+  return QTN_OK;
+}
 
 extern "C" {
 
@@ -872,10 +1031,16 @@ int qtn_bucket(const qtn_bucket_desc_t* d, void* stream) {
   int smem = 0;
   int rc = make_plan(d, &P, &smem);
   if (rc) return rc;
-  const void* fn = P.v2 ? (d->dtype == QTN_C64 ? k3v2_fn<float>(P.nb, P.nf > 0, P.inv) : k3v2_fn<double>(P.nb, P.nf > 0, P.inv))
+  const void* fn = P.v2 ? (d->dtype == QTN_C64 ? k3v2_fn<float>(P.nb, P.nf > 0, P.inv, P.k > 1)
+                                                : k3v2_fn<double>(P.nb, P.nf > 0, P.inv, P.k > 1))
                        : (d->dtype == QTN_C64 ? k3_fn<float>(P.nm) : k3_fn<double>(P.nm));
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return fail(QTN_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+  cudaFuncAttributes fa;   // the attribute only grows (graph nodes of the same kernel may need more)
+  cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+  if (e != cudaSuccess) return fail(QTN_E_CUDA, "cudaFuncGetAttributes: %s", cudaGetErrorString(e));
+  if (smem > fa.maxDynamicSharedSizeBytes) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return fail(QTN_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+  }
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NT, smem);
   if (e != cudaSuccess) return fail(QTN_E_CUDA, "occupancy: %s", cudaGetErrorString(e));

@@ -37,7 +37,9 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdarg>
+#include <cstring>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -928,6 +930,7 @@ struct LaunchSpec {
   qtn_program_t prog;
   int32_t a0, a1, a2;
   uint32_t* ctl;
+  std::vector<unsigned char> k3plan;   // K3 node: its Plan (kernel parameter)
 };
 
 int check_program(const qtn_program_t* p) {
@@ -977,6 +980,60 @@ int make_launch(const qtn_program_t* p, const qtn_node_t* nd, int ni, int32_t n_
 }  // namespace
 
 int qtn_internal_set_error(int code, const char* msg) { return set_err(code, "%s", msg); }
+
+// K3 (bucket_strided.cu) as a program node: expansion items whose staged
+// members K1 would gather per tile
+size_t qtn_k3_plan_bytes();
+int qtn_k3_node(const qtn_bucket_desc_t* d, unsigned long long* timing, int32_t item, void* plan, const void** fn,
+                int* grid, int* smem);
+
+namespace {
+
+int getenv_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && v[0] ? atoi(v) : dflt;
+}
+
+// Route a large item to K3?  QTN_K3_ROUTE: 0 never, 1 merged expansion items
+// (k >= 2, >= 2 varying staged members), 2 every large item, >= 10: every
+// large item at least that wide.  Default (measured on B200):
+// complex64 keeps K1 (K3 on merged expansions: cfg-2 -0.3 %, 45-cone graph
+// +2 %, cfg-3 +4 %); complex128 routes items of width >= 20 to K3 (cfg-2
+// 0.593 -> 0.497 ms, 45-cone graph +0.8 %).
+bool k3_route(const qtn_bucket_t& b, const qtn_member_t* mem, int dtype) {
+  static const int env = getenv_int("QTN_K3_ROUTE", -1);
+  const int mode = env >= 0 ? env : (dtype == QTN_C64 ? 0 : 20);
+  if (mode == 0 || b.w < 0 || b.k > 3 || b.w > 31 || b.n_mem > QTN_MAX_MEMBERS) return false;
+  if (mode == 2) return true;
+  if (mode >= 10) return b.w >= mode;   // A/B: every large item at least that wide
+  int nv = 0;
+  for (int i = 0; i < b.n_mem; ++i) nv += mem[b.mem_begin + i].cls == QTN_CLS_VARYING;
+  return b.k >= 2 && nv >= 2;
+}
+
+// canonical layout -> K3 strides: member offset (pext(s, smask) << popc(mask)) + pext(r, mask)
+void k3_desc(const qtn_program_t* p, const qtn_bucket_t& b, const qtn_member_t* mem, qtn_bucket_desc_t* d) {
+  const size_t esz = p->dtype == QTN_C64 ? 8 : 16;
+  memset(d, 0, sizeof(*d));
+  d->dtype = p->dtype;
+  d->w = b.w;
+  d->k = b.k;
+  d->n_mem = b.n_mem;
+  d->out = (char*)p->arena + b.out_off * esz;
+  for (int i = 0; i < b.n_mem; ++i) {
+    const qtn_member_t& m = mem[b.mem_begin + i];
+    d->mem[i].data = (const char*)p->arena + m.off * esz;
+    const int pc = __builtin_popcountll(m.mask);
+    int r = 0;
+    for (int bit = 0; bit < b.w; ++bit)
+      if ((m.mask >> bit) & 1) d->mem[i].strides[bit] = (int64_t)1 << r++;
+    int q = 0;
+    for (int j = 0; j < b.k; ++j)
+      if ((m.smask >> j) & 1) d->mem[i].strides[b.w + j] = (int64_t)1 << (pc + q++);
+  }
+}
+
+}  // namespace
 
 struct qtn_graph {
   cudaGraph_t graph = nullptr;
@@ -1040,6 +1097,13 @@ int qtn_graph_create(const qtn_program_t* p, const qtn_node_t* nodes, int32_t n_
         cudaMemcpy(items.data(), p->buckets, sizeof(qtn_bucket_t) * items.size(), cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cuda_err(e, "cudaMemcpy(items)");
   }
+  int64_t n_members = 0;
+  for (const qtn_bucket_t& b : items) n_members = std::max<int64_t>(n_members, (int64_t)b.mem_begin + std::max(0, b.n_mem));
+  std::vector<qtn_member_t> mems(n_members);
+  if (n_members && p->members && p->arena) {
+    const cudaError_t e = cudaMemcpy(mems.data(), p->members, sizeof(qtn_member_t) * mems.size(), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_err(e, "cudaMemcpy(members)");
+  }
   qtn_graph* g = new qtn_graph();
   cudaError_t e = cudaGraphCreate(&g->graph, 0);
   if (e != cudaSuccess) {
@@ -1061,6 +1125,19 @@ int qtn_graph_create(const qtn_program_t* p, const qtn_node_t* nodes, int32_t n_
     if (rc) {
       qtn_graph_destroy(g);
       return rc;
+    }
+    if (nd.kind == QTN_NODE_LARGE && p->arena && !mems.empty() && k3_route(items[nd.first], mems.data(), p->dtype)) {
+      qtn_bucket_desc_t d;
+      k3_desc(p, items[nd.first], mems.data(), &d);
+      specs[i].k3plan.resize(qtn_k3_plan_bytes());
+      const void* fn = nullptr;
+      int grid = 0, smem = 0;
+      if (qtn_k3_node(&d, p->timing, nd.first, specs[i].k3plan.data(), &fn, &grid, &smem) == QTN_OK) {
+        specs[i].fn = fn;
+        specs[i].grid = grid;
+        specs[i].smem = smem;
+        specs[i].args[0] = specs[i].k3plan.data();
+      }   // else: K1 stays (the K3 planner declined this item)
     }
     std::vector<cudaGraphNode_t> deps;
     for (int d = 0; d < nd.n_dep; ++d) {

@@ -137,3 +137,61 @@ def test_k3_strided_device_members_and_mixed_dtypes():
     out, _ = Q.contract_bucket(b, C64)
     assert isinstance(out, Q.DeviceTensor) and out.dtype == "complex64"
     np.testing.assert_allclose(out.data, ref, rtol=1e-5, atol=1e-5 * max(1.0, np.abs(ref).max()))
+
+
+def _multisum_case(w, k, nmem, seed, dtype, big_ranks=True):
+    """Members over result ids 1..w and summed ids w+1..w+k, random axis
+    orders; every summed index carried by at least one member."""
+    import torch
+    rng = np.random.default_rng(seed)
+    res = list(range(1, w + 1))
+    summ = list(range(w + 1, w + k + 1))
+    mem = []
+    for i in range(nmem):
+        if i == 0 and big_ranks:
+            ids = res + summ
+        else:
+            pick = [x for x in res if rng.random() < (0.6 if big_ranks else 0.2)]
+            sp = [x for x in summ if rng.random() < 0.7]
+            ids = pick + sp
+        mem.append(list(int(x) for x in rng.permutation(ids)))
+    for x in summ + res:                 # every index somewhere (result = union - summed)
+        if not any(x in m for m in mem):
+            mem[int(rng.integers(nmem))].append(x)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(seed)
+    cdt = torch.complex64 if dtype == "complex64" else torch.complex128
+    rdt = torch.float32 if dtype == "complex64" else torch.float64
+    data = []
+    for ids in mem:
+        n = 1 << len(ids)
+        x = torch.randn(2 * n, generator=gen, device="cuda", dtype=rdt) * (1.0 / np.sqrt(2.0))
+        data.append(torch.view_as_complex(x.view(n, 2)).view(cdt))
+    return res, summ, mem, data
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("w,k,nmem,big", [(10, 2, 3, True), (16, 2, 4, True), (20, 3, 4, True), (14, 3, 2, False),
+                                          (22, 2, 5, True), (9, 3, 6, False), (0, 2, 2, False), (5, 3, 3, True)])
+@pytest.mark.parametrize("dtype", ["complex64", "complex128"])
+def test_k3_multisum_vs_einsum(w, k, nmem, big, dtype):
+    """K3 with k summed indices (the program path's merged-chain items)."""
+    import torch
+    from paper_2210_15874_b200 import engine as E
+    res, summ, mem, data = _multisum_case(w, k, nmem, 7 + w + k, dtype, big)
+    bit = {a: w - 1 - j for j, a in enumerate(res)}
+    for q, a in enumerate(summ):
+        bit[a] = w + q
+    members = [(t.data_ptr(), {bit[a]: 1 << (len(ids) - 1 - ax) for ax, a in enumerate(ids)})
+               for ids, t in zip(mem, data)]
+    out = torch.empty(max(1, 1 << w), dtype=data[0].dtype, device="cuda")
+    d = N.bucket_desc(E.DTYPE_CODE[dtype], w, out.data_ptr(), members, k=k)
+    N.bucket_launch(d, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    letters = "abcdefghijklmnopqrstuvwxyzABCDEFGHIJKLMNOPQRSTUVWXYZ"
+    ops = [t.to(torch.complex128).view((2,) * len(ids)) for ids, t in zip(mem, data)]
+    subs = ",".join("".join(letters[a] for a in ids) for ids in mem)
+    ref = torch.einsum(subs + "->" + "".join(letters[a] for a in res), *ops).reshape(-1)
+    tol = 1e-5 if dtype == "complex64" else 1e-12
+    err = (out[: 1 << w].to(torch.complex128) - ref).abs().max().item()
+    assert err <= tol * max(1.0, ref.abs().max().item()), err
