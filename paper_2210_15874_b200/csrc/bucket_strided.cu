@@ -426,7 +426,9 @@ __global__ void __launch_bounds__(NT) k3v2_kernel(const __grid_constant__ Plan P
   using T = typename Cx<R>::T;
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   constexpr int NJ = sizeof(R) == 4 ? 8 : 4;
-  constexpr int B0 = (INV && !HF) ? 1 : 0;   // first big member read per result
+  // INV 1: F (or big member 0 when nothing is folded) is the same for all of a
+  // thread's results; INV 2: F and big member 0 are (their product is hoisted)
+  constexpr int B0 = (INV == 2 || (INV == 1 && !HF)) ? 1 : 0;   // first big member read per result
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Tables* tab = reinterpret_cast<Tables*>(smem_raw);
   uint32_t* OL = reinterpret_cast<uint32_t*>(smem_raw + NB * sizeof(Tables));
@@ -554,7 +556,8 @@ __global__ void __launch_bounds__(NT) k3v2_kernel(const __grid_constant__ Plan P
           sp[b] = stb + o;
         }
         T iv = T{};
-        if (INV) iv = HF ? lds<T>(Fb + offF[0] + s * (uint32_t)sizeof(T)) : lds<T>(sp[0] + off[0][0]);
+        if (INV == 1) iv = HF ? lds<T>(Fb + offF[0] + s * (uint32_t)sizeof(T)) : lds<T>(sp[0] + off[0][0]);
+        if (INV == 2) iv = cmul(lds<T>(Fb + offF[0] + s * (uint32_t)sizeof(T)), lds<T>(sp[0] + off[0][0]));
         auto term = [&](int j) {
           T p = iv;
 #pragma unroll
@@ -562,7 +565,7 @@ __global__ void __launch_bounds__(NT) k3v2_kernel(const __grid_constant__ Plan P
             const T x = lds<T>(sp[b] + off[b][j]);
             p = (!INV && b == 0) ? x : cmul(p, x);
           }
-          if (HF && !INV) p = cmul(p, lds<T>(Fb + offF[j] + s * (uint32_t)sizeof(T)));
+          if (HF && INV == 0) p = cmul(p, lds<T>(Fb + offF[j] + s * (uint32_t)sizeof(T)));
           acc[j] = cadd(acc[j], p);   // acc starts at +0: s ascending, as the reference
         };
         if (nj == NJ) {
@@ -580,7 +583,7 @@ __global__ void __launch_bounds__(NT) k3v2_kernel(const __grid_constant__ Plan P
     }
     if (!MS && active) {
       T i0 = T{}, i1 = T{};
-      if (INV) {   // operand invariant across j: F, or big member 0
+      if (INV == 1) {   // operand invariant across j: F, or big member 0
         if (HF) {
           i0 = lds<T>(Fb + offF[0]);
           i1 = lds<T>(Fb + offF[0] + (uint32_t)sizeof(T));
@@ -588,6 +591,10 @@ __global__ void __launch_bounds__(NT) k3v2_kernel(const __grid_constant__ Plan P
           i0 = lds<T>(stb + off[0][0]);
           i1 = lds<T>(stb + off[0][0] + psb[0]);
         }
+      }
+      if (INV == 2) {   // F and big member 0 invariant: their product
+        i0 = cmul(lds<T>(Fb + offF[0]), lds<T>(stb + off[0][0]));
+        i1 = cmul(lds<T>(Fb + offF[0] + (uint32_t)sizeof(T)), lds<T>(stb + off[0][0] + psb[0]));
       }
       // per member: the s = 0 and s = 1 planes as two base addresses, so each
       // value is one shared load at [register offset + base]
@@ -604,7 +611,7 @@ __global__ void __launch_bounds__(NT) k3v2_kernel(const __grid_constant__ Plan P
           p0 = first ? x0 : cmul(p0, x0);
           p1 = first ? x1 : cmul(p1, x1);
         }
-        if (HF && !INV) {
+        if (HF && INV == 0) {
           p0 = cmul(p0, lds<T>(Fb + offF[j]));
           p1 = cmul(p1, lds<T>(Fb + offF[j] + (uint32_t)sizeof(T)));
         }
@@ -634,10 +641,15 @@ __global__ void __launch_bounds__(NT) k3v2_kernel(const __grid_constant__ Plan P
   }
 }
 
+template <typename R, int NB, int HF, int MS>
+const void* k3v2_fn_inv_ms(int inv) {
+  if (HF && inv == 2) return (const void*)k3v2_kernel<R, NB, HF, (HF ? 2 : 1), MS>;
+  return inv ? (const void*)k3v2_kernel<R, NB, HF, 1, MS> : (const void*)k3v2_kernel<R, NB, HF, 0, MS>;
+}
+
 template <typename R, int NB, int HF>
 const void* k3v2_fn_inv(int inv, int ms) {
-  if (ms) return inv ? (const void*)k3v2_kernel<R, NB, HF, 1, 1> : (const void*)k3v2_kernel<R, NB, HF, 0, 1>;
-  return inv ? (const void*)k3v2_kernel<R, NB, HF, 1, 0> : (const void*)k3v2_kernel<R, NB, HF, 0, 0>;
+  return ms ? k3v2_fn_inv_ms<R, NB, HF, 1>(inv) : k3v2_fn_inv_ms<R, NB, HF, 0>(inv);
 }
 
 template <typename R>
@@ -813,19 +825,38 @@ int make_plan(const qtn_bucket_desc_t* d, Plan* P, int* smem_bytes) {
   // every index it carries
   int inv_member = -1;
   bool has_inv = false;
-  uint64_t avoid = 0;   // iteration bits of the invariant operand
+  uint64_t avoid = 0;     // iteration bits of the invariant operands
+  uint64_t avoid_f = 0;   // ... of the folded table F alone
+  auto member_bits = [&](int i) {
+    uint64_t a = 0;
+    for (int b = 0; b < w; ++b)
+      if (d->mem[i].strides[b]) a |= 1ull << b;
+    return a;
+  };
+  int inv_cand = -1;   // staged member with the fewest indices (never the widest)
+  for (int i = 0; i < nm; ++i)
+    if (!folded[i] && i != imax && (inv_cand < 0 || rank[i] < rank[inv_cand])) inv_cand = i;
   if (P->v2 && nf > 0) {
     has_inv = true;
     for (int i = 0; i < nm; ++i)
-      if (folded[i])
-        for (int b = 0; b < w; ++b)
-          if (d->mem[i].strides[b]) avoid |= 1ull << b;
+      if (folded[i]) avoid_f |= member_bits(i);
+    avoid = avoid_f;
+    // level 2: F and one staged member invariant, when enough bits remain for j
+    static const bool inv2_off = getenv("QTN_K3_INV2") && atoi(getenv("QTN_K3_INV2")) == 0;
+    if (!inv2_off && nb >= 2 && inv_cand >= 0) {
+      const uint64_t a2 = avoid_f | member_bits(inv_cand);
+      int free_bits = 0;
+      for (int b = 0; b < w; ++b)
+        if (!inT[b] && !((a2 >> b) & 1)) ++free_bits;
+      if (free_bits >= nt_target - core) {   // only with full-size tiles
+        inv_member = inv_cand;
+        avoid = a2;
+      }
+    }
   } else if (P->v2 && nb >= 2) {
-    for (int i = 0; i < nm; ++i)
-      if (i != imax && (inv_member < 0 || rank[i] < rank[inv_member])) inv_member = i;
+    inv_member = inv_cand;
     has_inv = true;
-    for (int b = 0; b < w; ++b)
-      if (d->mem[inv_member].strides[b]) avoid |= 1ull << b;
+    avoid = member_bits(inv_member);
   }
   // j bits: the lowest bits the invariant operand lacks, reserved first; the
   // core is filled with the invariant operand's own bits first when it is a
@@ -842,25 +873,33 @@ int make_plan(const qtn_bucket_desc_t* d, Plan* P, int* smem_bytes) {
         if (jres[q] == b) return true;
       return false;
     };
-    const bool core_in_avoid_first = nf == 0;
-    for (int pass = 0; pass < 3 && nt < core; ++pass)
+    // core fill: bits of an invariant staged member first (free), then bits
+    // no invariant operand carries, F's bits last (they would grow the table)
+    const uint64_t avoid_big = avoid & ~avoid_f;
+    for (int pass = 0; pass < 4 && nt < core; ++pass)
       for (int b = 0; b < w && nt < core; ++b) {
         if (inT[b]) continue;
-        const bool in_av = (avoid >> b) & 1;
-        const bool ok = pass == 2 ? true
-                        : pass == 0 ? (in_av == core_in_avoid_first && !reserved(b))
+        const bool ok = pass == 3   ? true
+                        : pass == 0 ? (((avoid_big >> b) & 1) && !reserved(b))
+                        : pass == 1 ? (!((avoid >> b) & 1) && !reserved(b))
                                     : !reserved(b);
-        if (ok && !add(b, true)) pass = 3, b = w;
+        if (ok && !add(b, true)) pass = 4, b = w;
       }
     for (int q = 0; q < nj_res && nt < nt_goal; ++q)
       if (!inT[jres[q]] && !add(jres[q], true)) break;
     for (int b = 0; b < w && nt < nt_goal; ++b)
       if (!inT[b] && !add(b, true)) break;
   }
-  bool inv = has_inv;
-  for (int j = 8; j < nt; ++j)
-    if ((avoid >> T[j]) & 1) inv = false;
-  P->inv = inv ? 1 : 0;
+  bool inv_f = has_inv, inv_b = inv_member >= 0;
+  for (int j = 8; j < nt; ++j) {
+    if (((nf > 0 ? avoid_f : 0) >> T[j]) & 1) inv_f = false;
+    if (inv_member >= 0 && ((member_bits(inv_member) >> T[j]) & 1)) inv_b = false;
+  }
+  // INV 1: F (or, with no folded member, big member 0) invariant; 2: F and big member 0
+  if (nf > 0)
+    P->inv = inv_f ? (inv_b ? 2 : 1) : 0;
+  else
+    P->inv = inv_b ? 1 : 0;
 
   P->nt = nt;
   int N[MAXN], nn = 0;
@@ -873,8 +912,8 @@ int make_plan(const qtn_bucket_desc_t* d, Plan* P, int* smem_bytes) {
   for (int j = 0; j < nn; ++j) P->onstride[j] = (int64_t)1 << N[j];
 
   // ---- member roles ----
+  const bool inv_big = P->v2 && inv_member >= 0 && ((nf == 0 && P->inv == 1) || P->inv == 2);   // big member 0 invariant
   nb = nf = 0;
-  const bool inv_big = P->v2 && inv && inv_member >= 0;   // big member 0 is the invariant operand
   if (inv_big) P->big[nb++] = (int8_t)inv_member;
   for (int i = 0; i < nm; ++i) {
     if (folded[i])
