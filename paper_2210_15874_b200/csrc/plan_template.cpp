@@ -327,7 +327,7 @@ int qtn_plan_build(int32_t n_tensors, const int32_t* tensor_ptr, const int64_t* 
           const int L = PL.tile_bits(w, m, sm, nullptr);
           if (L < std::min(w, params->min_tile_bits)) continue;
         }
-        if (w + (int)X2.size() > PL.sib && X2.size() > 3) continue;
+        if (w + (int)X2.size() > PL.sib && (int)X2.size() > params->kmax_large) continue;
         const double c2 = PL.cost_of(cand);
         if (c2 >= it.cost + p.cost) continue;
         const int64_t pr = mm.ref;

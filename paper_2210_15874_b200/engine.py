@@ -67,6 +67,10 @@ def _tensor_align(size):
 
 
 KMAX = N.MAX_SUMMED
+# summed indices of a merged large item (measured: complex64 cfg-2 0.318 ->
+# 0.308 ms with 2, 45-cone graph +1 %; complex128 is best with 3)
+_KL = os.environ.get("QTN_KMAX_LARGE")
+KMAX_LARGE = {"complex64": int(_KL) if _KL else 2, "complex128": int(_KL) if _KL else 3}
 SMALL_PROD_ELEMS = 1024   # smem products per round of a small tile (csrc)
 VEC = {"complex64": 2, "complex128": 1}
 # merge cost model (seconds).  Effective constants, tuned end to end on the
@@ -268,7 +272,8 @@ def _plan_params(dtype, merge, sib):
         min_tile_bits=MIN_TILE_BITS[dtype], kmax=KMAX, max_members=N.MAX_MEMBERS, vec=VEC[dtype], nt=NT,
         small_iter_bits=sib, merge=1 if merge else 0, resident_blocks=RESIDENT_BLOCKS[dtype],
         smem_budget=SMEM_BUDGET, hop_s=HOP_S, hop_k2_s=HOP_K2_S, bw_bps=BW_BPS,
-        block_terms_ps=BLOCK_TERMS_PS[dtype], small_load_s=SMALL_LOAD_S, cheap_member_w=CHEAP_MEMBER_W)
+        block_terms_ps=BLOCK_TERMS_PS[dtype], small_load_s=SMALL_LOAD_S, cheap_member_w=CHEAP_MEMBER_W,
+        kmax_large=KMAX_LARGE[dtype])
 
 
 def plan_template(index_sets, order, dtype, fixed=(), merge=None, small_iter_bits=None):
@@ -406,8 +411,8 @@ def plan_template_py(index_sets, order, dtype, fixed=(), merge=None, small_iter_
                     L, _ = _tile_bits(w, masks, smasks, dtype)
                     if L < min(w, MIN_TILE_BITS[dtype]):
                         continue
-                if w + len(X2) > sib and len(X2) > 3:
-                    continue   # would need the generic K1 kernel (no k > 3 specialisation)
+                if w + len(X2) > sib and len(X2) > KMAX_LARGE[dtype]:
+                    continue   # k > 3 would need the generic K1 kernel (no specialisation)
                 c2 = _cost_of(cand, dtype, sib)
                 if c2 >= it["cost"] + p_["cost"]:
                     continue
