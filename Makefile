@@ -1,28 +1,41 @@
 # Build the sm_100a engine library in-tree (travels to the GPU box with the repo).
+# Translation units compile in parallel (make -j); the library links them.
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -cudart static -Iinclude
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude
 LIB := paper_2210_15874_b200/lib/libqtn_b200.so
-SRC := paper_2210_15874_b200/csrc/qtn_b200.cu paper_2210_15874_b200/csrc/bucket_strided.cu paper_2210_15874_b200/csrc/planner.cpp paper_2210_15874_b200/csrc/plan_template.cpp
+CSRC := paper_2210_15874_b200/csrc
+SRC := $(CSRC)/qtn_b200.cu $(CSRC)/bucket_strided.cu $(CSRC)/planner.cpp $(CSRC)/plan_template.cpp
+OBJDIR := build/obj
+OBJ := $(patsubst $(CSRC)/%,$(OBJDIR)/%.o,$(SRC))
+DBGOBJ := $(patsubst $(CSRC)/%,$(OBJDIR)/debug/%.o,$(SRC))
 
 all: $(LIB)
 
-$(LIB): $(SRC) include/qtn_b200.h
+$(OBJDIR)/%.o: $(CSRC)/% include/qtn_b200.h
 	@mkdir -p $(dir $@)
-	$(NVCC) $(NVFLAGS) -o $@ $(SRC)
+	$(NVCC) $(NVFLAGS) $(EXTRA) -c -o $@ $<
+
+$(OBJDIR)/debug/%.o: $(CSRC)/% include/qtn_b200.h
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -DQTN_DEBUG -c -o $@ $<
+
+$(LIB): $(OBJ)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJ)
 
 # variant build for A/B measurements: make variant TAG=x EXTRA="-DFOO" -> lib/libqtn_b200_x.so
 variant:
-	$(NVCC) $(NVFLAGS) $(EXTRA) -o paper_2210_15874_b200/lib/libqtn_b200_$(TAG).so $(SRC)
+	$(NVCC) $(NVFLAGS) $(EXTRA) -shared -cudart static -o paper_2210_15874_b200/lib/libqtn_b200_$(TAG).so $(SRC)
 
 # bounds-checked build (device asserts), for GPU debugging without compute-sanitizer
-debug:
-	$(NVCC) $(NVFLAGS) -DQTN_DEBUG -o paper_2210_15874_b200/lib/libqtn_b200_debug.so $(SRC)
+debug: $(DBGOBJ)
+	$(NVCC) $(ARCH) -shared -cudart static -o paper_2210_15874_b200/lib/libqtn_b200_debug.so $(DBGOBJ)
 
 sass: $(LIB)
 	cuobjdump -sass $(LIB) | grep -E "Function|LDG|STG|ATOM|RED" | head -50
 
 clean:
-	rm -f $(LIB)
+	rm -rf $(LIB) build
 
-.PHONY: all clean sass
+.PHONY: all clean sass variant debug
