@@ -44,8 +44,16 @@ class UnitPlan:
     widths: list = field(default_factory=list)
 
 
-def plan_units(cones, backend: Backend, heuristic="minfill", mem_cap=4 << 30, slice_target=None, n_workers=1):
-    """Order every cone, slice the wide ones, build templates and units."""
+def plan_units(cones, backend: Backend, heuristic="minfill", mem_cap=4 << 30, slice_target=None, n_workers=1,
+               balance_ranks=None, balance_factor=2.0):
+    """Order every cone, slice the wide ones, build templates and units.
+
+    balance_ranks: additionally slice the heaviest cones (one more index at a
+    time, suggest_slicing with a narrower target) until no unit costs more
+    than total / (balance_ranks * balance_factor) — so LPT can spread an
+    over-wide lightcone's index slices across that many GPUs.  The plan
+    depends only on balance_ranks, not on the actual world size, so energies
+    stay bitwise identical for any number of ranks."""
     from .ordering import MemoryCapError, greedy_order, suggest_slicing
 
     def one(lc):
@@ -68,6 +76,8 @@ def plan_units(cones, backend: Backend, heuristic="minfill", mem_cap=4 << 30, sl
             res = list(pool.map(one, cones))
     else:
         res = [one(lc) for lc in cones]
+    if balance_ranks and balance_ranks > 1:
+        res = _balance(cones, res, backend, heuristic, mem_cap, balance_ranks, balance_factor)
     units = []
     templates, raws = [], []
     for ci, (tmpl, sliced, raw) in enumerate(res):
@@ -77,6 +87,39 @@ def plan_units(cones, backend: Backend, heuristic="minfill", mem_cap=4 << 30, sl
         for bits in np.ndindex(*(2,) * len(sliced)):
             units.append(Unit(ci, dict(zip(sliced, (int(b) for b in bits))), cost))
     return UnitPlan(list(cones), templates, raws, units)
+
+
+def _balance(cones, res, backend, heuristic, mem_cap, n_ranks, factor, max_rounds=64, max_extra_bits=6):
+    """Slice the most expensive cone one index further until every unit is at
+    most total / (n_ranks * factor) (algorithmic bytes per slice)."""
+    from .ordering import greedy_order, suggest_slicing
+    res = list(res)
+    orders = {}
+    base = [len(s_) for _, s_, _ in res]
+    stuck = set()
+    sib = E.small_iter_bits_for(backend.threshold)
+    for _ in range(max_rounds):
+        per = [E.algorithmic_bytes(t, backend.dtype) for t, _, _ in res]
+        total = sum(c << len(s_) for c, (_, s_, _) in zip(per, res))
+        target = total / (n_ranks * factor)
+        cand = [i for i in range(len(res)) if i not in stuck and per[i] > target]
+        if not cand:
+            break
+        ci = max(cand, key=lambda i: (per[i], -i))
+        tmpl, sliced, raw = res[ci]
+        if len(sliced) - base[ci] >= max_extra_bits or tmpl.max_width <= 1:
+            stuck.add(ci)
+            continue
+        tn = cones[ci].network
+        order = orders.get(ci) or greedy_order(tn, heuristic)
+        orders[ci] = order
+        new = suggest_slicing(tn, order, tmpl.max_width - 1)
+        if len(new) <= len(sliced) or not set(sliced) <= set(new):
+            stuck.add(ci)
+            continue
+        t2 = E.plan_template([t.indices for t in tn.tensors], order, backend.dtype, fixed=new, small_iter_bits=sib)
+        res[ci] = (t2, new, raw)
+    return res
 
 
 def lpt_assign(costs, n_ranks):

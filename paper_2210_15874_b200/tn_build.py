@@ -363,6 +363,7 @@ def qaoa_energy_detailed(
     n_gpus: int | None = None,
     group=None,
     simplify: bool = False,
+    balance_ranks: int | None = None,
 ):
     """Per-edge <Z_u Z_v> and bucket stats, one lightcone per edge
     (src/tn_build.py:166-186).
@@ -372,7 +373,8 @@ def qaoa_energy_detailed(
     suggest_slicing.  (cone, slice) units run as batched device programs;
     under torch.distributed (or `group`) they are sharded over ranks by LPT
     on algorithmic bytes and the unit values are combined with one
-    all-reduce.  Accumulation is in sorted-edge then slice order, so the
+    all-reduce.  balance_ranks=R slices the heaviest cones further so that
+    R ranks can share them (the plan depends on R, not on the world size).  Accumulation is in sorted-edge then slice order, so the
     result is bitwise identical for any worker / GPU count."""
     import dataclasses
     from . import distributed as D
@@ -384,11 +386,11 @@ def qaoa_energy_detailed(
     # are re-staged
     struct = tuple(tuple(t.indices for t in lc.network.tensors) for lc in cones)
     key = (struct, heuristic, mem_cap, slice_target, backend.dtype, backend.threshold, backend.profile,
-           n_gpus, id(group) if group is not None else None)
+           n_gpus, id(group) if group is not None else None, balance_ranks)
     hit = _ENERGY_PLANS.get(key)
     if hit is None:
         plan = D.plan_units(cones, backend, heuristic=heuristic, mem_cap=mem_cap,
-                            slice_target=slice_target, n_workers=n_workers)
+                            slice_target=slice_target, n_workers=n_workers, balance_ranks=balance_ranks)
         hit = _ENERGY_PLANS[key] = (plan, {})
         while len(_ENERGY_PLANS) > 2:
             _ENERGY_PLANS.pop(next(iter(_ENERGY_PLANS)))

@@ -36,7 +36,7 @@ def _emulated_run_local(plan, mine, backend, device, budget_bytes=None, cache=No
     return vals, stats
 
 
-def _energy(world, rank, port, out, slice_target):
+def _energy(world, rank, port, out, slice_target, balance=None):
     import paper_2210_15874_b200 as Q
     from paper_2210_15874_b200 import distributed as D
     if world > 1:
@@ -50,7 +50,7 @@ def _energy(world, rank, port, out, slice_target):
     be = Q.Backend.b200(dtype="complex128")
     c = Q.qaoa_maxcut_circuit(graph, params)
     cones = [Q.extract_lightcone(c, e) for e in graph.edges]
-    plan = D.plan_units(cones, be, slice_target=slice_target)
+    plan = D.plan_units(cones, be, slice_target=slice_target, balance_ranks=balance)
     vals, _ = D.run_units(plan, be)
     e = sum(0.5 * (1.0 - v.real) for v in vals)
     owner = D.lpt_assign([u.cost for u in plan.units], max(world, 1))
@@ -59,19 +59,21 @@ def _energy(world, rank, port, out, slice_target):
         dist.destroy_process_group()
 
 
-def _worker(rank, world, port, out, slice_target):
-    _energy(world, rank, port, out, slice_target)
+def _worker(rank, world, port, out, slice_target, balance):
+    _energy(world, rank, port, out, slice_target, balance)
 
 
-@pytest.mark.parametrize("slice_target", [None, 2])
-def test_gloo_world2_matches_single_rank(slice_target):
+@pytest.mark.parametrize("slice_target,balance", [(None, None), (2, None), (None, 16)])
+def test_gloo_world2_matches_single_rank(slice_target, balance):
+    """Energies are bitwise identical for 1 and 2 ranks, also with slicing
+    and with balance slicing (the plan depends on balance_ranks only)."""
     single = {}
-    _energy(1, 0, 0, single, slice_target)
+    _energy(1, 0, 0, single, slice_target, balance)
     e1, n_units, _ = single[0]
     mgr = mp.Manager()
     out = mgr.dict()
     port = _free_port()
-    mp.spawn(_worker, args=(2, port, out, slice_target), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, port, out, slice_target, balance), nprocs=2, join=True)
     g = load_json("qaoa.json")["cfg1"]
     for r in (0, 1):
         e, n, owner = out[r]
@@ -79,7 +81,7 @@ def test_gloo_world2_matches_single_rank(slice_target):
         assert e == e1                         # bitwise: one contributor per slot
         assert set(owner) == {0, 1}            # both ranks got work
     assert abs(e1 - g["energy"]) < 1e-10
-    if slice_target is not None:
+    if slice_target is not None or balance is not None:
         assert n_units > len(g["cones"])       # some cones were sliced
 
 
@@ -92,3 +94,25 @@ def test_lpt_assignment_balanced_and_deterministic():
         assert own == D.lpt_assign(costs, n)
         loads = [sum(c for c, o in zip(costs, own) if o == r) for r in range(n)]
         assert max(loads) - min(loads) <= max(costs)
+
+
+def test_balance_slicing_spreads_the_heaviest_cone():
+    """plan_units(balance_ranks=8) on N=30 p=4 tight cones: no unit above
+    total / 16 (the widest cone holds ~30 % of the work unsliced), LPT
+    makespan at 8 ranks within 15 % of ideal, total work inflated < 3 %."""
+    import paper_2210_15874_b200 as Q
+    from paper_2210_15874_b200 import distributed as D
+    g = Q.random_regular_graph(30, 3, seed=0)
+    c = Q.qaoa_maxcut_circuit(g, Q.QaoaParams.seeded(4, 0))
+    cones = [Q.extract_lightcone(c, e, cone="tight") for e in g.edges]
+    be = Q.Backend.b200(dtype="complex64")
+    p0 = D.plan_units(cones, be, mem_cap=1 << 40)
+    p8 = D.plan_units(cones, be, mem_cap=1 << 40, balance_ranks=8)
+    c0 = [u.cost for u in p0.units]
+    c8 = [u.cost for u in p8.units]
+    assert max(c0) > 0.25 * sum(c0)
+    assert max(c8) <= sum(c8) / 16
+    assert sum(c8) < 1.03 * sum(c0)
+    own = D.lpt_assign(c8, 8)
+    load = [sum(c for c, o in zip(c8, own) if o == r) for r in range(8)]
+    assert max(load) <= 1.15 * sum(c8) / 8
