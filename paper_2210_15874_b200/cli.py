@@ -48,7 +48,8 @@ def _backend_from_args(args) -> Backend:
 
 def _add_backend_flags(p):
     p.add_argument("--backend", choices=["b200", "reference", "fast", "mixed"], default="b200")
-    p.add_argument("--threshold", type=int, default=11, help="K2/K1 routing width (result rank)")
+    p.add_argument("--threshold", type=int, default=None,
+                   help="K2/K1 routing width (result rank); default: the measured per-dtype value")
     p.add_argument("--heuristic", choices=["minfill", "mindegree"], default="minfill")
     p.add_argument("--mem-cap", type=int, default=DEFAULT_MEM_CAP, help="contraction memory cap in bytes")
     p.add_argument("--dtype", choices=["complex64", "complex128"], default="complex128")

@@ -60,7 +60,7 @@ def plan_units(cones, backend: Backend, heuristic="minfill", mem_cap=4 << 30, sl
         tn = lc.network
         order = greedy_order(tn, heuristic)
         ix = [t.indices for t in tn.tensors]
-        sib = E.small_iter_bits_for(backend.threshold)
+        sib = E.small_iter_bits_for(backend.threshold, backend.dtype)
         tmpl = E.plan_template(ix, order, backend.dtype, small_iter_bits=sib)
         sliced = []
         if slice_target is not None and tmpl.max_width > slice_target:   # width = the dry run's
@@ -97,7 +97,7 @@ def _balance(cones, res, backend, heuristic, mem_cap, n_ranks, factor, max_round
     orders = {}
     base = [len(s_) for _, s_, _ in res]
     stuck = set()
-    sib = E.small_iter_bits_for(backend.threshold)
+    sib = E.small_iter_bits_for(backend.threshold, backend.dtype)
     for _ in range(max_rounds):
         per = [E.algorithmic_bytes(t, backend.dtype) for t, _, _ in res]
         total = sum(c << len(s_) for c, (_, s_, _) in zip(per, res))

@@ -90,7 +90,10 @@ BLOCK_TERMS_PS = {"complex64": 5.0e9 * _TERMS_SCALE, "complex128": 2.4e9 * _TERM
 RESIDENT_BLOCKS = {"complex64": 296, "complex128": 296}
 SMALL_LOAD_S = 0.65e-6
 MIN_TILE_BITS = {"complex64": 9, "complex128": 8}   # vector path needs VEC*NT results
-SMALL_ITER_BITS = int(os.environ.get("QTN_SMALL_ITER", "12"))  # items with w + k <= this run in K2
+# items with w + k <= this run in K2 (default per dtype, measured on cfg-2:
+# complex64 flat over 12..16, complex128 best at 16: 0.473 -> 0.452 ms)
+_SIB = os.environ.get("QTN_SMALL_ITER")
+SMALL_ITER_BITS = {"complex64": int(_SIB) if _SIB else 12, "complex128": int(_SIB) if _SIB else 16}
 SMALL_TILE_BITS = {"complex64": 8, "complex128": 7}  # K2 tiles: below one vector step
 # QTN_MERGE=0 disables chain merging (A/B measurements)
 MERGE_DEFAULT = os.environ.get("QTN_MERGE", "1") != "0"
@@ -241,7 +244,7 @@ def _item_cost(w, k, L, sizes, dtype, hop=None, nm_eff=None):
 
 
 def _cost_of(it, dtype, small_iter_bits=None):
-    sib = SMALL_ITER_BITS if small_iter_bits is None else small_iter_bits
+    sib = SMALL_ITER_BITS[dtype] if small_iter_bits is None else small_iter_bits
     masks, smasks = _masks(it["members"], it["X"], it["R"])
     w, k = len(it["R"]), len(it["X"])
     if w + k <= sib:
@@ -258,11 +261,13 @@ def _cost_of(it, dtype, small_iter_bits=None):
                       nm_eff=nm_eff)
 
 
-def small_iter_bits_for(threshold):
+def small_iter_bits_for(threshold, dtype="complex64"):
     """Backend.threshold (result width at or below which a bucket runs in the
     batched small-bucket schedule, the analogue of the reference's Mixed
     threshold, src/tensor_core.py:176-184) -> iteration bits (w + k) of the
-    K2 routing rule."""
+    K2 routing rule; None -> the measured per-dtype default."""
+    if threshold is None:
+        return SMALL_ITER_BITS[norm_dtype(dtype)]
     return int(threshold) + 1
 
 
@@ -283,7 +288,7 @@ def plan_template(index_sets, order, dtype, fixed=(), merge=None, small_iter_bit
     stays as its checker (tests compare the two array by array)."""
     dtype = norm_dtype(dtype)
     merge = MERGE_DEFAULT if merge is None else merge
-    sib = SMALL_ITER_BITS if small_iter_bits is None else int(small_iter_bits)
+    sib = SMALL_ITER_BITS[dtype] if small_iter_bits is None else int(small_iter_bits)
     fixed = list(dict.fromkeys(int(f) for f in fixed))
     sc, a = N.plan_build([tuple(int(i) for i in s) for s in index_sets], order, fixed, _plan_params(dtype, merge, sib))
     ncanon = len(a["gdst"])
@@ -312,7 +317,7 @@ def plan_template_py(index_sets, order, dtype, fixed=(), merge=None, small_iter_
     small_iter_bits: items with w + k <= this run in a K2 small stage
     (default SMALL_ITER_BITS = Backend threshold 11 + 1)."""
     dtype = norm_dtype(dtype)
-    sib = SMALL_ITER_BITS if small_iter_bits is None else int(small_iter_bits)
+    sib = SMALL_ITER_BITS[dtype] if small_iter_bits is None else int(small_iter_bits)
     merge = MERGE_DEFAULT if merge is None else merge
     fixed = set(int(f) for f in fixed)
     act = [int(i) for i in order if int(i) not in fixed]

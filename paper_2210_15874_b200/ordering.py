@@ -290,7 +290,7 @@ def _template(tn, order, backend, fixed=()):
     hit = PLAN_CACHE.get(key)
     if hit is None:
         hit = E.plan_template(list(struct), order, backend.dtype, fixed,
-                              small_iter_bits=E.small_iter_bits_for(backend.threshold))
+                              small_iter_bits=E.small_iter_bits_for(backend.threshold, backend.dtype))
         PLAN_CACHE.put(key, hit)
     plans[okey] = (key, hit)
     return key, hit

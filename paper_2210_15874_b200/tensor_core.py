@@ -41,7 +41,7 @@ class Backend:
     """
 
     kind: str = B200
-    threshold: int = DEFAULT_MIXED_THRESHOLD
+    threshold: int | None = None
     dtype: str = "complex128"
     device: int = 0
     profile: bool = True
@@ -49,12 +49,12 @@ class Backend:
     def __post_init__(self):
         if self.kind not in KINDS:
             raise ValueError(f"unknown backend kind: {self.kind!r}")
-        if self.threshold < 0:
+        if self.threshold is not None and self.threshold < 0:
             raise ValueError("mixed threshold must be >= 0")
         object.__setattr__(self, "dtype", E.norm_dtype(self.dtype))
 
     @classmethod
-    def b200(cls, dtype="complex128", threshold=DEFAULT_MIXED_THRESHOLD, device=0, profile=True):
+    def b200(cls, dtype="complex128", threshold=None, device=0, profile=True):
         return cls(B200, threshold, dtype, device, profile)
 
     # drop-in aliases for code written against the reference's constructors
@@ -71,7 +71,8 @@ class Backend:
         return cls(B200, threshold)
 
     def route(self, width: int) -> str:
-        return "b200-large" if width > self.threshold else "b200-small"
+        thr = DEFAULT_MIXED_THRESHOLD if self.threshold is None else self.threshold
+        return "b200-large" if width > thr else "b200-small"
 
     @property
     def elem_bytes(self) -> int:

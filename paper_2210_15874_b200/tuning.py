@@ -54,7 +54,7 @@ def _item_times(tn, order, backend, threshold, dtype):
     """(per reference bucket widths, per reference bucket ns, per bucket 'ran in K2')."""
     import torch
     tmpl = E.plan_template([t.indices for t in tn.tensors], order, dtype, merge=False,
-                           small_iter_bits=E.small_iter_bits_for(threshold))
+                           small_iter_bits=E.small_iter_bits_for(threshold, dtype))
     prog = E.Program([E.Instance(tmpl)], dtype)
     ex = E.Executor(prog, device=backend.device, timing=True)
     raw = np.concatenate([np.asarray(t.data, np.complex128).ravel() for t in tn.tensors])
@@ -160,7 +160,7 @@ def sweep_thresholds(cones, orders, thresholds, backend: Backend = None, reps: i
         for lc, order in zip(cones, orders):
             tn = lc.network
             tmpl = E.plan_template([t.indices for t in tn.tensors], order, backend.dtype,
-                                   small_iter_bits=E.small_iter_bits_for(thr))
+                                   small_iter_bits=E.small_iter_bits_for(thr, backend.dtype))
             ex = E.Executor(E.Program([E.Instance(tmpl)], backend.dtype), device=backend.device, timing=False)
             ex.stage_inputs([np.concatenate([np.asarray(t.data, np.complex128).ravel() for t in tn.tensors])])
             s = torch.cuda.current_stream(backend.device)
