@@ -817,8 +817,13 @@ __device__ __forceinline__ void large_body(const qtn_program_t& P, int32_t item)
 // One kernel per element type so each gets its own register budget: complex64
 // runs best with the compiler's default allocation, complex128 with a cap
 // that keeps 3 blocks resident (measured on cfg-2: 0.671 -> 0.605 ms).
+#ifdef K1_C64_MINB
+#define K1_C64_BOUNDS __launch_bounds__(NT, K1_C64_MINB)
+#else
+#define K1_C64_BOUNDS __launch_bounds__(NT)
+#endif
 template <int NS, int NV, int ST, int NB0>
-__global__ void __launch_bounds__(NT) large_kernel_c64(const qtn_program_t P, int32_t item) {
+__global__ void K1_C64_BOUNDS large_kernel_c64(const qtn_program_t P, int32_t item) {
   large_body<float, NS, NV, ST, NB0>(P, item);
 }
 template <int NS, int NV, int ST, int NB0>

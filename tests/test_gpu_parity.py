@@ -200,3 +200,40 @@ def test_energy_sweep_reuses_plans():
         vals.append(e)
     assert len(set(vals)) == 3
     assert any(len(cache) > 0 for _, cache in T._ENERGY_PLANS.values())
+
+
+_K3_ROUTE_CHECK = r"""
+import sys
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import numpy as np
+from conftest import load_json
+import paper_2210_15874_b200 as Q
+errs = []
+for rec in load_json("networks.json"):
+    c = Q.Circuit(rec["n"], [Q.Gate(a, tuple(b), x) for a, b, x in rec["gates"]])
+    tn = Q.amplitude_network(c, rec["bits"])
+    for dt, tol in (("complex64", 1e-5), ("complex128", 1e-10)):
+        v, _ = Q.contract_network(tn, rec["order_minfill"], Q.Backend.b200(dtype=dt))
+        errs.append(abs(v - complex(*rec["value"])) / tol)
+g = Q.random_regular_graph(30, 3, seed=0)
+lc = Q.extract_lightcone(Q.qaoa_maxcut_circuit(g, Q.QaoaParams.seeded(4, 0)), (0, 15), cone="tight")
+for dt, tol in (("complex64", 1e-5), ("complex128", 1e-10)):
+    v, _ = Q.contract_network(lc.network, Q.greedy_order(lc.network), Q.Backend.b200(dtype=dt))
+    errs.append(abs(v.real - (-0.0017371891851279)) / tol)
+print(max(errs))
+"""
+
+
+@pytest.mark.parametrize("route", ["1", "2"])
+def test_program_items_through_k3(route):
+    """Program graphs with large items routed to K3 (QTN_K3_ROUTE, read once
+    per process): golden networks and the cfg-2 cone at both dtypes."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = _K3_ROUTE_CHECK.format(root=root, tests=os.path.join(root, "tests"))
+    env = dict(os.environ, QTN_K3_ROUTE=route)
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert float(out.stdout.strip().splitlines()[-1]) <= 1.0
