@@ -170,6 +170,19 @@ int qtn_node_launch(const qtn_program_t* prog, const qtn_node_t* node, int32_t n
  * indices of the nodes it waits for) on the current device. */
 int qtn_graph_create(const qtn_program_t* prog, const qtn_node_t* nodes, int32_t n_nodes,
                      const int32_t* node_deps, qtn_graph_t** out);
+/* Same, with the program's input upload (pinned host -> arena) as the graph's
+ * first node and the result download (result slots -> pinned host) as its
+ * last: one graph launch per contraction, end to end. */
+typedef struct {
+  const void* h2d_src;   /* pinned host input image                       */
+  void* h2d_dst;         /* device arena (input region)                   */
+  int64_t h2d_bytes;     /* 0 = no upload node                            */
+  const void* d2h_src;   /* device result slots                           */
+  void* d2h_dst;         /* pinned host result buffer                     */
+  int64_t d2h_bytes;     /* 0 = no download node                          */
+} qtn_graph_io_t;
+int qtn_graph_create_io(const qtn_program_t* prog, const qtn_node_t* nodes, int32_t n_nodes,
+                        const int32_t* node_deps, const qtn_graph_io_t* io, qtn_graph_t** out);
 /* Launch the instantiated graph (one call per program execution). */
 int qtn_graph_launch(qtn_graph_t* g, void* stream);
 int qtn_graph_destroy(qtn_graph_t* g);

@@ -39,6 +39,7 @@ EXPORTS = (
     "qtn_program_reset",
     "qtn_node_launch",
     "qtn_graph_create",
+    "qtn_graph_create_io",
     "qtn_graph_launch",
     "qtn_graph_destroy",
     "qtn_permute",
@@ -98,6 +99,12 @@ class BucketDescC(ctypes.Structure):
                 ("reserved", ctypes.c_int32), ("out", ctypes.c_void_p), ("mem", BMemberC * MAX_MEMBERS)]
 
 
+class GraphIOC(ctypes.Structure):
+    """qtn_graph_io_t: input upload / result download nodes of a program graph."""
+    _fields_ = [("h2d_src", ctypes.c_void_p), ("h2d_dst", ctypes.c_void_p), ("h2d_bytes", ctypes.c_int64),
+                ("d2h_src", ctypes.c_void_p), ("d2h_dst", ctypes.c_void_p), ("d2h_bytes", ctypes.c_int64)]
+
+
 class PlanParamsC(ctypes.Structure):
     """qtn_plan_params_t: the engine's cost-model constants."""
     _fields_ = [("elem_bytes", ctypes.c_int32), ("tile_bits", ctypes.c_int32), ("small_tile_bits", ctypes.c_int32),
@@ -133,6 +140,9 @@ def load(path: str = LIB_PATH):
     lib.qtn_node_launch.argtypes = [ctypes.POINTER(ProgramC), vp, i32, vp]
     lib.qtn_graph_create.restype = ctypes.c_int
     lib.qtn_graph_create.argtypes = [ctypes.POINTER(ProgramC), vp, i32, vp, ctypes.POINTER(ctypes.c_void_p)]
+    lib.qtn_graph_create_io.restype = ctypes.c_int
+    lib.qtn_graph_create_io.argtypes = [ctypes.POINTER(ProgramC), vp, i32, vp, ctypes.POINTER(GraphIOC),
+                                        ctypes.POINTER(ctypes.c_void_p)]
     lib.qtn_graph_launch.restype = ctypes.c_int
     lib.qtn_graph_launch.argtypes = [ctypes.c_void_p, vp]
     lib.qtn_graph_destroy.restype = ctypes.c_int

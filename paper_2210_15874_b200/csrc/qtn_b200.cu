@@ -1093,6 +1093,11 @@ int qtn_node_launch(const qtn_program_t* p, const qtn_node_t* nd, int32_t ni, vo
 
 int qtn_graph_create(const qtn_program_t* p, const qtn_node_t* nodes, int32_t n_nodes, const int32_t* node_deps,
                      qtn_graph_t** out) {
+  return qtn_graph_create_io(p, nodes, n_nodes, node_deps, nullptr, out);
+}
+
+int qtn_graph_create_io(const qtn_program_t* p, const qtn_node_t* nodes, int32_t n_nodes, const int32_t* node_deps,
+                        const qtn_graph_io_t* io, qtn_graph_t** out) {
   int rc = check_program(p);
   if (rc) return rc;
   if (!out || (n_nodes > 0 && !nodes)) return set_err(QTN_E_INVALID, "null argument");
@@ -1117,6 +1122,16 @@ int qtn_graph_create(const qtn_program_t* p, const qtn_node_t* nodes, int32_t n_
   }
   std::vector<cudaGraphNode_t> gn(n_nodes);
   std::vector<LaunchSpec> specs(n_nodes);
+  // optional input upload: every kernel node without a predecessor waits for it
+  cudaGraphNode_t h2d = nullptr;
+  if (io && io->h2d_bytes > 0) {
+    e = cudaGraphAddMemcpyNode1D(&h2d, g->graph, nullptr, 0, io->h2d_dst, io->h2d_src, (size_t)io->h2d_bytes,
+                                 cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      qtn_graph_destroy(g);
+      return cuda_err(e, "cudaGraphAddMemcpyNode1D(h2d)");
+    }
+  }
   const char* pdl_env = getenv("QTN_PDL");
   const bool use_pdl = !(pdl_env && pdl_env[0] == '0');
   for (int i = 0; i < n_nodes; ++i) {
@@ -1159,7 +1174,8 @@ int qtn_graph_create(const qtn_program_t* p, const qtn_node_t* nodes, int32_t n_
     kp.blockDim = dim3(NT);
     kp.sharedMemBytes = specs[i].smem;
     kp.kernelParams = specs[i].args;
-    e = cudaGraphAddKernelNode(&gn[i], g->graph, nullptr, 0, &kp);
+    e = cudaGraphAddKernelNode(&gn[i], g->graph, (h2d && nd.n_dep == 0) ? &h2d : nullptr,
+                               (h2d && nd.n_dep == 0) ? 1 : 0, &kp);
     if (e != cudaSuccess) {
       qtn_graph_destroy(g);
       return cuda_err(e, "cudaGraphAddKernelNode");
@@ -1175,6 +1191,16 @@ int qtn_graph_create(const qtn_program_t* p, const qtn_node_t* nodes, int32_t n_
         qtn_graph_destroy(g);
         return cuda_err(e, "cudaGraphAddDependencies_v2");
       }
+    }
+  }
+  // optional result download after every kernel node
+  if (io && io->d2h_bytes > 0) {
+    cudaGraphNode_t d2h = nullptr;
+    e = cudaGraphAddMemcpyNode1D(&d2h, g->graph, gn.data(), (size_t)n_nodes, io->d2h_dst, io->d2h_src,
+                                 (size_t)io->d2h_bytes, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+      qtn_graph_destroy(g);
+      return cuda_err(e, "cudaGraphAddMemcpyNode1D(d2h)");
     }
   }
   e = cudaGraphInstantiate(&g->exec, g->graph, 0);

@@ -883,12 +883,13 @@ class Executor:
             self.graph = g
 
     def __del__(self):
-        g = getattr(self, "graph", None)
-        if g is not None and g.value:
-            try:
-                N.load().qtn_graph_destroy(g)
-            except Exception:
-                pass
+        for name in ("graph", "graph_io"):
+            g = getattr(self, name, None)
+            if g is not None and g.value:
+                try:
+                    N.load().qtn_graph_destroy(g)
+                except Exception:
+                    pass
 
     # -- input image -------------------------------------------------------
     def stage_inputs(self, raw_parts):
@@ -930,7 +931,43 @@ class Executor:
         t = self.timing.cpu().numpy()
         return t[0::2], t[1::2]
 
+    def _io_graph(self):
+        """The program graph with the input upload as its first node and the
+        result download as its last (built on first use): run() is then one
+        graph launch and one stream synchronisation."""
+        g = getattr(self, "graph_io", None)
+        if g is None:
+            torch = self.torch
+            lib = N.load()
+            esz = self.arena.element_size()
+            io = N.GraphIOC(h2d_src=self.img_pinned.data_ptr(), h2d_dst=self.arena.data_ptr(),
+                            h2d_bytes=int(self.prog.n_input_elems) * esz,
+                            d2h_src=self.results.data_ptr(), d2h_dst=self.results_host.data_ptr(),
+                            d2h_bytes=self.results.numel() * self.results.element_size())
+            g = ctypes.c_void_p()
+            nodes = np.ascontiguousarray(self.prog.nodes)
+            deps = np.ascontiguousarray(self.prog.node_deps)
+            with torch.cuda.device(self.device):
+                N.check(lib.qtn_graph_create_io(ctypes.byref(self.c), nodes.ctypes.data_as(ctypes.c_void_p),
+                                                self.prog.n_nodes, deps.ctypes.data_as(ctypes.c_void_p),
+                                                ctypes.byref(io), ctypes.byref(g)))
+            self.graph_io = g
+        return g
+
     def run(self, raw_parts, stream=None):
-        self.stage_inputs(raw_parts)
-        self.launch(stream)
-        return self.fetch_results(stream)
+        """Stage the inputs on the host, then one graph launch (upload,
+        kernels, download) and one synchronisation."""
+        torch = self.torch
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        view = self.img_pinned.numpy()
+        parts = self.prog.img_src_parts
+        if len(parts) == 1:
+            view[self.prog.img_dst] = raw_parts[0][parts[0]]
+        elif parts:
+            view[self.prog.img_dst] = np.concatenate([raw[p_] for raw, p_ in zip(raw_parts, parts)])
+        if self.timing is not None:
+            self.timing.copy_(self.timing_init, non_blocking=True)
+        N.check(N.load().qtn_graph_launch(self._io_graph(), ctypes.c_void_p(s.cuda_stream)))
+        s.synchronize()
+        r = self.results_host.numpy()
+        return r[0::2] + 1j * r[1::2]

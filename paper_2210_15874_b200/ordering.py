@@ -282,6 +282,10 @@ def _raw_inputs(tn: TensorNetwork) -> np.ndarray:
 
 def _template(tn, order, backend, fixed=()):
     struct, _, plans = NETWORK_INPUTS.get(tn)
+    return _template_from(struct, plans, order, backend, fixed)
+
+
+def _template_from(struct, plans, order, backend, fixed=()):
     okey = (tuple(order), tuple(fixed), backend.dtype, backend.threshold)
     got = plans.get(okey)
     if got is not None:
@@ -354,9 +358,9 @@ def contract_network(tn: TensorNetwork, order, backend: Backend = None, mem_cap:
     backend = backend or Backend()
     if tn.open_indices:
         raise ValueError("contract_network requires a closed network")
-    key, tmpl = _template(tn, order, backend)   # raises for indices missing from the order
-    _check_cap(tmpl, backend, mem_cap)
     struct, raw, plans = NETWORK_INPUTS.get(tn)
+    key, tmpl = _template_from(struct, plans, order, backend)   # raises for indices missing from the order
+    _check_cap(tmpl, backend, mem_cap)
     xkey = ("exec", tuple(order), backend.dtype, backend.threshold, backend.device, backend.profile)
     got = plans.get(xkey)
     if got is None:
