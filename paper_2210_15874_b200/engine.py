@@ -597,6 +597,17 @@ class Instance:
     assignment: dict = field(default_factory=dict)   # fixed index -> 0/1
 
 
+def _template_lists(t: Template) -> dict:
+    """Python-list copies of a template's item/member tables (cached on it)."""
+    tl = getattr(t, "_lists", None)
+    if tl is None:
+        tl = {name: getattr(t, name).tolist() for name in
+              ("w", "k", "L", "level", "smem_elems", "stmask", "variant", "mem_ptr", "mem_kind", "mem_ref",
+               "mem_mask", "mem_smask", "mem_cls", "in_off", "fin_kind", "fin_ref")}
+        t._lists = tl
+    return tl
+
+
 class Program:
     """Several instances laid out in one arena, their items grouped into the
     nodes of one CUDA graph.
@@ -623,25 +634,24 @@ class Program:
         self.in_base = in_base
 
         # ---- global item order (topological) ----
+        tls = [_template_lists(inst.template) for inst in self.instances]
         keys = []
-        for i, inst in enumerate(self.instances):
-            t = inst.template
-            for b in range(t.n_items):
-                keys.append((int(t.level[b]), i, b))
-            top = int(t.level.max()) + 1 if len(t.level) else 0
-            keys.append((top, i, -1))  # finaliser
+        for i, tl in enumerate(tls):
+            lev = tl["level"]
+            keys.extend((lev[b], i, b) for b in range(len(lev)))
+            keys.append(((max(lev) + 1) if lev else 0, i, -1))  # finaliser
         keys.sort(key=lambda q: (q[0], q[1], q[2] if q[2] >= 0 else 1 << 40))
 
         # ---- producers of every item (global ids) ----
         order_gid = {(i, b): g for g, (_, i, b) in enumerate(keys)}
         prods = []
         for (_, i, b) in keys:
-            t = self.instances[i].template
+            tl = tls[i]
             if b >= 0:
-                ps = [order_gid[(i, int(t.mem_ref[j]))] for j in range(t.mem_ptr[b], t.mem_ptr[b + 1])
-                      if t.mem_kind[j] == 1]
+                mk, mr = tl["mem_kind"], tl["mem_ref"]
+                ps = [order_gid[(i, mr[j])] for j in range(tl["mem_ptr"][b], tl["mem_ptr"][b + 1]) if mk[j] == 1]
             else:
-                ps = [order_gid[(i, int(r))] for kd, r in zip(t.fin_kind, t.fin_ref) if kd == 1]
+                ps = [order_gid[(i, r)] for kd, r in zip(tl["fin_kind"], tl["fin_ref"]) if kd == 1]
             prods.append(ps)
 
         # ---- intermediates: liveness-based reuse in item order ----
@@ -658,7 +668,7 @@ class Program:
         wid, in_small = {}, set()
         for g, (_, i, b) in enumerate(keys):
             if b >= 0:
-                size = 1 << int(self.instances[i].template.w[b])
+                size = 1 << tls[i]["w"][b]
                 wid[g] = size
                 if self.reuse and size >= REUSE_MIN_ELEMS:
                     off, readers = pool.alloc(size, _tensor_align(size))
@@ -679,7 +689,7 @@ class Program:
         # ---- nodes: large items alone, small items in stages ----
         def is_small(q):
             _, i, b = q
-            return b < 0 or int(self.instances[i].template.variant[b]) == VARIANT_SMALL
+            return b < 0 or tls[i]["variant"][b] == VARIANT_SMALL
 
         node_of = [-1] * len(keys)
         nodes = []           # dict(kind, items, deps:set)
@@ -711,77 +721,72 @@ class Program:
             item_keys[new_of[g]] = (q, g)
 
         nb = len(keys)
-        B = np.zeros(nb, N.BUCKET_DT)
+        # tables built from plain Python lists (numpy scalar field writes cost
+        # ~1 us each; cfg-4 batches have thousands of items)
+        recs = [None] * nb
         members, deps = [], []
         smem_max = 0
         self.bucket_gid = [np.zeros(inst.template.n_items, np.int64) for inst in self.instances]
         self.fin_gid = [0] * len(self.instances)
-        ntiles = np.zeros(nb, np.int64)
+        ntiles = [0] * nb
         for gid, ((_, i, b), g) in enumerate(item_keys):
-            t = self.instances[i].template
-            ntiles[gid] = (1 << int(t.w[b] - t.L[b])) if b >= 0 else 1
+            tl = tls[i]
+            ntiles[gid] = (1 << (tl["w"][b] - tl["L"][b])) if b >= 0 else 1
             if b >= 0:
                 self.bucket_gid[i][b] = gid
             else:
                 self.fin_gid[i] = gid
         node_list = []
         node_deps = []
+        small_kind = N.QTN_NODE_SMALL
         for ni, nd in enumerate(nodes):
             gids = [new_of[g] for g in nd["items"]]
             first, count = min(gids), len(gids)
             assert gids == list(range(first, first + count))
             tick = 0
-            node_smem = SMALL_PROD_ELEMS * esz if nd["kind"] == N.QTN_NODE_SMALL else 0
+            is_stage = nd["kind"] == small_kind
+            node_smem = SMALL_PROD_ELEMS * esz if is_stage else 0
             variant = 0
             for gid in gids:
                 (_, i, b), g = item_keys[gid]
-                t = self.instances[i].template
+                tl = tls[i]
                 ib = in_base[i]
-                rec = B[gid]
-                rec["tick_begin"] = tick if nd["kind"] == N.QTN_NODE_SMALL else 0
-                rec["n_tiles"] = ntiles[gid]
-                rec["mem_begin"] = len(members)
-                rec["dep_begin"] = len(deps)
+                mem_begin, dep_begin = len(members), len(deps)
                 if b >= 0:
-                    rec["w"], rec["k"], rec["tile_bits"] = t.w[b], t.k[b], t.L[b]
-                    rec["out_off"] = out_elem[g]
-                    rec["slot"] = -1
-                    rec["smem_elems"] = t.smem_elems[b]
-                    rec["stmask"] = t.stmask[b]
-                    for j in range(t.mem_ptr[b], t.mem_ptr[b + 1]):
-                        kind, ref = int(t.mem_kind[j]), int(t.mem_ref[j])
-                        if kind == 0:
-                            off = ib + int(t.in_off[ref])
-                        else:
-                            off = out_elem[order_gid[(i, ref)]]
-                        members.append((off, int(t.mem_mask[j]), int(t.mem_smask[j]), int(t.mem_cls[j])))
-                    rec["n_mem"] = t.mem_ptr[b + 1] - t.mem_ptr[b]
-                    if nd["kind"] == N.QTN_NODE_LARGE:
-                        variant = int(t.variant[b])
-                        node_smem = _align(int(t.smem_elems[b]) * esz, 16)
+                    in_off, mk, mr = tl["in_off"], tl["mem_kind"], tl["mem_ref"]
+                    mm, msm, mc = tl["mem_mask"], tl["mem_smask"], tl["mem_cls"]
+                    j0, j1 = tl["mem_ptr"][b], tl["mem_ptr"][b + 1]
+                    for j in range(j0, j1):
+                        ref = mr[j]
+                        off = ib + in_off[ref] if mk[j] == 0 else out_elem[order_gid[(i, ref)]]
+                        members.append((off, mm[j], msm[j], mc[j]))
+                    if not is_stage:
+                        variant = tl["variant"][b]
+                        node_smem = _align(tl["smem_elems"][b] * esz, 16)
+                    w_, k_, L_, out_, slot_, nmem_ = tl["w"][b], tl["k"][b], tl["L"][b], out_elem[g], -1, j1 - j0
+                    smem_, stm_ = tl["smem_elems"][b], tl["stmask"][b]
                 else:
-                    rec["w"] = N.QTN_FINALIZE
-                    rec["k"], rec["tile_bits"], rec["out_off"] = 0, 0, 0
-                    rec["slot"] = i
-                    for kd, ref in zip(t.fin_kind, t.fin_ref):
-                        if kd == 0:
-                            off = ib + int(t.in_off[ref])
-                        else:
-                            off = out_elem[order_gid[(i, int(ref))]]
+                    in_off = tl["in_off"]
+                    for kd, ref in zip(tl["fin_kind"], tl["fin_ref"]):
+                        off = ib + in_off[ref] if kd == 0 else out_elem[order_gid[(i, ref)]]
                         members.append((off, 0, 0, 0))
-                    rec["n_mem"] = len(t.fin_kind)
+                    w_, k_, L_, out_, slot_, nmem_ = N.QTN_FINALIZE, 0, 0, 0, i, len(tl["fin_kind"])
+                    smem_, stm_ = 0, 0
                 # completion dependencies inside this stage (RAW + WAR)
                 for dg in deps_all[g]:
                     if node_of[dg] == ni:
                         pg = new_of[dg]
                         deps.append((pg, ntiles[pg]))
-                rec["n_dep"] = len(deps) - rec["dep_begin"]
-                tick += int(ntiles[gid])
+                # BUCKET_DT field order
+                recs[gid] = (out_, w_, L_, k_, mem_begin, nmem_, dep_begin, len(deps) - dep_begin,
+                             tick if is_stage else 0, ntiles[gid], slot_, smem_, stm_)
+                tick += ntiles[gid]
             smem_max = max(smem_max, node_smem)
             dl = sorted(nd["deps"])
-            node_list.append((nd["kind"], first, count, tick if nd["kind"] == N.QTN_NODE_SMALL else 0,
+            node_list.append((nd["kind"], first, count, tick if is_stage else 0,
                               variant, len(node_deps), len(dl), node_smem))
             node_deps.extend(dl)
+        B = np.array(recs, dtype=N.BUCKET_DT) if nb else np.zeros(0, N.BUCKET_DT)
         if max(int(n[3]) for n in node_list) >= 2 ** 31 - 1:
             raise ValueError("program stage too large (ticket space)")
         self.n_buckets = nb
