@@ -421,6 +421,14 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
 // =========================================================================
 // K1: large-item kernels
 // =========================================================================
+// A large item's descriptor and member records, passed to its K1 launch as
+// a kernel parameter (known when the graph is built): the prologue needs no
+// dependent global loads.
+struct K1Item {
+  qtn_bucket_t b;
+  qtn_member_t mem[MAXM];
+};
+
 struct LargeCtx {
   qtn_bucket_t b;
   uint64_t off[MAXM];
@@ -449,18 +457,18 @@ struct LargeCtx {
 // mapping (v -> bit 0 for c64, lane -> the next 5 bits for coalesced warp
 // stores, warp and step bits -> the rest; step bits = the item's stmask).
 template <typename R>
-__device__ __forceinline__ void large_prep(LargeCtx& S, const qtn_program_t& P, int item, int nb0_expected) {
+__device__ __forceinline__ void large_prep(LargeCtx& S, const qtn_program_t& P, int item, const K1Item& it,
+                                           int nb0_expected) {
   using T = typename Cx<R>::T;
   constexpr int VEC = Cx<R>::VEC;
   constexpr int EPV = 16 / (int)sizeof(T);
   const int tid = threadIdx.x;
-  if (tid == 0) S.b = P.buckets[item];
-  __syncthreads();
-  const int nm = S.b.n_mem;
-  const int L = S.b.tile_bits;
-  const int k = S.b.k;
+  if (tid == 0) S.b = it.b;   // published by the __syncthreads below
+  const int nm = it.b.n_mem;
+  const int L = it.b.tile_bits;
+  const int k = it.b.k;
   if (tid < nm) {
-    const qtn_member_t m = P.members[S.b.mem_begin + tid];
+    const qtn_member_t m = it.mem[tid];
     const uint32_t lowmask = (1u << L) - 1u;
     S.off[tid] = m.off;
     S.mlo[tid] = (uint32_t)(m.mask & lowmask);
@@ -475,7 +483,7 @@ __device__ __forceinline__ void large_prep(LargeCtx& S, const qtn_program_t& P, 
   {
     constexpr int LB = (VEC == 2) ? 1 : 0;
     const uint32_t hi = ((1u << L) - 1u) & ~((1u << (LB + 5)) - 1u);
-    uint32_t stm = S.b.stmask & hi;
+    uint32_t stm = it.b.stmask & hi;
     if (__popc(stm) != L - LB - 8) stm = hi & ~((1u << (LB + 8)) - 1u);
     const uint32_t wm = hi & ~stm;
     S.eth[tid] = (int)(((uint32_t)(tid & 31) << LB) | pdep32((uint32_t)(tid >> 5), wm));
@@ -778,7 +786,7 @@ __device__ __forceinline__ void large_compute_generic(const LargeCtx& S, const t
 
 // NS < 0: generic compute.
 template <typename R, int NS, int NV, int ST, int NB0>
-__device__ __forceinline__ void large_body(const qtn_program_t& P, int32_t item) {
+__device__ __forceinline__ void large_body(const qtn_program_t& P, int32_t item, const K1Item& it) {
   using T = typename Cx<R>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sseg = reinterpret_cast<T*>(smem_raw);
@@ -792,7 +800,7 @@ __device__ __forceinline__ void large_body(const qtn_program_t& P, int32_t item)
     mbar_init(&bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  large_prep<R>(S, P, item, NS > 0 ? NB0 : -1);   // static tables only
+  large_prep<R>(S, P, item, it, NS > 0 ? NB0 : -1);   // static tables only
   pdl_wait();                  // predecessors complete: their outputs are readable
   unsigned long long t_start = 0;
   if (P.timing && tid == 0) t_start = globaltimer();
@@ -823,12 +831,13 @@ __device__ __forceinline__ void large_body(const qtn_program_t& P, int32_t item)
 #define K1_C64_BOUNDS __launch_bounds__(NT)
 #endif
 template <int NS, int NV, int ST, int NB0>
-__global__ void K1_C64_BOUNDS large_kernel_c64(const qtn_program_t P, int32_t item) {
-  large_body<float, NS, NV, ST, NB0>(P, item);
+__global__ void K1_C64_BOUNDS large_kernel_c64(const qtn_program_t P, int32_t item, const __grid_constant__ K1Item it) {
+  large_body<float, NS, NV, ST, NB0>(P, item, it);
 }
 template <int NS, int NV, int ST, int NB0>
-__global__ void __launch_bounds__(NT, 3) large_kernel_c128(const qtn_program_t P, int32_t item) {
-  large_body<double, NS, NV, ST, NB0>(P, item);
+__global__ void __launch_bounds__(NT, 3) large_kernel_c128(const qtn_program_t P, int32_t item,
+                                                           const __grid_constant__ K1Item it) {
+  large_body<double, NS, NV, ST, NB0>(P, item, it);
 }
 template <typename R, int NS, int NV, int ST, int NB0>
 struct LargeK {
@@ -862,7 +871,7 @@ __global__ void permute_kernel(const typename Cx<RS>::T* __restrict__ src, int64
 // =========================================================================
 // host side: kernel selection, launch configuration, graphs
 // =========================================================================
-using LargeFn = void (*)(const qtn_program_t, int32_t);
+using LargeFn = void (*)(const qtn_program_t, int32_t, K1Item);
 
 template <typename R, int NS, int NV, int ST>
 LargeFn large_fn_nb0(int nb0) {
@@ -935,6 +944,7 @@ struct LaunchSpec {
   qtn_program_t prog;
   int32_t a0, a1, a2;
   uint32_t* ctl;
+  K1Item k1item;                       // K1 node: its item (kernel parameter)
   std::vector<unsigned char> k3plan;   // K3 node: its Plan (kernel parameter)
 };
 
@@ -947,8 +957,8 @@ int check_program(const qtn_program_t* p) {
   return QTN_OK;
 }
 
-// Fill the launch of node `ni` (n_tiles: tiles of a LARGE node's item).
-int make_launch(const qtn_program_t* p, const qtn_node_t* nd, int ni, int32_t n_tiles, LaunchSpec* L) {
+// Fill the launch of node `ni` (itm: host copy of a LARGE node's item + members).
+int make_launch(const qtn_program_t* p, const qtn_node_t* nd, int ni, const K1Item* itm, LaunchSpec* L) {
   L->prog = *p;
   L->smem = nd->smem_bytes;
   if (L->smem < 0 || L->smem > 227 * 1024) return set_err(QTN_E_INVALID, "node smem %d", L->smem);
@@ -972,10 +982,14 @@ int make_launch(const qtn_program_t* p, const qtn_node_t* nd, int ni, int32_t n_
                                 : (const void*)large_fn<double>(nd->variant);
     rc = resident_grid(L->fn, L->smem, &L->grid);
     if (rc) return rc;
+    if (!itm) return set_err(QTN_E_INVALID, "large node without item");
+    const int32_t n_tiles = itm->b.n_tiles;
     if (n_tiles < L->grid) L->grid = n_tiles > 0 ? n_tiles : 1;
     L->a0 = nd->first;
+    L->k1item = *itm;
     L->args[0] = &L->prog;
     L->args[1] = &L->a0;
+    L->args[2] = &L->k1item;
   } else {
     return set_err(QTN_E_INVALID, "bad node kind %d", nd->kind);
   }
@@ -1075,16 +1089,19 @@ int qtn_node_launch(const qtn_program_t* p, const qtn_node_t* nd, int32_t ni, vo
   int rc = check_program(p);
   if (rc) return rc;
   if (!nd) return set_err(QTN_E_INVALID, "null node");
-  int32_t tiles = 0;
+  K1Item itm{};
   if (nd->kind == QTN_NODE_LARGE) {
     if (nd->first < 0 || nd->first >= p->n_buckets) return set_err(QTN_E_INVALID, "item %d out of range", nd->first);
-    qtn_bucket_t b;
-    const cudaError_t e = cudaMemcpy(&b, p->buckets + nd->first, sizeof(b), cudaMemcpyDeviceToHost);
+    cudaError_t e = cudaMemcpy(&itm.b, p->buckets + nd->first, sizeof(itm.b), cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cuda_err(e, "cudaMemcpy(item)");
-    tiles = b.n_tiles;
+    if (itm.b.n_mem < 0 || itm.b.n_mem > MAXM) return set_err(QTN_E_INVALID, "item %d: %d members", nd->first, itm.b.n_mem);
+    if (itm.b.n_mem > 0) {
+      e = cudaMemcpy(itm.mem, p->members + itm.b.mem_begin, sizeof(qtn_member_t) * itm.b.n_mem, cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) return cuda_err(e, "cudaMemcpy(members)");
+    }
   }
   LaunchSpec L;
-  rc = make_launch(p, nd, ni, tiles, &L);
+  rc = make_launch(p, nd, ni, nd->kind == QTN_NODE_LARGE ? &itm : nullptr, &L);
   if (rc) return rc;
   const cudaError_t e = cudaLaunchKernel(L.fn, dim3(L.grid), dim3(NT), L.args, L.smem, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_err(e, "cudaLaunchKernel");
@@ -1110,7 +1127,7 @@ int qtn_graph_create_io(const qtn_program_t* p, const qtn_node_t* nodes, int32_t
   int64_t n_members = 0;
   for (const qtn_bucket_t& b : items) n_members = std::max<int64_t>(n_members, (int64_t)b.mem_begin + std::max(0, b.n_mem));
   std::vector<qtn_member_t> mems(n_members);
-  if (n_members && p->members && p->arena) {
+  if (n_members && p->members) {
     const cudaError_t e = cudaMemcpy(mems.data(), p->members, sizeof(qtn_member_t) * mems.size(), cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cuda_err(e, "cudaMemcpy(members)");
   }
@@ -1140,8 +1157,16 @@ int qtn_graph_create_io(const qtn_program_t* p, const qtn_node_t* nodes, int32_t
       qtn_graph_destroy(g);
       return set_err(QTN_E_INVALID, "node %d: item %d out of range", i, nd.first);
     }
-    const int32_t tiles = nd.kind == QTN_NODE_LARGE ? items[nd.first].n_tiles : 0;
-    rc = make_launch(p, &nd, i, tiles, &specs[i]);
+    K1Item itm{};
+    if (nd.kind == QTN_NODE_LARGE) {
+      itm.b = items[nd.first];
+      if (itm.b.n_mem < 0 || itm.b.n_mem > MAXM) {
+        qtn_graph_destroy(g);
+        return set_err(QTN_E_INVALID, "node %d: item with %d members", i, itm.b.n_mem);
+      }
+      for (int j = 0; j < itm.b.n_mem; ++j) itm.mem[j] = mems[itm.b.mem_begin + j];
+    }
+    rc = make_launch(p, &nd, i, nd.kind == QTN_NODE_LARGE ? &itm : nullptr, &specs[i]);
     if (rc) {
       qtn_graph_destroy(g);
       return rc;
