@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define QTN_ABI_VERSION 7
+#define QTN_ABI_VERSION 8
 
 enum {
   QTN_OK = 0,
@@ -183,6 +183,14 @@ typedef struct {
 } qtn_graph_io_t;
 int qtn_graph_create_io(const qtn_program_t* prog, const qtn_node_t* nodes, int32_t n_nodes,
                         const int32_t* node_deps, const qtn_graph_io_t* io, qtn_graph_t** out);
+/* Same, reading the item and member tables from HOST copies (the caller's
+ * planner output, identical to what prog->buckets / prog->members hold on the
+ * device) instead of copying them back: no synchronous device access, so a
+ * graph can be built while earlier work still runs on the device.  io may be
+ * NULL; host_members must hold every member the items reference. */
+int qtn_graph_create_host(const qtn_program_t* prog, const qtn_bucket_t* host_items, const qtn_member_t* host_members,
+                          int64_t n_host_members, const qtn_node_t* nodes, int32_t n_nodes,
+                          const int32_t* node_deps, const qtn_graph_io_t* io, qtn_graph_t** out);
 /* Launch the instantiated graph (one call per program execution). */
 int qtn_graph_launch(qtn_graph_t* g, void* stream);
 int qtn_graph_destroy(qtn_graph_t* g);

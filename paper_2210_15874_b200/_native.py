@@ -26,7 +26,7 @@ QTN_FINALIZE = -1
 MAX_MEMBERS = 8
 MAX_WIDTH = 40
 MAX_SUMMED = 6
-ABI_VERSION = 7
+ABI_VERSION = 8
 QTN_NODE_SMALL = 0
 QTN_NODE_LARGE = 1
 QTN_VARIANT_GENERIC = -1
@@ -40,6 +40,7 @@ EXPORTS = (
     "qtn_node_launch",
     "qtn_graph_create",
     "qtn_graph_create_io",
+    "qtn_graph_create_host",
     "qtn_graph_launch",
     "qtn_graph_destroy",
     "qtn_permute",
@@ -140,6 +141,9 @@ def load(path: str = LIB_PATH):
     lib.qtn_node_launch.argtypes = [ctypes.POINTER(ProgramC), vp, i32, vp]
     lib.qtn_graph_create.restype = ctypes.c_int
     lib.qtn_graph_create.argtypes = [ctypes.POINTER(ProgramC), vp, i32, vp, ctypes.POINTER(ctypes.c_void_p)]
+    lib.qtn_graph_create_host.restype = ctypes.c_int
+    lib.qtn_graph_create_host.argtypes = [ctypes.POINTER(ProgramC), vp, vp, ctypes.c_int64, vp, i32, vp,
+                                          ctypes.POINTER(GraphIOC), ctypes.POINTER(ctypes.c_void_p)]
     lib.qtn_graph_create_io.restype = ctypes.c_int
     lib.qtn_graph_create_io.argtypes = [ctypes.POINTER(ProgramC), vp, i32, vp, ctypes.POINTER(GraphIOC),
                                         ctypes.POINTER(ctypes.c_void_p)]

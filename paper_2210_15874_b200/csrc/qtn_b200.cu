@@ -1117,7 +1117,6 @@ int qtn_graph_create_io(const qtn_program_t* p, const qtn_node_t* nodes, int32_t
                         const qtn_graph_io_t* io, qtn_graph_t** out) {
   int rc = check_program(p);
   if (rc) return rc;
-  if (!out || (n_nodes > 0 && !nodes)) return set_err(QTN_E_INVALID, "null argument");
   std::vector<qtn_bucket_t> items(p->n_buckets);
   if (p->n_buckets) {
     const cudaError_t e =
@@ -1131,6 +1130,24 @@ int qtn_graph_create_io(const qtn_program_t* p, const qtn_node_t* nodes, int32_t
     const cudaError_t e = cudaMemcpy(mems.data(), p->members, sizeof(qtn_member_t) * mems.size(), cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cuda_err(e, "cudaMemcpy(members)");
   }
+  return qtn_graph_create_host(p, items.data(), mems.data(), n_members, nodes, n_nodes, node_deps, io, out);
+}
+
+int qtn_graph_create_host(const qtn_program_t* p, const qtn_bucket_t* items, const qtn_member_t* mems_in,
+                          int64_t n_host_members, const qtn_node_t* nodes, int32_t n_nodes, const int32_t* node_deps,
+                          const qtn_graph_io_t* io, qtn_graph_t** out) {
+  int rc = check_program(p);
+  if (rc) return rc;
+  if (!out || (n_nodes > 0 && !nodes) || (p->n_buckets > 0 && !items)) return set_err(QTN_E_INVALID, "null argument");
+  for (int32_t i = 0; i < p->n_buckets; ++i) {
+    const qtn_bucket_t& b = items[i];
+    if (b.n_mem < 0 || b.mem_begin < 0 || (int64_t)b.mem_begin + b.n_mem > n_host_members || (b.n_mem > 0 && !mems_in))
+      return set_err(QTN_E_INVALID, "item %d: members [%d, +%d) outside the %lld host members", i, b.mem_begin,
+                     b.n_mem, (long long)n_host_members);
+  }
+  // the K3 route wants a member array it can index (empty when there is none)
+  const qtn_member_t* mems_ptr = mems_in;
+  const bool have_mems = n_host_members > 0 && mems_in;
   qtn_graph* g = new qtn_graph();
   cudaError_t e = cudaGraphCreate(&g->graph, 0);
   if (e != cudaSuccess) {
@@ -1164,16 +1181,16 @@ int qtn_graph_create_io(const qtn_program_t* p, const qtn_node_t* nodes, int32_t
         qtn_graph_destroy(g);
         return set_err(QTN_E_INVALID, "node %d: item with %d members", i, itm.b.n_mem);
       }
-      for (int j = 0; j < itm.b.n_mem; ++j) itm.mem[j] = mems[itm.b.mem_begin + j];
+      for (int j = 0; j < itm.b.n_mem; ++j) itm.mem[j] = mems_ptr[itm.b.mem_begin + j];
     }
     rc = make_launch(p, &nd, i, nd.kind == QTN_NODE_LARGE ? &itm : nullptr, &specs[i]);
     if (rc) {
       qtn_graph_destroy(g);
       return rc;
     }
-    if (nd.kind == QTN_NODE_LARGE && p->arena && !mems.empty() && k3_route(items[nd.first], mems.data(), p->dtype)) {
+    if (nd.kind == QTN_NODE_LARGE && p->arena && have_mems && k3_route(items[nd.first], mems_ptr, p->dtype)) {
       qtn_bucket_desc_t d;
-      k3_desc(p, items[nd.first], mems.data(), &d);
+      k3_desc(p, items[nd.first], mems_ptr, &d);
       specs[i].k3plan.resize(qtn_k3_plan_bytes());
       const void* fn = nullptr;
       int grid = 0, smem = 0;

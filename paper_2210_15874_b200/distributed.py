@@ -203,8 +203,11 @@ def run_local(plan: UnitPlan, mine, backend: Backend, device: int, budget_bytes=
         if budget_bytes is None:
             free, _ = torch.cuda.mem_get_info(device)
             budget_bytes = int(0.6 * free)
+        batches = list(_batches(mine, plan, be, budget_bytes))
+        if len(batches) > 1:   # does not fit at once: stream the batches, keep nothing
+            return _run_streamed(plan, batches, be, device)
         built = []
-        for batch in _batches(mine, plan, be, budget_bytes):
+        for batch in batches:
             insts = [E.Instance(plan.templates[plan.units[u].cone], plan.units[u].assignment) for u in batch]
             built.append((E.Executor(E.Program(insts, be.dtype), device=device, timing=be.profile), batch))
         if cache is not None:
@@ -222,6 +225,48 @@ def run_local(plan: UnitPlan, mine, backend: Backend, device: int, budget_bytes=
             tm = plan.templates[ci]
             el = np.maximum(t1[prog.bucket_gid[k]] - t0[prog.bucket_gid[k]], 0) if be.profile else None
             stats.setdefault(ci, []).extend(ref_stats(tm, be, el))
+    return vals, stats
+
+
+def _run_streamed(plan, batches, be, device):
+    """Batches that do not fit in HBM together, run one after another through
+    one shared arena: batch k+1's Program (host planning, the expensive part)
+    and Executor (graph build from host tables, pinned uploads) are prepared
+    while batch k runs, then queued behind it on the same stream; batch k's
+    results are read after k+1 was submitted.  The arena grows (after a wait)
+    when a batch needs more."""
+    import torch
+    from .ordering import ref_stats
+    tdt = torch.complex64 if be.dtype == "complex64" else torch.complex128
+    vals, stats = {}, {}
+    arena, prev = None, None
+
+    def finish(ex, batch):
+        res = ex.collect()
+        if be.profile:
+            t0, t1 = ex.fetch_timing()
+        for k, u in enumerate(batch):
+            vals[u] = complex(res[k])
+            ci = plan.units[u].cone
+            el = (np.maximum(t1[ex.prog.bucket_gid[k]] - t0[ex.prog.bucket_gid[k]], 0) if be.profile else None)
+            stats.setdefault(ci, []).extend(ref_stats(plan.templates[ci], be, el))
+
+    for batch in batches:
+        insts = [E.Instance(plan.templates[plan.units[u].cone], plan.units[u].assignment) for u in batch]
+        prog = E.Program(insts, be.dtype)
+        if arena is None or arena.numel() < prog.arena_elems:
+            if prev is not None:
+                finish(*prev)
+                prev = None
+            arena = None
+            arena = torch.empty(prog.arena_elems, dtype=tdt, device=torch.device("cuda", device))
+        ex = E.Executor(prog, device=device, timing=be.profile, arena=arena)
+        ex.submit([plan.raws[plan.units[u].cone] for u in batch])
+        if prev is not None:
+            finish(*prev)
+        prev = (ex, batch)
+    if prev is not None:
+        finish(*prev)
     return vals, stats
 
 

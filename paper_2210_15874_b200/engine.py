@@ -827,9 +827,15 @@ class Program:
 class Executor:
     """Device-resident copy of a Program: tables, control block, arena and
     result slots owned by torch; the node graph is built once through the C
-    ABI (qtn_graph_create) and every run is one cudaGraphLaunch."""
+    ABI (qtn_graph_create_host, from the host copies of the tables: no device
+    synchronisation, so an executor can be built while earlier work runs) and
+    every run is one cudaGraphLaunch.
 
-    def __init__(self, prog: Program, device=0, timing=False):
+    arena: optional caller-owned element buffer (dtype of the program, at
+    least prog.arena_elems) shared by executors that run one after another on
+    one stream — stream order keeps a later upload behind earlier kernels."""
+
+    def __init__(self, prog: Program, device=0, timing=False, arena=None):
         import torch
         self.torch = torch
         N.require_device()
@@ -851,9 +857,16 @@ class Executor:
             host = np.zeros(_align(total, 16), np.uint8)
             for o, p_ in zip(offs, parts):
                 host[o:o + len(p_)] = np.frombuffer(p_, np.uint8)
-            self.tables = torch.from_numpy(host).to(dev)
+            # pinned + non_blocking: a pageable copy would wait for the stream
+            self.tables = torch.from_numpy(host).pin_memory().to(dev, non_blocking=True)
             base = self.tables.data_ptr()
-            self.arena = torch.empty(prog.arena_elems, dtype=tdt, device=dev)
+            if arena is not None:
+                if arena.dtype != tdt or arena.device != dev or arena.numel() < prog.arena_elems:
+                    raise ValueError(f"arena: need {prog.arena_elems} {tdt} elements on {dev}, got "
+                                     f"{arena.numel()} {arena.dtype} on {arena.device}")
+                self.arena = arena
+            else:
+                self.arena = torch.empty(prog.arena_elems, dtype=tdt, device=dev)
             self.results = torch.zeros(2 * max(1, len(prog.instances)), dtype=torch.float64, device=dev)
             self.results_host = torch.zeros_like(self.results, device="cpu").pin_memory()
             self.timing = None
@@ -879,16 +892,32 @@ class Executor:
             c.timing = self.timing.data_ptr() if timing else None
             c.arena_elems = prog.arena_elems
             self.c = c
-            torch.cuda.synchronize(dev)
-            g = ctypes.c_void_p()
-            nodes = np.ascontiguousarray(prog.nodes)
-            deps = np.ascontiguousarray(prog.node_deps)
-            N.check(lib.qtn_graph_create(ctypes.byref(c), nodes.ctypes.data_as(ctypes.c_void_p), prog.n_nodes,
-                                         deps.ctypes.data_as(ctypes.c_void_p), ctypes.byref(g)))
-            self.graph = g
+            self.done = torch.cuda.Event()
+        self._graph = None
+        self.graph_io = None
+
+    def _create_graph(self, io):
+        nodes = np.ascontiguousarray(self.prog.nodes)
+        deps = np.ascontiguousarray(self.prog.node_deps)
+        items = np.ascontiguousarray(self.prog.buckets)
+        mems = np.ascontiguousarray(self.prog.members)
+        g = ctypes.c_void_p()
+        with self.torch.cuda.device(self.device):
+            N.check(N.load().qtn_graph_create_host(
+                ctypes.byref(self.c), items.ctypes.data_as(ctypes.c_void_p), mems.ctypes.data_as(ctypes.c_void_p),
+                len(mems), nodes.ctypes.data_as(ctypes.c_void_p), self.prog.n_nodes,
+                deps.ctypes.data_as(ctypes.c_void_p), ctypes.byref(io) if io is not None else None, ctypes.byref(g)))
+        return g
+
+    @property
+    def graph(self):
+        """The program graph (kernels only), built on first use."""
+        if self._graph is None:
+            self._graph = self._create_graph(None)
+        return self._graph
 
     def __del__(self):
-        for name in ("graph", "graph_io"):
+        for name in ("_graph", "graph_io"):
             g = getattr(self, name, None)
             if g is not None and g.value:
                 try:
@@ -940,28 +969,26 @@ class Executor:
         """The program graph with the input upload as its first node and the
         result download as its last (built on first use): run() is then one
         graph launch and one stream synchronisation."""
-        g = getattr(self, "graph_io", None)
+        g = self.graph_io
         if g is None:
-            torch = self.torch
-            lib = N.load()
             esz = self.arena.element_size()
             io = N.GraphIOC(h2d_src=self.img_pinned.data_ptr(), h2d_dst=self.arena.data_ptr(),
                             h2d_bytes=int(self.prog.n_input_elems) * esz,
                             d2h_src=self.results.data_ptr(), d2h_dst=self.results_host.data_ptr(),
                             d2h_bytes=self.results.numel() * self.results.element_size())
-            g = ctypes.c_void_p()
-            nodes = np.ascontiguousarray(self.prog.nodes)
-            deps = np.ascontiguousarray(self.prog.node_deps)
-            with torch.cuda.device(self.device):
-                N.check(lib.qtn_graph_create_io(ctypes.byref(self.c), nodes.ctypes.data_as(ctypes.c_void_p),
-                                                self.prog.n_nodes, deps.ctypes.data_as(ctypes.c_void_p),
-                                                ctypes.byref(io), ctypes.byref(g)))
-            self.graph_io = g
+            g = self.graph_io = self._create_graph(io)
         return g
 
     def run(self, raw_parts, stream=None):
         """Stage the inputs on the host, then one graph launch (upload,
         kernels, download) and one synchronisation."""
+        self.submit(raw_parts, stream)
+        return self.collect()
+
+    def submit(self, raw_parts, stream=None):
+        """run() without the wait: stage the inputs into the pinned image,
+        launch the end-to-end graph and record `done`; collect() waits.  The
+        pinned image must not be restaged before collect()."""
         torch = self.torch
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         view = self.img_pinned.numpy()
@@ -973,6 +1000,10 @@ class Executor:
         if self.timing is not None:
             self.timing.copy_(self.timing_init, non_blocking=True)
         N.check(N.load().qtn_graph_launch(self._io_graph(), ctypes.c_void_p(s.cuda_stream)))
-        s.synchronize()
+        self.done.record(s)
+
+    def collect(self):
+        """Wait for the last submit() and return its per-instance values."""
+        self.done.synchronize()
         r = self.results_host.numpy()
         return r[0::2] + 1j * r[1::2]

@@ -237,3 +237,29 @@ def test_program_items_through_k3(route):
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     assert float(out.stdout.strip().splitlines()[-1]) <= 1.0
+
+
+def test_streamed_batches_shared_arena():
+    """Units that do not fit in one program's HBM budget run as streamed
+    batches through one shared, growing arena (batch k+1 prepared and queued
+    while k runs): same values as one batch, golden <ZZ> per cone."""
+    from paper_2210_15874_b200 import distributed as D
+    g, graph, params = _cfg("cfg2")
+    c = Q.qaoa_maxcut_circuit(graph, params)
+    recs = g["cones"]
+    cones = [Q.extract_lightcone(c, tuple(r["edge"]), cone="tight") for r in recs]
+    for be, tol in ((C64, 1e-5), (C128, 1e-10)):
+        plan = D.plan_units(cones, be, slice_target=20, mem_cap=1 << 40)
+        mine = list(range(len(plan.units)))
+        one, _ = D.run_local(plan, mine, be, 0, budget_bytes=1 << 40)
+        # ascending unit sizes: every few batches need a bigger arena
+        mine_sorted = sorted(mine, key=lambda u: plan.units[u].cost)
+        streamed, _ = D.run_local(plan, mine_sorted, be, 0, budget_bytes=1)
+        assert set(streamed) == set(one)
+        for u in mine:
+            assert abs(streamed[u] - one[u]) <= tol * 1e-2
+        zz = [0j] * len(cones)
+        for u, unit in enumerate(plan.units):
+            zz[unit.cone] += streamed[u]
+        for z, r in zip(zz, recs):
+            assert abs(z.real - r["zz"][0]) <= tol
