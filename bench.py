@@ -234,7 +234,7 @@ def run_ours(args):
     be = Q.Backend.b200(dtype=dtype, device=local, profile=False)
 
     # ---- device-resident program (inputs in HBM before the timed region) ----
-    tmpl = E.plan_template([t.indices for t in tn.tensors], order, dtype)
+    tmpl = E.plan_template([t.indices for t in tn.tensors], order, dtype, wave_aware=True)  # as contract_network
     prog = E.Program([E.Instance(tmpl)], dtype)
     ex = E.Executor(prog, device=local, timing=False)
     raw = np.concatenate([np.asarray(t.data).ravel() for t in tn.tensors])
@@ -325,7 +325,7 @@ def run_ours(args):
         del ext
     side = {}
     if dtype == "complex64":
-        tm2 = E.plan_template([t.indices for t in tn.tensors], order, "complex128")
+        tm2 = E.plan_template([t.indices for t in tn.tensors], order, "complex128", wave_aware=True)
         ex2 = E.Executor(E.Program([E.Instance(tm2)], "complex128"), device=local, timing=False)
         ex2.stage_inputs([raw])
         for _ in range(3):

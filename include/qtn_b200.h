@@ -228,6 +228,8 @@ typedef struct {
   double hop_s, hop_k2_s, bw_bps, block_terms_ps, small_load_s;
   double cheap_member_w;  /* per-result weight of uniform / invariant members (1 = all equal) */
   int32_t kmax_large;     /* summed indices of a merged large (K1) item, <= 3            */
+  int32_t wave_slots;     /* resident K1 blocks on the device (0 = no wave-aware tiles)   */
+  int32_t wave_ov_elems;  /* per-tile fixed cost in result-element equivalents           */
 } qtn_plan_params_t;
 typedef struct qtn_plan qtn_plan_t;
 int qtn_plan_build(int32_t n_tensors, const int32_t* tensor_ptr, const int64_t* tensor_idx,

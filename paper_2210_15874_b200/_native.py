@@ -114,7 +114,8 @@ class PlanParamsC(ctypes.Structure):
                 ("merge", ctypes.c_int32), ("resident_blocks", ctypes.c_int32), ("smem_budget", ctypes.c_int64),
                 ("hop_s", ctypes.c_double), ("hop_k2_s", ctypes.c_double), ("bw_bps", ctypes.c_double),
                 ("block_terms_ps", ctypes.c_double), ("small_load_s", ctypes.c_double),
-                ("cheap_member_w", ctypes.c_double), ("kmax_large", ctypes.c_int32)]
+                ("cheap_member_w", ctypes.c_double), ("kmax_large", ctypes.c_int32),
+                ("wave_slots", ctypes.c_int32), ("wave_ov_elems", ctypes.c_int32)]
 
 
 _lib = None

@@ -74,6 +74,26 @@ struct Planner {
         if ((m[i] & low) != low) st += ((int64_t)1 << popc64(sm[i]) << popc64(m[i] & low)) + 1;
       st += (int64_t)1 << P.kmax;
       if (st * P.elem_bytes <= P.smem_budget || L == 0) {
+        // wave-aware: a smaller tile when the last wave of the persistent
+        // grid would run mostly empty (engine._tile_bits)
+        if (P.wave_slots > 0) {
+          const int lmin = std::max(std::min(w, P.min_tile_bits), L - 2);
+          int best = L;
+          int64_t best_t = -1;
+          for (int l = L; l >= lmin; --l) {
+            const int64_t tiles = (int64_t)1 << (w - l);
+            const int64_t t = (tiles + P.wave_slots - 1) / P.wave_slots * (((int64_t)1 << l) + P.wave_ov_elems);
+            if (best_t < 0 || t < best_t) best = l, best_t = t;
+          }
+          if (best != L) {
+            L = best;
+            const uint64_t low2 = (1ull << L) - 1;
+            st = 0;
+            for (size_t i = 0; i < m.size(); ++i)
+              if ((m[i] & low2) != low2) st += ((int64_t)1 << popc64(sm[i]) << popc64(m[i] & low2)) + 1;
+            st += (int64_t)1 << P.kmax;
+          }
+        }
         if (st_out) *st_out = st;
         return L;
       }

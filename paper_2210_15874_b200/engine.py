@@ -26,6 +26,7 @@ ends with a finaliser item that writes its scalar to a result slot.
 """
 from __future__ import annotations
 
+import bisect
 import ctypes
 import os
 from dataclasses import dataclass, field
@@ -88,6 +89,10 @@ _TERMS_SCALE = float(os.environ.get("QTN_TERMS_SCALE", 1.0))
 CHEAP_MEMBER_W = float(os.environ.get("QTN_CHEAP_W", 1.0))   # per-result weight of uniform/invariant members
 BLOCK_TERMS_PS = {"complex64": 5.0e9 * _TERMS_SCALE, "complex128": 2.4e9 * _TERMS_SCALE}
 RESIDENT_BLOCKS = {"complex64": 296, "complex128": 296}
+# Wave-aware tile size: resident K1 blocks (3 per SM at both dtypes) and the
+# per-tile fixed cost in result-element equivalents; 0 slots = off.
+WAVE_SLOTS = {d: int(os.environ.get("QTN_WAVE_SLOTS", 444)) for d in ("complex64", "complex128")}
+WAVE_OV_ELEMS = int(os.environ.get("QTN_WAVE_OV", 2048))
 SMALL_LOAD_S = 0.65e-6
 MIN_TILE_BITS = {"complex64": 9, "complex128": 8}   # vector path needs VEC*NT results
 # items with w + k <= this run in K2 (default per dtype, measured on cfg-2:
@@ -151,8 +156,10 @@ def _popc(x):
     return bin(x).count("1")
 
 
-def _tile_bits(w, masks, smasks, dtype):
-    """Largest L <= TILE_BITS whose staged runs fit the smem budget."""
+def _tile_bits(w, masks, smasks, dtype, slots=0):
+    """Largest L <= TILE_BITS whose staged runs fit the smem budget; with
+    `slots` (resident K1 blocks, wave-aware plans) up to 2 bits smaller when
+    that fills the persistent grid's last wave better."""
     esz = ELEM_BYTES[dtype]
     L = min(w, TILE_BITS[dtype])
     while True:
@@ -160,8 +167,22 @@ def _tile_bits(w, masks, smasks, dtype):
         st = sum(((1 << _popc(sm)) << _popc(m & low)) + 1 for m, sm in zip(masks, smasks) if (m & low) != low)
         st += 1 << KMAX   # U[s] (tile-uniform product)
         if st * esz <= SMEM_BUDGET or L == 0:
-            return L, st
+            break
         L -= 1
+    if slots > 0:
+        # wave-aware: a smaller tile when the last wave of the persistent grid
+        # would run mostly empty (up to 2 bits smaller, ties keep the larger)
+        best, best_t = L, None
+        for l in range(L, max(min(w, MIN_TILE_BITS[dtype]), L - 2) - 1, -1):
+            t = -(-(1 << (w - l)) // slots) * ((1 << l) + WAVE_OV_ELEMS)
+            if best_t is None or t < best_t:
+                best, best_t = l, t
+        if best != L:
+            L = best
+            low = (1 << L) - 1
+            st = sum(((1 << _popc(sm)) << _popc(m & low)) + 1 for m, sm in zip(masks, smasks) if (m & low) != low)
+            st += 1 << KMAX
+    return L, st
 
 
 def _step_mask(L, masks, dtype):
@@ -243,14 +264,14 @@ def _item_cost(w, k, L, sizes, dtype, hop=None, nm_eff=None):
     return hop + max(byt / BW_BPS, waves * per_tile)
 
 
-def _cost_of(it, dtype, small_iter_bits=None):
+def _cost_of(it, dtype, small_iter_bits=None, slots=0):
     sib = SMALL_ITER_BITS[dtype] if small_iter_bits is None else small_iter_bits
     masks, smasks = _masks(it["members"], it["X"], it["R"])
     w, k = len(it["R"]), len(it["X"])
     if w + k <= sib:
         L = min(w, SMALL_TILE_BITS[dtype])
         return _item_cost(w, k, L, [1 << len(s2) for _, _, s2 in it["members"]], dtype, hop=HOP_K2_S)
-    L, _ = _tile_bits(w, masks, smasks, dtype)
+    L, _ = _tile_bits(w, masks, smasks, dtype, slots)
     nm_eff = None
     if CHEAP_MEMBER_W != 1.0 and (1 << L) >= VEC[dtype] * NT:
         stm = _step_mask(L, masks, dtype)
@@ -271,26 +292,32 @@ def small_iter_bits_for(threshold, dtype="complex64"):
     return int(threshold) + 1
 
 
-def _plan_params(dtype, merge, sib):
+def _plan_params(dtype, merge, sib, wave_aware=False):
     return N.PlanParamsC(
         elem_bytes=ELEM_BYTES[dtype], tile_bits=TILE_BITS[dtype], small_tile_bits=SMALL_TILE_BITS[dtype],
         min_tile_bits=MIN_TILE_BITS[dtype], kmax=KMAX, max_members=N.MAX_MEMBERS, vec=VEC[dtype], nt=NT,
         small_iter_bits=sib, merge=1 if merge else 0, resident_blocks=RESIDENT_BLOCKS[dtype],
         smem_budget=SMEM_BUDGET, hop_s=HOP_S, hop_k2_s=HOP_K2_S, bw_bps=BW_BPS,
         block_terms_ps=BLOCK_TERMS_PS[dtype], small_load_s=SMALL_LOAD_S, cheap_member_w=CHEAP_MEMBER_W,
-        kmax_large=KMAX_LARGE[dtype])
+        kmax_large=KMAX_LARGE[dtype], wave_slots=WAVE_SLOTS[dtype] if wave_aware else 0,
+        wave_ov_elems=WAVE_OV_ELEMS)
 
 
-def plan_template(index_sets, order, dtype, fixed=(), merge=None, small_iter_bits=None):
+def plan_template(index_sets, order, dtype, fixed=(), merge=None, small_iter_bits=None, wave_aware=False):
     """The symbolic plan of one network structure + order (+ sliced
     indices), computed by the native planner (csrc/plan_template.cpp,
     qtn_plan_build) — the C++ restatement of plan_template_py below, which
-    stays as its checker (tests compare the two array by array)."""
+    stays as its checker (tests compare the two array by array).
+
+    wave_aware: the program will run this network alone (one contraction per
+    graph launch), so large items pick tile sizes that fill the last wave of
+    the persistent grid; programs of many instances overlap items instead and
+    keep the largest tiles."""
     dtype = norm_dtype(dtype)
     merge = MERGE_DEFAULT if merge is None else merge
     sib = SMALL_ITER_BITS[dtype] if small_iter_bits is None else int(small_iter_bits)
     fixed = list(dict.fromkeys(int(f) for f in fixed))
-    sc, a = N.plan_build([tuple(int(i) for i in s) for s in index_sets], order, fixed, _plan_params(dtype, merge, sib))
+    sc, a = N.plan_build([tuple(int(i) for i in s) for s in index_sets], order, fixed, _plan_params(dtype, merge, sib, wave_aware))
     ncanon = len(a["gdst"])
     gfix = {f: a["gfix"][j * ncanon:(j + 1) * ncanon] for j, f in enumerate(fixed)}
     return Template(
@@ -306,7 +333,7 @@ def plan_template(index_sets, order, dtype, fixed=(), merge=None, small_iter_bit
     )
 
 
-def plan_template_py(index_sets, order, dtype, fixed=(), merge=None, small_iter_bits=None):
+def plan_template_py(index_sets, order, dtype, fixed=(), merge=None, small_iter_bits=None, wave_aware=False):
     """Replay contract_network's bucket assignment (src/ordering.py:165-187)
     over index sets only and freeze it into a Template.
 
@@ -319,6 +346,7 @@ def plan_template_py(index_sets, order, dtype, fixed=(), merge=None, small_iter_
     dtype = norm_dtype(dtype)
     sib = SMALL_ITER_BITS[dtype] if small_iter_bits is None else int(small_iter_bits)
     merge = MERGE_DEFAULT if merge is None else merge
+    slots = WAVE_SLOTS[dtype] if wave_aware else 0
     fixed = set(int(f) for f in fixed)
     act = [int(i) for i in order if int(i) not in fixed]
     pos = {x: k for k, x in enumerate(act)}
@@ -397,7 +425,7 @@ def plan_template_py(index_sets, order, dtype, fixed=(), merge=None, small_iter_
     for b, (x, mem, R) in enumerate(refs):
         it = {"X": [x], "R": R, "refs": [b],
               "members": [(k_, (item_of[r_] if k_ == 1 else r_), st) for k_, r_, st in mem]}
-        it["cost"] = _cost_of(it, dtype, sib)
+        it["cost"] = _cost_of(it, dtype, sib, slots)
         changed = merge
         while changed:
             changed = False
@@ -413,12 +441,12 @@ def plan_template_py(index_sets, order, dtype, fixed=(), merge=None, small_iter_
                 cand = {"X": X2, "R": R, "members": mem2}
                 if w + len(X2) > sib:
                     masks, smasks = _masks(mem2, X2, R)
-                    L, _ = _tile_bits(w, masks, smasks, dtype)
+                    L, _ = _tile_bits(w, masks, smasks, dtype, slots)
                     if L < min(w, MIN_TILE_BITS[dtype]):
                         continue
                 if w + len(X2) > sib and len(X2) > KMAX_LARGE[dtype]:
                     continue   # k > 3 would need the generic K1 kernel (no specialisation)
-                c2 = _cost_of(cand, dtype, sib)
+                c2 = _cost_of(cand, dtype, sib, slots)
                 if c2 >= it["cost"] + p_["cost"]:
                     continue
                 it["X"], it["members"], it["cost"] = X2, mem2, c2
@@ -446,7 +474,7 @@ def plan_template_py(index_sets, order, dtype, fixed=(), merge=None, small_iter_
             # work; a K2 dependency hop costs ~1.5 us against ~7 us for a K1 node)
             L, st = min(w, SMALL_TILE_BITS[dtype]), 0
         else:
-            L, st = _tile_bits(w, masks, smasks, dtype)
+            L, st = _tile_bits(w, masks, smasks, dtype, slots)
         lv = 0
         for (k_, r_, _), m, sm in zip(it["members"], masks, smasks):
             if k_ == 1:
@@ -523,6 +551,10 @@ def executed_bytes(t: Template, dtype) -> int:
     return tot * ELEM_BYTES[norm_dtype(dtype)]
 
 
+def _blk_start(blk):
+    return blk[0]
+
+
 class _Pool:
     """Best-fit arena allocator over element offsets with free-block
     coalescing.  A freed block remembers the items that last READ it; an
@@ -563,16 +595,25 @@ class _Pool:
         self._insert(start, size, {reader})
 
     def _insert(self, st, sz, rd):
-        self.free.append([st, sz, rd])
-        self.free.sort(key=lambda blk: blk[0])
-        merged = []
-        for blk in self.free:
-            if merged and merged[-1][0] + merged[-1][1] == blk[0]:
-                merged[-1][1] += blk[1]
-                merged[-1][2] = merged[-1][2] | blk[2]
-            else:
-                merged.append(blk)
-        self.free = merged
+        # the list is sorted and coalesced (no two blocks touch): only the
+        # neighbours of the new block can merge with it
+        free = self.free
+        i = bisect.bisect_left(free, st, key=_blk_start)
+        if i > 0 and free[i - 1][0] + free[i - 1][1] == st:
+            prev = free[i - 1]
+            prev[1] += sz
+            prev[2] = prev[2] | rd
+            if i < len(free) and prev[0] + prev[1] == free[i][0]:
+                nxt = free.pop(i)
+                prev[1] += nxt[1]
+                prev[2] = prev[2] | nxt[2]
+        elif i < len(free) and st + sz == free[i][0]:
+            nxt = free[i]
+            nxt[0] = st
+            nxt[1] += sz
+            nxt[2] = rd | nxt[2]
+        else:
+            free.insert(i, [st, sz, rd])
 
 
 def template_peak_elems(t: Template) -> int:

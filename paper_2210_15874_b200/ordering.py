@@ -293,8 +293,11 @@ def _template_from(struct, plans, order, backend, fixed=()):
     key = ("tmpl", struct) + okey
     hit = PLAN_CACHE.get(key)
     if hit is None:
+        # an unsliced contraction runs alone in its graph: wave-aware tiles;
+        # the 2^s slices of contract_sliced run together in one program
         hit = E.plan_template(list(struct), order, backend.dtype, fixed,
-                              small_iter_bits=E.small_iter_bits_for(backend.threshold, backend.dtype))
+                              small_iter_bits=E.small_iter_bits_for(backend.threshold, backend.dtype),
+                              wave_aware=not fixed)
         PLAN_CACHE.put(key, hit)
     plans[okey] = (key, hit)
     return key, hit

@@ -291,7 +291,8 @@ def _same_template(a, b):
 def test_native_planner_matches_python_planner():
     """csrc/plan_template.cpp (qtn_plan_build) restates engine.plan_template_py:
     identical templates on QAOA cones (both cone modes, both dtypes, merging
-    on/off, several K2 thresholds), sliced networks and random circuits."""
+    on/off, several K2 thresholds, wave-aware tiles on/off), sliced networks
+    and random circuits."""
     cases = []
     g = Q.random_regular_graph(16, 3, seed=2)
     c = Q.qaoa_maxcut_circuit(g, Q.QaoaParams.seeded(3, 1))
@@ -307,9 +308,10 @@ def test_native_planner_matches_python_planner():
     for tn, order, fixed in cases:
         ix = [t.indices for t in tn.tensors]
         for dtype in ("complex64", "complex128"):
-            for merge, sib in ((True, 12), (False, 12), (True, 8), (True, 16)):
-                a = E.plan_template_py(ix, order, dtype, fixed, merge=merge, small_iter_bits=sib)
-                b = E.plan_template(ix, order, dtype, fixed, merge=merge, small_iter_bits=sib)
+            for merge, sib, wave in ((True, 12, False), (False, 12, False), (True, 8, False), (True, 16, False),
+                                     (True, 12, True), (True, 8, True)):
+                a = E.plan_template_py(ix, order, dtype, fixed, merge=merge, small_iter_bits=sib, wave_aware=wave)
+                b = E.plan_template(ix, order, dtype, fixed, merge=merge, small_iter_bits=sib, wave_aware=wave)
                 _same_template(a, b)
 
 
@@ -318,3 +320,56 @@ def test_native_planner_errors():
     order = Q.greedy_order(tn)
     with pytest.raises(ValueError, match="order is missing indices"):
         E.plan_template([t.indices for t in tn.tensors], order[:-1], "complex64")
+
+
+def test_pool_incremental_coalescing_matches_full_merge():
+    """_Pool keeps its free list sorted and coalesced incrementally; the
+    allocations (offsets, inherited readers, top) equal those of a pool that
+    re-sorts and re-merges the whole list on every insert."""
+    import random
+    from paper_2210_15874_b200 import engine as E
+
+    class Naive(E._Pool):
+        def _insert(self, st, sz, rd):
+            self.free.append([st, sz, rd])
+            self.free.sort(key=lambda blk: blk[0])
+            merged = []
+            for blk in self.free:
+                if merged and merged[-1][0] + merged[-1][1] == blk[0]:
+                    merged[-1][1] += blk[1]
+                    merged[-1][2] = merged[-1][2] | blk[2]
+                else:
+                    merged.append(blk)
+            self.free = merged
+
+    for seed in range(20):
+        rng = random.Random(seed)
+        a, b = E._Pool(7), Naive(7)
+        live = []
+        for step in range(400):
+            if live and rng.random() < 0.45:
+                off, size = live.pop(rng.randrange(len(live)))
+                a.release(off, size, step)
+                b.release(off, size, step)
+            else:
+                size = 1 << rng.randrange(0, 12)
+                align = E._tensor_align(size)
+                ra, rb = a.alloc(size, align), b.alloc(size, align)
+                assert ra == rb
+                live.append((ra[0], size))
+            assert a.top == b.top and a.free == b.free
+
+
+def test_wave_aware_tiles():
+    """Wave-aware plans shrink a large item's tile (by <= 2 bits, never below
+    the vector minimum) only when that fills the persistent grid's last wave
+    better: w=21 (512 tiles of 2^12 on 444 slots) -> 2^11; w=24 keeps 2^12."""
+    slots = E.WAVE_SLOTS["complex64"]
+    full = [(1 << 24) - 1]
+    assert E._tile_bits(24, full, [3], "complex64", slots)[0] == 12
+    assert E._tile_bits(21, [(1 << 21) - 1], [3], "complex64", slots)[0] == 11
+    assert E._tile_bits(21, [(1 << 21) - 1], [3], "complex64", 0)[0] == 12
+    for w in range(9, 30):
+        L0 = E._tile_bits(w, [(1 << w) - 1], [1], "complex64", 0)[0]
+        L1 = E._tile_bits(w, [(1 << w) - 1], [1], "complex64", slots)[0]
+        assert L0 - 2 <= L1 <= L0 and L1 >= min(w, E.MIN_TILE_BITS["complex64"])
