@@ -194,6 +194,10 @@ int qtn_graph_create_host(const qtn_program_t* prog, const qtn_bucket_t* host_it
 /* Launch the instantiated graph (one call per program execution). */
 int qtn_graph_launch(qtn_graph_t* g, void* stream);
 int qtn_graph_destroy(qtn_graph_t* g);
+/* Kernel mix of a built graph: counts[4] = nodes run by K1 (fused large-item
+ * kernels), K2 (small-item stages), K3 (permutation-aware bucket kernel) and
+ * K4 (expansion-item kernel). */
+int qtn_graph_kinds(const qtn_graph_t* g, int32_t* counts);
 /* Host planning (no device needed): the greedy min-fill (heuristic 0) or
  * min-degree (1) elimination order of a network given as CSR index lists
  * (tensor t holds tensor_idx[tensor_ptr[t] .. tensor_ptr[t+1])); open indices

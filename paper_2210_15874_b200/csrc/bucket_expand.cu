@@ -1,0 +1,338 @@
+// bucket_expand.cu — K4: the expansion-item kernel (one dominant member).
+//
+// Same contraction as the reference's fast_kernel (src/tensor_core.py:148-164)
+// for one program item: out[r] = sum_s prod_i m_i(r, s) over the item's
+// summed bits s (one bucket index, or a merged chain of up to 3).  K4 takes
+// the items whose result is an EXPANSION of one dominant member B: B carries
+// all but |E| <= 4 of the w result bits ("expansion bits" E), every other
+// member is small inside a tile.  K1/K3 stage B's tile slice through shared
+// memory and re-read it once per result (2^k x 2^|E| reads of every staged
+// element); K4 reads B straight into registers instead and keeps it there for
+// all 2^|E| results that share it:
+//
+//   tile   = 8 "thread bits" TB (B's lowest result bits: lanes read B
+//            contiguously) + the expansion bits E; the other result bits H
+//            select the tile (persistent grid over 2^|H| tiles)
+//   F      = per tile, the product of all members except B over the tile's
+//            F bits (the result bits in TB u E that any other member carries)
+//            and s: 2^(|F|+k) entries in shared memory, built from L2
+//   thread = one B coordinate: loads B(s) for the 2^k values of s once, then
+//            out[r(e)] = sum_s B(s) * F[f(e), s] for its 2^|E| results
+//
+// Bytes moved are the algorithmic ones (B once, every result once, the small
+// members from L2); per result the inner loop is 2^k complex FMAs and one
+// 2^k-wide shared-memory read.  Every index map is GF(2)-linear in the bits,
+// so offsets are sums of per-bit strides (6-bit look-up tables for F).
+#include "qtn_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+int qtn_internal_set_error(int code, const char* msg);
+
+namespace qtn_k4 {
+
+constexpr int NT = 256;
+constexpr int TBB = 8;                  // thread bits (log2 NT)
+constexpr int MAXE = 4;                 // expansion bits
+constexpr int MAXKS = 3;                // summed bits
+constexpr int MAXFB = 12;               // F table bits (|F| + k)
+constexpr int MAXM = QTN_MAX_MEMBERS;
+constexpr int MAXH = 32;                // tile-selecting result bits
+
+struct Plan {
+  void* out;
+  const void* mptr[MAXM];
+  int32_t nm, k, nE, nF, nH, iB;
+  int64_t n_tiles;
+  int64_t hs[MAXM + 1][MAXH];           // per member (and out, index nm): stride of tile bit j
+  uint32_t fs[MAXM][MAXFB];             // F entry bit q (s bits first) -> member stride
+  int64_t bs[MAXKS];                    // B strides of the summed bits
+  int64_t btb[TBB];                     // B strides of the thread bits
+  int32_t otb[TBB], ftb[TBB];           // out stride / F index bit of the thread bits
+  int32_t oe[MAXE], fe[MAXE];           // out stride / F index bit of the expansion bits
+  unsigned long long* timing;
+  int32_t item;
+};
+
+template <typename R> struct Cx;
+template <> struct Cx<float> { using T = float2; };
+template <> struct Cx<double> { using T = double2; };
+
+template <typename T>
+__device__ __forceinline__ T cmul(T a, T b) {
+  return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x};
+}
+template <typename T>
+__device__ __forceinline__ void cfma(T& acc, T a, T b) {
+  acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
+  acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
+}
+
+template <typename R, int K, int NE>
+__global__ void __launch_bounds__(NT) k4_kernel(const __grid_constant__ Plan P) {
+  using T = typename Cx<R>::T;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  constexpr int NS = 1 << K;
+  constexpr int NEV = 1 << NE;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* F = reinterpret_cast<T*>(smem_raw);
+  const int nfe = 1 << (P.nF + K);                  // F entries
+  uint32_t* LUT = reinterpret_cast<uint32_t*>(smem_raw + sizeof(T) * nfe);   // [member][lo 64 | hi 64]
+  __shared__ int64_t sbase[MAXM + 1];
+  const int tid = threadIdx.x;
+  const int nm = P.nm;
+  const int nlo = P.nF + K < 6 ? P.nF + K : 6;
+  // F-entry offset tables (tile independent)
+  for (int x = tid; x < nm * 128; x += NT) {
+    const int j = x >> 7, y = x & 63, hi = (x >> 6) & 1;
+    uint32_t o = 0;
+    if (j != P.iB)
+      for (int b = 0; b < 6; ++b) {
+        const int q = hi ? nlo + b : b;
+        if (((y >> b) & 1) && (hi ? q < P.nF + K : b < nlo)) o += P.fs[j][q];
+      }
+    LUT[x] = o;
+  }
+  // this thread's B coordinate
+  int64_t boff = 0;
+  int32_t ob = 0, fb = 0;
+#pragma unroll
+  for (int b = 0; b < TBB; ++b)
+    if ((tid >> b) & 1) {
+      boff += P.btb[b];
+      ob += P.otb[b];
+      fb += P.ftb[b];
+    }
+  int32_t oe[NEV], fe[NEV];
+#pragma unroll
+  for (int e = 0; e < NEV; ++e) {
+    int32_t o = 0, f = 0;
+#pragma unroll
+    for (int b = 0; b < NE; ++b)
+      if ((e >> b) & 1) {
+        o += P.oe[b];
+        f += P.fe[b];
+      }
+    oe[e] = o;
+    fe[e] = (fb + f) << K;
+  }
+  int64_t soffB[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    int64_t o = 0;
+#pragma unroll
+    for (int b = 0; b < K; ++b)
+      if ((s >> b) & 1) o += P.bs[b];
+    soffB[s] = o;
+  }
+  const int64_t G = gridDim.x;
+  int64_t h = blockIdx.x;
+  __syncthreads();
+  if (h >= P.n_tiles) return;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  unsigned long long t_start = 0;
+  if (P.timing && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  const T* Bm = reinterpret_cast<const T*>(P.mptr[P.iB]);
+  T* out = reinterpret_cast<T*>(P.out);
+  for (; h < P.n_tiles; h += G) {
+    if (tid <= nm) {
+      int64_t o = 0;
+      for (int b = 0; b < P.nH; ++b)
+        if ((h >> b) & 1) o += P.hs[tid][b];
+      sbase[tid] = o;
+    }
+    __syncthreads();
+    // B for all s (registers), issued before the F gathers
+    T bv[NS];
+    const T* bp = Bm + sbase[P.iB] + boff;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) bv[s] = __ldg(bp + soffB[s]);
+    // F = product of the other members over (F bits, s)
+    for (int x = tid; x < nfe; x += NT) {
+      T v = {R(1), R(0)};
+      const int lo = x & 63, hi = x >> 6;
+      for (int j = 0; j < nm; ++j) {
+        if (j == P.iB) continue;
+        const T* mp = reinterpret_cast<const T*>(P.mptr[j]);
+        v = cmul(v, __ldg(mp + sbase[j] + LUT[j * 128 + lo] + LUT[j * 128 + 64 + hi]));
+      }
+      F[x] = v;
+    }
+    __syncthreads();
+    T* op = out + sbase[nm] + ob;
+#pragma unroll
+    for (int e = 0; e < NEV; ++e) {
+      const T* fp = F + fe[e];
+      T acc = cmul(bv[0], fp[0]);
+#pragma unroll
+      for (int s = 1; s < NS; ++s) cfma(acc, bv[s], fp[s]);
+      op[oe[e]] = acc;
+    }
+    __syncthreads();
+  }
+  if (P.timing && tid == 0) {
+    unsigned long long t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    atomicMin(&P.timing[2 * P.item], t_start);
+    atomicMax(&P.timing[2 * P.item + 1], t_end);
+  }
+}
+
+template <typename R, int K>
+const void* fn_ne(int ne) {
+  switch (ne) {
+    case 0: return (const void*)k4_kernel<R, K, 0>;
+    case 1: return (const void*)k4_kernel<R, K, 1>;
+    case 2: return (const void*)k4_kernel<R, K, 2>;
+    case 3: return (const void*)k4_kernel<R, K, 3>;
+    default: return (const void*)k4_kernel<R, K, 4>;
+  }
+}
+
+template <typename R>
+const void* fn_of(int k, int ne) {
+  if (k == 1) return fn_ne<R, 1>(ne);
+  if (k == 2) return fn_ne<R, 2>(ne);
+  return fn_ne<R, 3>(ne);
+}
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  return qtn_internal_set_error(code, buf);
+}
+
+int sm_count() {
+  int dev = 0, nsm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
+  return nsm;
+}
+
+// Plan K4 for `d` (QTN_E_UNSUPPORTED when the item is not an expansion of one
+// dominant member); min_e: fewest expansion bits accepted.
+int make_plan(const qtn_bucket_desc_t* d, int min_e, Plan* P, int* smem) {
+  memset(P, 0, sizeof(*P));
+  const int w = d->w, k = d->k, nm = d->n_mem;
+  const size_t esz = d->dtype == QTN_C64 ? 8 : 16;
+  if (d->dtype != QTN_C64 && d->dtype != QTN_C128) return fail(QTN_E_INVALID, "K4: bad dtype");
+  if (k < 1 || k > MAXKS || nm < 1 || nm > MAXM || w < TBB || w > 31)
+    return fail(QTN_E_UNSUPPORTED, "K4: w=%d k=%d n_mem=%d", w, k, nm);
+  // dominant member: most result bits
+  int iB = 0, best = -1;
+  for (int i = 0; i < nm; ++i) {
+    int c = 0;
+    for (int b = 0; b < w; ++b) c += d->mem[i].strides[b] != 0;
+    if (c > best) best = c, iB = i;
+  }
+  const qtn_bmember_t& B = d->mem[iB];
+  int tb[TBB], nt = 0, eb[MAXE], ne = 0;
+  for (int b = 0; b < w; ++b) {
+    if (B.strides[b] == 0) {
+      if (ne == MAXE) return fail(QTN_E_UNSUPPORTED, "K4: more than %d expansion bits", MAXE);
+      eb[ne++] = b;
+    } else if (nt < TBB) {
+      tb[nt++] = b;
+    }
+  }
+  if (nt < TBB) return fail(QTN_E_UNSUPPORTED, "K4: dominant member has %d result bits", best);
+  if (ne < min_e) return fail(QTN_E_UNSUPPORTED, "K4: %d expansion bits", ne);
+  // tile bits T = tb u eb; F bits = T bits any other member carries
+  bool inT[64] = {};
+  for (int i = 0; i < nt; ++i) inT[tb[i]] = true;
+  for (int i = 0; i < ne; ++i) inT[eb[i]] = true;
+  int fbit[64], nf = 0;
+  for (int b = 0; b < w; ++b) {
+    fbit[b] = -1;
+    if (!inT[b]) continue;
+    bool other = false;
+    for (int i = 0; i < nm; ++i)
+      if (i != iB && d->mem[i].strides[b] != 0) other = true;
+    if (other) fbit[b] = nf++;
+  }
+  const int max_fb = d->dtype == QTN_C64 ? MAXFB : MAXFB - 1;
+  if (nf + k > max_fb) return fail(QTN_E_UNSUPPORTED, "K4: F table of %d bits", nf + k);
+  // member element offsets must fit 32 bits inside a tile's F gathers
+  for (int i = 0; i < nm; ++i) {
+    if (!d->mem[i].data) return fail(QTN_E_INVALID, "K4: null member %d", i);
+    int64_t span = 0;
+    for (int b = 0; b < w + k; ++b) span += d->mem[i].strides[b];
+    if (span >= ((int64_t)1 << 31)) return fail(QTN_E_UNSUPPORTED, "K4: member %d spans 2^31 elements", i);
+    P->mptr[i] = d->mem[i].data;
+  }
+  if (!d->out) return fail(QTN_E_INVALID, "K4: null output");
+  P->out = d->out;
+  P->nm = nm;
+  P->k = k;
+  P->nE = ne;
+  P->nF = nf;
+  P->iB = iB;
+  int nh = 0;
+  for (int b = 0; b < w; ++b) {
+    if (inT[b]) continue;
+    for (int i = 0; i < nm; ++i) P->hs[i][nh] = d->mem[i].strides[b];
+    P->hs[nm][nh] = (int64_t)1 << b;
+    ++nh;
+  }
+  P->nH = nh;
+  P->n_tiles = (int64_t)1 << nh;
+  for (int i = 0; i < nm; ++i) {
+    if (i == iB) continue;
+    for (int q = 0; q < k; ++q) P->fs[i][q] = (uint32_t)d->mem[i].strides[w + q];
+    for (int b = 0; b < w; ++b)
+      if (fbit[b] >= 0) P->fs[i][k + fbit[b]] = (uint32_t)d->mem[i].strides[b];
+  }
+  for (int q = 0; q < k; ++q) P->bs[q] = B.strides[w + q];
+  for (int i = 0; i < TBB; ++i) {
+    P->btb[i] = B.strides[tb[i]];
+    P->otb[i] = 1 << tb[i];
+    P->ftb[i] = fbit[tb[i]] >= 0 ? 1 << fbit[tb[i]] : 0;
+  }
+  for (int i = 0; i < ne; ++i) {
+    P->oe[i] = 1 << eb[i];
+    P->fe[i] = fbit[eb[i]] >= 0 ? 1 << fbit[eb[i]] : 0;
+  }
+  *smem = (int)(esz << (nf + k)) + nm * 128 * 4;
+  (void)esz;
+  return QTN_OK;
+}
+
+}  // namespace qtn_k4
+
+size_t qtn_k4_plan_bytes() { return sizeof(qtn_k4::Plan); }
+
+// Program-graph node for one item (qtn_graph_create_host): QTN_E_UNSUPPORTED
+// when the item is not a K4 expansion with at least min_e expansion bits.
+int qtn_k4_node(const qtn_bucket_desc_t* d, int min_e, unsigned long long* timing, int32_t item, void* plan,
+                const void** fn, int* grid, int* smem) {
+  using namespace qtn_k4;
+  Plan* P = reinterpret_cast<Plan*>(plan);
+  int rc = make_plan(d, min_e, P, smem);
+  if (rc) return rc;
+  P->timing = timing;
+  P->item = item;
+  *fn = d->dtype == QTN_C64 ? fn_of<float>(P->k, P->nE) : fn_of<double>(P->k, P->nE);
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, *fn);
+  if (e != cudaSuccess) return fail(QTN_E_CUDA, "cudaFuncGetAttributes: %s", cudaGetErrorString(e));
+  if (*smem > fa.maxDynamicSharedSizeBytes) {
+    e = cudaFuncSetAttribute(*fn, cudaFuncAttributeMaxDynamicSharedMemorySize, *smem);
+    if (e != cudaSuccess) return fail(QTN_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+  }
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, *fn, NT, *smem);
+  if (e != cudaSuccess) return fail(QTN_E_CUDA, "occupancy: %s", cudaGetErrorString(e));
+  if (per_sm < 1) return fail(QTN_E_UNSUPPORTED, "K4 cannot be resident with %d B smem", *smem);
+  *grid = (int)std::min<int64_t>(P->n_tiles, (int64_t)per_sm * sm_count());
+  return QTN_OK;
+}

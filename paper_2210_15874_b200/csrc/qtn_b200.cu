@@ -1003,6 +1003,9 @@ int qtn_internal_set_error(int code, const char* msg) { return set_err(code, "%s
 // K3 (bucket_strided.cu) as a program node: expansion items whose staged
 // members K1 would gather per tile
 size_t qtn_k3_plan_bytes();
+size_t qtn_k4_plan_bytes();
+int qtn_k4_node(const qtn_bucket_desc_t* d, int min_e, unsigned long long* timing, int32_t item, void* plan,
+                const void** fn, int* grid, int* smem);
 int qtn_k3_node(const qtn_bucket_desc_t* d, unsigned long long* timing, int32_t item, void* plan, const void** fn,
                 int* grid, int* smem);
 
@@ -1057,6 +1060,7 @@ void k3_desc(const qtn_program_t* p, const qtn_bucket_t& b, const qtn_member_t* 
 struct qtn_graph {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
+  int32_t kinds[4] = {0, 0, 0, 0};   // nodes run by K1, K2, K3, K4
 };
 
 extern "C" {
@@ -1188,7 +1192,30 @@ int qtn_graph_create_host(const qtn_program_t* p, const qtn_bucket_t* items, con
       qtn_graph_destroy(g);
       return rc;
     }
-    if (nd.kind == QTN_NODE_LARGE && p->arena && have_mems && k3_route(items[nd.first], mems_ptr, p->dtype)) {
+    ++g->kinds[nd.kind == QTN_NODE_LARGE ? 0 : 1];
+    // K4: expansion items of one dominant member (QTN_K4 = fewest expansion
+    // bits routed, 0 = never)
+    static const int k4_min_e = getenv_int("QTN_K4", 1);
+    bool k4 = false;
+    if (nd.kind == QTN_NODE_LARGE && p->arena && have_mems && k4_min_e > 0 && items[nd.first].k >= 1 &&
+        items[nd.first].w >= 12) {
+      qtn_bucket_desc_t d;
+      k3_desc(p, items[nd.first], mems_ptr, &d);
+      std::vector<unsigned char> plan(qtn_k4_plan_bytes());
+      const void* fn = nullptr;
+      int grid = 0, smem = 0;
+      if (qtn_k4_node(&d, k4_min_e, p->timing, nd.first, plan.data(), &fn, &grid, &smem) == QTN_OK) {
+        specs[i].k3plan = std::move(plan);
+        specs[i].fn = fn;
+        specs[i].grid = grid;
+        specs[i].smem = smem;
+        specs[i].args[0] = specs[i].k3plan.data();
+        k4 = true;
+        ++g->kinds[3];
+        --g->kinds[0];
+      }   // else: not an expansion item (K3 / K1 below)
+    }
+    if (!k4 && nd.kind == QTN_NODE_LARGE && p->arena && have_mems && k3_route(items[nd.first], mems_ptr, p->dtype)) {
       qtn_bucket_desc_t d;
       k3_desc(p, items[nd.first], mems_ptr, &d);
       specs[i].k3plan.resize(qtn_k3_plan_bytes());
@@ -1199,6 +1226,8 @@ int qtn_graph_create_host(const qtn_program_t* p, const qtn_bucket_t* items, con
         specs[i].grid = grid;
         specs[i].smem = smem;
         specs[i].args[0] = specs[i].k3plan.data();
+        ++g->kinds[2];
+        --g->kinds[0];
       }   // else: K1 stays (the K3 planner declined this item)
     }
     std::vector<cudaGraphNode_t> deps;
@@ -1258,6 +1287,12 @@ int qtn_graph_launch(qtn_graph_t* g, void* stream) {
   if (!g || !g->exec) return set_err(QTN_E_INVALID, "null graph");
   const cudaError_t e = cudaGraphLaunch(g->exec, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_err(e, "cudaGraphLaunch");
+  return QTN_OK;
+}
+
+int qtn_graph_kinds(const qtn_graph_t* g, int32_t* counts) {
+  if (!g || !counts) return set_err(QTN_E_INVALID, "null argument");
+  for (int i = 0; i < 4; ++i) counts[i] = g->kinds[i];
   return QTN_OK;
 }
 

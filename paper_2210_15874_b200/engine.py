@@ -950,6 +950,14 @@ class Executor:
                 deps.ctypes.data_as(ctypes.c_void_p), ctypes.byref(io) if io is not None else None, ctypes.byref(g)))
         return g
 
+    def kernel_mix(self, io=True):
+        """{'K1', 'K2', 'K3', 'K4'}: graph nodes per kernel family (the
+        end-to-end graph when io, else the kernels-only graph)."""
+        g = self._io_graph() if io else self.graph
+        c = (ctypes.c_int32 * 4)()
+        N.check(N.load().qtn_graph_kinds(g, c))
+        return dict(zip(("K1", "K2", "K3", "K4"), (int(x) for x in c)))
+
     @property
     def graph(self):
         """The program graph (kernels only), built on first use."""

@@ -14,7 +14,7 @@ from paper_2210_15874_b200 import engine as E  # noqa: E402
 dtype = sys.argv[1] if len(sys.argv) > 1 else "complex64"
 g, params, lc, order = bench.build_workload()
 tn = lc.network
-t = E.plan_template([x.indices for x in tn.tensors], order, dtype)
+t = E.plan_template([x.indices for x in tn.tensors], order, dtype, wave_aware=True)
 prog = E.Program([E.Instance(t)], dtype)
 ex = E.Executor(prog, timing=True)
 raw = np.concatenate([np.asarray(x.data).ravel() for x in tn.tensors])

@@ -19,7 +19,7 @@ minw = int(sys.argv[2]) if len(sys.argv) > 2 else 12
 only = int(sys.argv[3]) if len(sys.argv) > 3 else -1   # run one item (for ncu)
 g, params, lc, order = bench.build_workload()
 tn = lc.network
-t = E.plan_template([x.indices for x in tn.tensors], order, dtype)
+t = E.plan_template([x.indices for x in tn.tensors], order, dtype, wave_aware=True)
 prog = E.Program([E.Instance(t)], dtype)
 ex = E.Executor(prog, timing=False)
 ex.arena.copy_(torch.randn(prog.arena_elems, dtype=ex.tdt, device="cuda") * 0.5)

@@ -263,3 +263,39 @@ def test_streamed_batches_shared_arena():
             zz[unit.cone] += streamed[u]
         for z, r in zip(zz, recs):
             assert abs(z.real - r["zz"][0]) <= tol
+
+
+_K4_CHECK = _K3_ROUTE_CHECK.replace("print(max(errs))", r"""
+from paper_2210_15874_b200 import engine as E
+mix = {{}}
+for dt in ("complex64", "complex128"):
+    t = E.plan_template([x.indices for x in lc.network.tensors], Q.greedy_order(lc.network), dt, wave_aware=True)
+    ex = E.Executor(E.Program([E.Instance(t)], dt))
+    mix[dt] = ex.kernel_mix()
+    raw = np.concatenate([np.asarray(x.data).ravel() for x in lc.network.tensors])
+    v = ex.run([raw])[0]
+    errs.append(abs(v.real - (-0.0017371891851279)) / (1e-5 if dt == "complex64" else 1e-10))
+print(mix["complex64"]["K4"], mix["complex128"]["K4"])
+print(max(errs))""")
+
+
+@pytest.mark.parametrize("min_e", ["1", "3", "0"])
+def test_program_items_through_k4(min_e):
+    """Expansion items routed to K4 (QTN_K4 = fewest expansion bits, 0 =
+    off): golden networks and the cfg-2 cone at both dtypes, and the cfg-2
+    program really contains K4 nodes unless K4 is off."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = _K4_CHECK.format(root=root, tests=os.path.join(root, "tests"))
+    env = dict(os.environ, QTN_K4=min_e)
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = out.stdout.strip().splitlines()
+    assert float(lines[-1]) <= 1.0
+    n64, n128 = (int(x) for x in lines[-2].split())
+    if min_e == "0":
+        assert n64 == 0 and n128 == 0
+    else:
+        assert n64 > 0 and n128 > 0
