@@ -13,9 +13,13 @@
 //   tile   = 8 "thread bits" TB (B's lowest result bits: lanes read B
 //            contiguously) + the expansion bits E; the other result bits H
 //            select the tile (persistent grid over 2^|H| tiles)
-//   F      = per tile, the product of all members except B over the tile's
-//            F bits (the result bits in TB u E that any other member carries)
-//            and s: 2^(|F|+k) entries in shared memory, built from L2
+//   F      = the product of all members except B over the tile's F bits (the
+//            result bits in TB u E that any other member carries) and s:
+//            2^(|F|+k) entries in shared memory, gathered from L2.  F depends
+//            on the tile only through the H bits other members carry; those
+//            are the HIGH bits of the tile id and every block walks a
+//            contiguous run of tile ids, so F is rebuilt only when they change
+//            (typically once per block)
 //   thread = one B coordinate: loads B(s) for the 2^k values of s once, then
 //            out[r(e)] = sum_s B(s) * F[f(e), s] for its 2^|E| results
 //
@@ -50,6 +54,7 @@ struct Plan {
   void* out;
   const void* mptr[MAXM];
   int32_t nm, k, nE, nF, nH, iB;
+  int32_t nHF;                          // tile-id bits other members carry (the highest nHF of nH)
   int64_t n_tiles;
   int64_t hs[MAXM + 1][MAXH];           // per member (and out, index nm): stride of tile bit j
   uint32_t fs[MAXM][MAXFB];             // F entry bit q (s bits first) -> member stride
@@ -132,41 +137,56 @@ __global__ void __launch_bounds__(NT) k4_kernel(const __grid_constant__ Plan P) 
       if ((s >> b) & 1) o += P.bs[b];
     soffB[s] = o;
   }
-  const int64_t G = gridDim.x;
-  int64_t h = blockIdx.x;
+  // contiguous run of tile ids per block
+  const int64_t per = (P.n_tiles + gridDim.x - 1) / gridDim.x;
+  int64_t h = (int64_t)blockIdx.x * per;
+  const int64_t h_end = h + per < P.n_tiles ? h + per : P.n_tiles;
   __syncthreads();
-  if (h >= P.n_tiles) return;
+  if (h >= h_end) return;
   asm volatile("griddepcontrol.wait;" ::: "memory");
   unsigned long long t_start = 0;
   if (P.timing && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   const T* Bm = reinterpret_cast<const T*>(P.mptr[P.iB]);
   T* out = reinterpret_cast<T*>(P.out);
-  for (; h < P.n_tiles; h += G) {
-    if (tid <= nm) {
-      int64_t o = 0;
-      for (int b = 0; b < P.nH; ++b)
-        if ((h >> b) & 1) o += P.hs[tid][b];
-      sbase[tid] = o;
-    }
-    __syncthreads();
-    // B for all s (registers), issued before the F gathers
+  const int shf = P.nH - P.nHF;
+  int64_t fkey = -1;
+  for (; h < h_end; ++h) {
+    // B and output bases of this tile (every thread: no barrier)
+    int64_t bb = 0, obase = 0;
+    for (int b = 0; b < P.nH; ++b)
+      if ((h >> b) & 1) {
+        bb += P.hs[P.iB][b];
+        obase += P.hs[nm][b];
+      }
+    // B for all s (registers), issued before a possible F rebuild
     T bv[NS];
-    const T* bp = Bm + sbase[P.iB] + boff;
+    const T* bp = Bm + bb + boff;
 #pragma unroll
     for (int s = 0; s < NS; ++s) bv[s] = __ldg(bp + soffB[s]);
-    // F = product of the other members over (F bits, s)
-    for (int x = tid; x < nfe; x += NT) {
-      T v = {R(1), R(0)};
-      const int lo = x & 63, hi = x >> 6;
-      for (int j = 0; j < nm; ++j) {
-        if (j == P.iB) continue;
-        const T* mp = reinterpret_cast<const T*>(P.mptr[j]);
-        v = cmul(v, __ldg(mp + sbase[j] + LUT[j * 128 + lo] + LUT[j * 128 + 64 + hi]));
+    if ((h >> shf) != fkey) {
+      fkey = h >> shf;
+      __syncthreads();   // previous F no longer read
+      if (tid < nm) {
+        int64_t o = 0;
+        for (int b = shf; b < P.nH; ++b)
+          if ((h >> b) & 1) o += P.hs[tid][b];
+        sbase[tid] = o;
       }
-      F[x] = v;
+      __syncthreads();
+      // F = product of the other members over (F bits, s)
+      for (int x = tid; x < nfe; x += NT) {
+        T v = {R(1), R(0)};
+        const int lo = x & 63, hi = x >> 6;
+        for (int j = 0; j < nm; ++j) {
+          if (j == P.iB) continue;
+          const T* mp = reinterpret_cast<const T*>(P.mptr[j]);
+          v = cmul(v, __ldg(mp + sbase[j] + LUT[j * 128 + lo] + LUT[j * 128 + 64 + hi]));
+        }
+        F[x] = v;
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    T* op = out + sbase[nm] + ob;
+    T* op = out + obase + ob;
 #pragma unroll
     for (int e = 0; e < NEV; ++e) {
       const T* fp = F + fe[e];
@@ -175,7 +195,6 @@ __global__ void __launch_bounds__(NT) k4_kernel(const __grid_constant__ Plan P) 
       for (int s = 1; s < NS; ++s) cfma(acc, bv[s], fp[s]);
       op[oe[e]] = acc;
     }
-    __syncthreads();
   }
   if (P.timing && tid == 0) {
     unsigned long long t_end;
@@ -277,14 +296,21 @@ int make_plan(const qtn_bucket_desc_t* d, int min_e, Plan* P, int* smem) {
   P->nE = ne;
   P->nF = nf;
   P->iB = iB;
-  int nh = 0;
-  for (int b = 0; b < w; ++b) {
-    if (inT[b]) continue;
-    for (int i = 0; i < nm; ++i) P->hs[i][nh] = d->mem[i].strides[b];
-    P->hs[nm][nh] = (int64_t)1 << b;
-    ++nh;
-  }
+  int nh = 0, nhf = 0;
+  for (int pass = 0; pass < 2; ++pass)
+    for (int b = 0; b < w; ++b) {
+      if (inT[b]) continue;
+      bool other = false;
+      for (int i = 0; i < nm; ++i)
+        if (i != iB && d->mem[i].strides[b] != 0) other = true;
+      if (other != (pass == 1)) continue;
+      for (int i = 0; i < nm; ++i) P->hs[i][nh] = d->mem[i].strides[b];
+      P->hs[nm][nh] = (int64_t)1 << b;
+      ++nh;
+      nhf += other;
+    }
   P->nH = nh;
+  P->nHF = nhf;
   P->n_tiles = (int64_t)1 << nh;
   for (int i = 0; i < nm; ++i) {
     if (i == iB) continue;
