@@ -237,6 +237,7 @@ def run_ours(args):
     tmpl = E.plan_template([t.indices for t in tn.tensors], order, dtype, wave_aware=True)  # as contract_network
     prog = E.Program([E.Instance(tmpl)], dtype)
     ex = E.Executor(prog, device=local, timing=False)
+    kernel_mix = ex.kernel_mix(io=False)   # graph nodes per kernel family (K1/K2/K3/K4)
     raw = np.concatenate([np.asarray(t.data).ravel() for t in tn.tensors])
     ex.stage_inputs([raw])
     stream = torch.cuda.current_stream()
@@ -316,10 +317,17 @@ def run_ours(args):
         acc /= nrep
         ibytes = np.zeros(tmpl.n_items)
         np.add.at(ibytes, tmpl.ref_item, tmpl.ref_elems * E.ELEM_BYTES[dtype])
+        # kernel family per item from the built graph (K4 / K3 routing happens there)
+        fam = ext.node_kernels(io=False)
+        node_of_gid = {}
+        for ni, nd in enumerate(prog.nodes):
+            for gid in range(int(nd["first"]), int(nd["first"]) + int(nd["count"])):
+                node_of_gid[gid] = ni
+        names = {"K1": "K1 large_kernel", "K2": "K2 small_kernel", "K3": "K3 k3v2_kernel", "K4": "K4 k4_kernel"}
         for it in np.argsort(-acc)[:3]:
+            kf = fam[node_of_gid[int(prog.bucket_gid[0][it])]]
             items.append({"item": int(it), "w": int(tmpl.w[it]), "k": int(tmpl.k[it]),
-                          "kernel": "K2 small_kernel" if int(tmpl.variant[it]) == E.VARIANT_SMALL
-                          else f"K1 large_kernel variant {int(tmpl.variant[it]):#x}",
+                          "kernel": names[kf] + (f" variant {int(tmpl.variant[it]):#x}" if kf == "K1" else ""),
                           "us": round(float(acc[it]) / 1e3, 1), "alg_MB": round(float(ibytes[it]) / 1e6, 1),
                           "alg_GBps": round(float(ibytes[it]) / max(float(acc[it]), 1.0), 1)})
         del ext
@@ -371,7 +379,9 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(args.dtype), "peak_source": peak_src,
                      "kernel": "one program graph per step: K2 small_kernel stages + K1 large_kernel variants "
-                               "(one cudaGraphLaunch); achieved = algorithmic bytes (SURVEY 8(d)) / device time",
+                               "+ K4 k4_kernel expansion items (one cudaGraphLaunch); achieved = algorithmic "
+                               "bytes (SURVEY 8(d)) / device time",
+                     "kernel_mix": kernel_mix,
                      "achieved_executed": prog.executed_bytes() / (t_kern / args.steps) / 1e9,
                      "top_items_live": items},
         "cpu_baseline": cpu,

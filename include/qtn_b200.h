@@ -198,6 +198,8 @@ int qtn_graph_destroy(qtn_graph_t* g);
  * kernels), K2 (small-item stages), K3 (permutation-aware bucket kernel) and
  * K4 (expansion-item kernel). */
 int qtn_graph_kinds(const qtn_graph_t* g, int32_t* counts);
+/* Per node (n = the graph's node count): 0 K1, 1 K2, 2 K3, 3 K4. */
+int qtn_graph_node_kinds(const qtn_graph_t* g, int32_t* kinds, int32_t n);
 /* Host planning (no device needed): the greedy min-fill (heuristic 0) or
  * min-degree (1) elimination order of a network given as CSR index lists
  * (tensor t holds tensor_idx[tensor_ptr[t] .. tensor_ptr[t+1])); open indices

@@ -42,6 +42,7 @@ EXPORTS = (
     "qtn_graph_create_io",
     "qtn_graph_create_host",
     "qtn_graph_kinds",
+    "qtn_graph_node_kinds",
     "qtn_graph_launch",
     "qtn_graph_destroy",
     "qtn_permute",
@@ -143,6 +144,8 @@ def load(path: str = LIB_PATH):
     lib.qtn_node_launch.argtypes = [ctypes.POINTER(ProgramC), vp, i32, vp]
     lib.qtn_graph_create.restype = ctypes.c_int
     lib.qtn_graph_create.argtypes = [ctypes.POINTER(ProgramC), vp, i32, vp, ctypes.POINTER(ctypes.c_void_p)]
+    lib.qtn_graph_node_kinds.restype = ctypes.c_int
+    lib.qtn_graph_node_kinds.argtypes = [vp, vp, i32]
     lib.qtn_graph_kinds.restype = ctypes.c_int
     lib.qtn_graph_kinds.argtypes = [vp, vp]
     lib.qtn_graph_create_host.restype = ctypes.c_int

@@ -1061,6 +1061,7 @@ struct qtn_graph {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   int32_t kinds[4] = {0, 0, 0, 0};   // nodes run by K1, K2, K3, K4
+  std::vector<int32_t> node_kind;    // per node: 0 K1, 1 K2, 2 K3, 3 K4
 };
 
 extern "C" {
@@ -1193,6 +1194,7 @@ int qtn_graph_create_host(const qtn_program_t* p, const qtn_bucket_t* items, con
       return rc;
     }
     ++g->kinds[nd.kind == QTN_NODE_LARGE ? 0 : 1];
+    g->node_kind.push_back(nd.kind == QTN_NODE_LARGE ? 0 : 1);
     // K4: expansion items of one dominant member (QTN_K4 = fewest expansion
     // bits routed, 0 = never)
     static const int k4_min_e = getenv_int("QTN_K4", 1);
@@ -1213,6 +1215,7 @@ int qtn_graph_create_host(const qtn_program_t* p, const qtn_bucket_t* items, con
         k4 = true;
         ++g->kinds[3];
         --g->kinds[0];
+        g->node_kind.back() = 3;
       }   // else: not an expansion item (K3 / K1 below)
     }
     if (!k4 && nd.kind == QTN_NODE_LARGE && p->arena && have_mems && k3_route(items[nd.first], mems_ptr, p->dtype)) {
@@ -1228,6 +1231,7 @@ int qtn_graph_create_host(const qtn_program_t* p, const qtn_bucket_t* items, con
         specs[i].args[0] = specs[i].k3plan.data();
         ++g->kinds[2];
         --g->kinds[0];
+        g->node_kind.back() = 2;
       }   // else: K1 stays (the K3 planner declined this item)
     }
     std::vector<cudaGraphNode_t> deps;
@@ -1293,6 +1297,14 @@ int qtn_graph_launch(qtn_graph_t* g, void* stream) {
 int qtn_graph_kinds(const qtn_graph_t* g, int32_t* counts) {
   if (!g || !counts) return set_err(QTN_E_INVALID, "null argument");
   for (int i = 0; i < 4; ++i) counts[i] = g->kinds[i];
+  return QTN_OK;
+}
+
+int qtn_graph_node_kinds(const qtn_graph_t* g, int32_t* kinds, int32_t n) {
+  if (!g || (n > 0 && !kinds)) return set_err(QTN_E_INVALID, "null argument");
+  if (n != (int32_t)g->node_kind.size()) return set_err(QTN_E_INVALID, "graph has %d nodes, not %d",
+                                                        (int)g->node_kind.size(), n);
+  for (int i = 0; i < n; ++i) kinds[i] = g->node_kind[i];
   return QTN_OK;
 }
 

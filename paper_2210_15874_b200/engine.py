@@ -958,6 +958,14 @@ class Executor:
         N.check(N.load().qtn_graph_kinds(g, c))
         return dict(zip(("K1", "K2", "K3", "K4"), (int(x) for x in c)))
 
+    def node_kernels(self, io=True):
+        """Per graph node, the kernel family that runs it ('K1'..'K4')."""
+        g = self._io_graph() if io else self.graph
+        n = int(self.prog.n_nodes)
+        c = (ctypes.c_int32 * max(n, 1))()
+        N.check(N.load().qtn_graph_node_kinds(g, c, n))
+        return [("K1", "K2", "K3", "K4")[c[i]] for i in range(n)]
+
     @property
     def graph(self):
         """The program graph (kernels only), built on first use."""

@@ -1,7 +1,8 @@
 """Per-kernel table of one cfg-2 program step from an ncu launch list
 (`ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
 --csv --log-file ... python bench.py --steps 1 --warmup 1`): the first
-complex64 program launch (K2 small_kernel stages + K1 large_kernel items),
+complex64 program launch (K2 small_kernel stages, K1 large_kernel items, K4
+k4_kernel expansion items),
 durations and DRAM bytes per kernel, cold-cache and serialised by ncu.
 
 usage: python scripts/launch_summary.py nodes.csv [graph.csv] > profiles/<name>.md"""
@@ -32,15 +33,16 @@ def rows(path):
 
 
 def short(name):
-    m = re.search(r"(large_kernel|small_kernel)<([^>]*)>", name)
+    m = re.search(r"(large_kernel_c64|large_kernel_c128|large_kernel|small_kernel|k4_kernel|k3v2_kernel)<([^>]*)>", name)
     return f"{m.group(1)}<{m.group(2).replace('(int)', '')}>" if m else name[:60]
 
 
 def main():
     ks = rows(sys.argv[1])
-    ours = [k for k in ks if ("large_kernel<float" in k["name"] or "small_kernel<float" in k["name"])]
-    # the first program launch: 27 kernels (the node count printed by bench.py)
-    n = int(sys.argv[3]) if len(sys.argv) > 3 else 27
+    fam = ("large_kernel_c64<", "large_kernel<float", "small_kernel<float", "k4_kernel<float", "k3v2_kernel<float")
+    ours = [k for k in ks if any(f in k["name"] for f in fam)]
+    # the first program launch: its node count (bench.py config.program.nodes)
+    n = int(sys.argv[3]) if len(sys.argv) > 3 else 21
     step = ours[:n]
     tot_t = sum(k["gpu__time_duration.sum"] for k in step)
     tot_b = sum(k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"] for k in step)

@@ -360,10 +360,12 @@ def test_pool_incremental_coalescing_matches_full_merge():
             assert a.top == b.top and a.free == b.free
 
 
-def test_wave_aware_tiles():
+def test_wave_aware_tiles(monkeypatch):
     """Wave-aware plans shrink a large item's tile (by <= 2 bits, never below
     the vector minimum) only when that fills the persistent grid's last wave
-    better: w=21 (512 tiles of 2^12 on 444 slots) -> 2^11; w=24 keeps 2^12."""
+    better: w=21 (512 tiles of 2^12 on 444 slots) -> 2^11 at a per-tile cost
+    of 1024 results; w=24 keeps 2^12."""
+    monkeypatch.setattr(E, "WAVE_OV_ELEMS", 1024)
     slots = E.WAVE_SLOTS["complex64"]
     full = [(1 << 24) - 1]
     assert E._tile_bits(24, full, [3], "complex64", slots)[0] == 12
