@@ -84,6 +84,11 @@ VEC = {"complex64": 2, "complex128": 1}
 # 0.286 -> 0.267 s.  QTN_* environment overrides are for A/B sweeps.
 HOP_S = float(os.environ.get("QTN_HOP_S", 8.0e-6))        # K1 graph node
 HOP_K2_S = float(os.environ.get("QTN_HOP_K2_S", 0.8e-6))   # item inside a K2 stage
+# K1 hop in wave-aware plans (one contraction per graph, nothing to overlap a
+# hop with): measured end to end, c64 5 us (cfg-2 0.2516 -> 0.2478 ms), c128
+# keeps 8 us (5 us was 1.4 % slower)
+HOP_SINGLE_S = {"complex64": float(os.environ.get("QTN_HOP_SINGLE_C64_S", 5.0e-6)),
+                "complex128": float(os.environ.get("QTN_HOP_SINGLE_C128_S", 8.0e-6))}
 BW_BPS = float(os.environ.get("QTN_BW_BPS", 5.5e12))
 _TERMS_SCALE = float(os.environ.get("QTN_TERMS_SCALE", 1.0))
 CHEAP_MEMBER_W = float(os.environ.get("QTN_CHEAP_W", 1.0))   # per-result weight of uniform/invariant members
@@ -279,7 +284,7 @@ def _cost_of(it, dtype, small_iter_bits=None, slots=0):
         n_cheap = sum(1 for c in cls if c in (CLS_UNIFORM, CLS_INVARIANT))
         nm_eff = max(1.0, (len(cls) - n_cheap) + CHEAP_MEMBER_W * n_cheap)
     return _item_cost(len(it["R"]), len(it["X"]), L, [1 << len(s2) for _, _, s2 in it["members"]], dtype,
-                      nm_eff=nm_eff)
+                      hop=HOP_SINGLE_S[dtype] if slots else HOP_S, nm_eff=nm_eff)
 
 
 def small_iter_bits_for(threshold, dtype="complex64"):
@@ -297,7 +302,8 @@ def _plan_params(dtype, merge, sib, wave_aware=False):
         elem_bytes=ELEM_BYTES[dtype], tile_bits=TILE_BITS[dtype], small_tile_bits=SMALL_TILE_BITS[dtype],
         min_tile_bits=MIN_TILE_BITS[dtype], kmax=KMAX, max_members=N.MAX_MEMBERS, vec=VEC[dtype], nt=NT,
         small_iter_bits=sib, merge=1 if merge else 0, resident_blocks=RESIDENT_BLOCKS[dtype],
-        smem_budget=SMEM_BUDGET, hop_s=HOP_S, hop_k2_s=HOP_K2_S, bw_bps=BW_BPS,
+        smem_budget=SMEM_BUDGET, hop_s=HOP_SINGLE_S[dtype] if wave_aware else HOP_S, hop_k2_s=HOP_K2_S,
+        bw_bps=BW_BPS,
         block_terms_ps=BLOCK_TERMS_PS[dtype], small_load_s=SMALL_LOAD_S, cheap_member_w=CHEAP_MEMBER_W,
         kmax_large=KMAX_LARGE[dtype], wave_slots=WAVE_SLOTS[dtype] if wave_aware else 0,
         wave_ov_elems=WAVE_OV_ELEMS)
