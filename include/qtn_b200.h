@@ -297,6 +297,16 @@ int qtn_bucket(const qtn_bucket_desc_t* desc, void* stream);
  * per-tile product table, [6] product-table bits. */
 int qtn_bucket_plan(const qtn_bucket_desc_t* desc, int32_t* info);
 
+/* ---- K4: an expansion bucket (one dominant member) ----
+ * Same contraction as qtn_bucket for a descriptor whose dominant member (the
+ * one with the most result bits) lacks between min_e (>= 0) and 4 result bits
+ * ("expansion bits"), k in 1..3, 8 <= w <= 31, the other members' bits inside
+ * the K4 tile <= 12 (c64) / 11 (c128) with the summed bits.  The dominant
+ * member is read once into registers, the others through a per-tile product
+ * table (csrc/bucket_expand.cu).  Program graphs route their expansion items
+ * here (QTN_K4).  QTN_E_UNSUPPORTED when the bucket is not such an expansion. */
+int qtn_bucket_expand(const qtn_bucket_desc_t* desc, int32_t min_e, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

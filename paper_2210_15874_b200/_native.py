@@ -42,6 +42,7 @@ EXPORTS = (
     "qtn_graph_create_io",
     "qtn_graph_create_host",
     "qtn_graph_kinds",
+    "qtn_bucket_expand",
     "qtn_graph_node_kinds",
     "qtn_graph_launch",
     "qtn_graph_destroy",
@@ -146,6 +147,8 @@ def load(path: str = LIB_PATH):
     lib.qtn_graph_create.argtypes = [ctypes.POINTER(ProgramC), vp, i32, vp, ctypes.POINTER(ctypes.c_void_p)]
     lib.qtn_graph_node_kinds.restype = ctypes.c_int
     lib.qtn_graph_node_kinds.argtypes = [vp, vp, i32]
+    lib.qtn_bucket_expand.restype = ctypes.c_int
+    lib.qtn_bucket_expand.argtypes = [ctypes.POINTER(BucketDescC), i32, vp]
     lib.qtn_graph_kinds.restype = ctypes.c_int
     lib.qtn_graph_kinds.argtypes = [vp, vp]
     lib.qtn_graph_create_host.restype = ctypes.c_int
@@ -254,6 +257,13 @@ def bucket_plan(desc):
 def bucket_launch(desc, stream):
     lib = require_device()
     check(lib.qtn_bucket(ctypes.byref(desc), ctypes.c_void_p(stream)))
+
+
+def bucket_expand_launch(desc, stream, min_e=0):
+    """K4 on one expansion bucket (QTN_E_UNSUPPORTED -> NativeError when the
+    descriptor is not an expansion of one dominant member)."""
+    lib = require_device()
+    check(lib.qtn_bucket_expand(ctypes.byref(desc), int(min_e), ctypes.c_void_p(stream)))
 
 
 def plan_build(index_lists, order, fixed, params):

@@ -362,3 +362,17 @@ int qtn_k4_node(const qtn_bucket_desc_t* d, int min_e, unsigned long long* timin
   *grid = (int)std::min<int64_t>(P->n_tiles, (int64_t)per_sm * sm_count());
   return QTN_OK;
 }
+
+extern "C" int qtn_bucket_expand(const qtn_bucket_desc_t* d, int32_t min_e, void* stream) {
+  using namespace qtn_k4;
+  if (!d) return fail(QTN_E_INVALID, "null descriptor");
+  static thread_local Plan P;
+  const void* fn = nullptr;
+  int grid = 0, smem = 0;
+  int rc = qtn_k4_node(d, min_e, nullptr, 0, &P, &fn, &grid, &smem);
+  if (rc) return rc;
+  void* args[] = {&P};
+  const cudaError_t e = cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(NT), args, smem, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(QTN_E_CUDA, "K4 launch: %s", cudaGetErrorString(e));
+  return QTN_OK;
+}
