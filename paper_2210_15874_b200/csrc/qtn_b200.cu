@@ -1206,7 +1206,8 @@ int qtn_graph_create_host(const qtn_program_t* p, const qtn_bucket_t* items, con
       std::vector<unsigned char> plan(qtn_k4_plan_bytes());
       const void* fn = nullptr;
       int grid = 0, smem = 0;
-      if (qtn_k4_node(&d, k4_min_e, p->timing, nd.first, plan.data(), &fn, &grid, &smem) == QTN_OK) {
+      static const int k4_all = getenv_int("QTN_K4_ALL", 0);   // A/B: non-expansion items too
+      if (qtn_k4_node(&d, k4_all ? 0 : k4_min_e, p->timing, nd.first, plan.data(), &fn, &grid, &smem) == QTN_OK) {
         specs[i].k3plan = std::move(plan);
         specs[i].fn = fn;
         specs[i].grid = grid;

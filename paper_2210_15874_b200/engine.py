@@ -942,6 +942,7 @@ class Executor:
             self.done = torch.cuda.Event()
         self._graph = None
         self.graph_io = None
+        self._staged = None   # raw parts the pinned image holds (submit)
 
     def _create_graph(self, io):
         nodes = np.ascontiguousarray(self.prog.nodes)
@@ -994,6 +995,7 @@ class Executor:
         (complex128, each tensor C-order in its own index order).  Gathered
         into canonical layout (and narrowed) straight into the pinned staging
         buffer, then one H2D copy; alignment padding is never read."""
+        self._staged = None
         view = self.img_pinned.numpy()
         parts = self.prog.img_src_parts
         if len(parts) == 1:
@@ -1054,12 +1056,20 @@ class Executor:
         pinned image must not be restaged before collect()."""
         torch = self.torch
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        view = self.img_pinned.numpy()
-        parts = self.prog.img_src_parts
-        if len(parts) == 1:
-            view[self.prog.img_dst] = raw_parts[0][parts[0]]
-        elif parts:
-            view[self.prog.img_dst] = np.concatenate([raw[p_] for raw, p_ in zip(raw_parts, parts)])
+        # the pinned image already holds these inputs when the parts are the
+        # very same read-only arrays as last time (immutable Tensors'
+        # concatenation, ordering._NetworkInputs): only the upload repeats
+        same = (self._staged is not None and len(self._staged) == len(raw_parts) and
+                all(a is b and not a.flags.writeable for a, b in zip(self._staged, raw_parts)))
+        if not same:
+            self._staged = None
+            view = self.img_pinned.numpy()
+            parts = self.prog.img_src_parts
+            if len(parts) == 1:
+                view[self.prog.img_dst] = raw_parts[0][parts[0]]
+            elif parts:
+                view[self.prog.img_dst] = np.concatenate([raw[p_] for raw, p_ in zip(raw_parts, parts)])
+            self._staged = list(raw_parts)
         if self.timing is not None:
             self.timing.copy_(self.timing_init, non_blocking=True)
         N.check(N.load().qtn_graph_launch(self._io_graph(), ctypes.c_void_p(s.cuda_stream)))

@@ -250,14 +250,23 @@ class _NetworkInputs:
         self.d = OrderedDict()
         self.lock = threading.Lock()
 
+    @staticmethod
+    def _same(snap, ts):
+        # Tensor has identity equality, so list == list is an element-wise
+        # identity check in C (~1 us for cfg-2's 564 tensors)
+        try:
+            return snap == (ts if isinstance(ts, list) else list(ts))
+        except Exception:
+            return len(snap) == len(ts) and all(map(operator.is_, snap, ts))
+
     def get(self, tn):
         ts = tn.tensors
         with self.lock:
             hit = self.d.get(id(tn))
-            if hit is not None and hit[0] is tn and len(hit[1]) == len(ts) and all(map(operator.is_, hit[1], ts)):
+            if hit is not None and hit[0] is tn and len(hit[1]) == len(ts) and self._same(hit[1], ts):
                 self.d.move_to_end(id(tn))
                 return hit[2], hit[3], hit[4]
-        snap = tuple(ts)
+        snap = list(ts)
         struct = tuple(t.indices for t in snap)
         parts = [t.data.ravel() for t in snap]
         raw = np.concatenate(parts) if parts else np.zeros(0, np.complex128)
@@ -286,9 +295,17 @@ def _template(tn, order, backend, fixed=()):
 
 
 def _template_from(struct, plans, order, backend, fixed=()):
+    # repeated calls with an equal order (list == list: a C-level compare)
+    # skip hashing the order tuple
+    last = plans.get("_last")
+    if (last is not None and last[1] == fixed and last[2] == backend.dtype and last[3] == backend.threshold
+            and isinstance(order, list) and last[0] == order):
+        return last[4]
     okey = (tuple(order), tuple(fixed), backend.dtype, backend.threshold)
     got = plans.get(okey)
     if got is not None:
+        if isinstance(order, list):
+            plans["_last"] = (list(order), fixed, backend.dtype, backend.threshold, got)
         return got
     key = ("tmpl", struct) + okey
     hit = PLAN_CACHE.get(key)
@@ -300,6 +317,8 @@ def _template_from(struct, plans, order, backend, fixed=()):
                               wave_aware=not fixed)
         PLAN_CACHE.put(key, hit)
     plans[okey] = (key, hit)
+    if isinstance(order, list):
+        plans["_last"] = (list(order), fixed, backend.dtype, backend.threshold, (key, hit))
     return key, hit
 
 
@@ -364,7 +383,7 @@ def contract_network(tn: TensorNetwork, order, backend: Backend = None, mem_cap:
     struct, raw, plans = NETWORK_INPUTS.get(tn)
     key, tmpl = _template_from(struct, plans, order, backend)   # raises for indices missing from the order
     _check_cap(tmpl, backend, mem_cap)
-    xkey = ("exec", tuple(order), backend.dtype, backend.threshold, backend.device, backend.profile)
+    xkey = ("exec", id(tmpl), backend.device, backend.profile)   # tmpl is held by `plans`
     got = plans.get(xkey)
     if got is None:
         got = plans[xkey] = _executor(key, lambda: E.Program([E.Instance(tmpl)], backend.dtype), backend, 1)
