@@ -944,7 +944,7 @@ class Executor:
         self.graph_io = None
         self._staged = None   # raw parts the pinned image holds (submit)
 
-    def _create_graph(self, io):
+    def _create_graph(self, io, prog_c=None):
         nodes = np.ascontiguousarray(self.prog.nodes)
         deps = np.ascontiguousarray(self.prog.node_deps)
         items = np.ascontiguousarray(self.prog.buckets)
@@ -952,7 +952,8 @@ class Executor:
         g = ctypes.c_void_p()
         with self.torch.cuda.device(self.device):
             N.check(N.load().qtn_graph_create_host(
-                ctypes.byref(self.c), items.ctypes.data_as(ctypes.c_void_p), mems.ctypes.data_as(ctypes.c_void_p),
+                ctypes.byref(prog_c if prog_c is not None else self.c), items.ctypes.data_as(ctypes.c_void_p),
+                mems.ctypes.data_as(ctypes.c_void_p),
                 len(mems), nodes.ctypes.data_as(ctypes.c_void_p), self.prog.n_nodes,
                 deps.ctypes.data_as(ctypes.c_void_p), ctypes.byref(io) if io is not None else None, ctypes.byref(g)))
         return g
@@ -1037,11 +1038,14 @@ class Executor:
         g = self.graph_io
         if g is None:
             esz = self.arena.element_size()
+            # the finalisers write the result slots straight into the pinned
+            # (device-mapped) host buffer: no download node after the last kernel
+            c_io = N.ProgramC.from_buffer_copy(self.c)
+            c_io.results = self.results_host.data_ptr()
+            self.c_io = c_io
             io = N.GraphIOC(h2d_src=self.img_pinned.data_ptr(), h2d_dst=self.arena.data_ptr(),
-                            h2d_bytes=int(self.prog.n_input_elems) * esz,
-                            d2h_src=self.results.data_ptr(), d2h_dst=self.results_host.data_ptr(),
-                            d2h_bytes=self.results.numel() * self.results.element_size())
-            g = self.graph_io = self._create_graph(io)
+                            h2d_bytes=int(self.prog.n_input_elems) * esz, d2h_src=None, d2h_dst=None, d2h_bytes=0)
+            g = self.graph_io = self._create_graph(io, c_io)
         return g
 
     def run(self, raw_parts, stream=None):
