@@ -147,6 +147,22 @@ __device__ __forceinline__ uint64_t pext64(uint64_t x, uint64_t m) {
   return r;
 }
 
+#ifndef K2_RED_RELEASE
+#define K2_RED_RELEASE 1
+#endif
+// Publish n finished tiles of an item (thread 0, after a __syncthreads that
+// ordered the block's result stores): one release-add at gpu scope, the
+// consumer's ld.acquire pairs with it (cumulativity covers the other
+// threads' stores via the barrier).
+__device__ __forceinline__ void publish_tiles(uint32_t* p, uint32_t n) {
+#if K2_RED_RELEASE
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(n) : "memory");
+#else
+  __threadfence();
+  atomicAdd(p, n);
+#endif
+}
+
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -275,8 +291,7 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
     if (cur != prepared) {
       // publish finished tiles of the previous item before any waiting
       if (tid == 0 && pend_cnt) {
-        __threadfence();
-        atomicAdd(&done[pend_item], pend_cnt);
+        publish_tiles(&done[pend_item], pend_cnt);
         pend_cnt = 0;
       }
       const int nm = S.b.w >= 0 ? S.b.n_mem : 0;
@@ -392,8 +407,7 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
       // the prefetched next ticket belongs to another item: publish now (a
       // dependent item may be waiting) instead of after the ticket search
       if (S.next >= S.item_end) {
-        __threadfence();
-        atomicAdd(&done[pend_item], pend_cnt);
+        publish_tiles(&done[pend_item], pend_cnt);
         pend_cnt = 0;
       }
     }
@@ -401,10 +415,12 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
   // exit: publish, then the last block out zeroes the stage's counters
   if (tid == 0) {
     if (pend_cnt) {
-      __threadfence();
-      atomicAdd(&done[pend_item], pend_cnt);
+      publish_tiles(&done[pend_item], pend_cnt);
     }
-    const unsigned v = atomicAdd(&ctl[1], 1u);
+    // acq_rel: this block's publishes are ordered before its exit count, and
+    // the last block out sees every block's publishes before it resets them
+    unsigned v;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(v) : "l"(&ctl[1]) : "memory");
     S.last = (v == gridDim.x - 1) ? 1 : 0;
   }
   __syncthreads();
