@@ -500,8 +500,9 @@ def run_graph(args):
         "e2e": {"value": len(cones) / t_api, "unit": UNIT, "h2d_bytes_per_step": in_bytes,
                 "d2h_bytes_per_step": 16 * n_units,
                 "call": f"qaoa_energy(g, QaoaParams.seeded(4, 100+k), backend, cone='tight', simplify={args.simplify}): "
-                        f"angle sweep of {n_sweep} calls (lightcone tensors built, inputs staged and results read "
-                        "back every call; plans and CUDA graphs reused)",
+                        f"angle sweep of {n_sweep} calls (every call: the cones' input tensors for the new angles "
+                        "(from the angle recipe; lightcone networks rebuilt only with simplify), host gather, upload "
+                        "and result read-back; plans and CUDA graphs reused)",
                 "cold_call_s": t_cold, "energy": e_api},
         "gpu_launches": args.steps * sum(ex.prog.n_nodes for ex, _ in prep.batches),
         "clocks": clk.summary(),

@@ -348,6 +348,93 @@ def _check_residue(edge, value, dtype="complex128"):
 
 
 _ENERGY_PLANS = {}   # structure key -> (UnitPlan, executor cache); insertion-ordered, 2 entries
+_ENERGY_RECIPES = {}  # (graph, p, cone, plan options) -> (UnitPlan, executor cache, _AngleRecipe)
+
+
+class _AngleRecipe:
+    """How every input element of every cone of a QAOA energy depends on the
+    angles, so that the next point of an angle sweep restages the cones
+    without rebuilding circuits and networks.  The lightcone structure of a
+    QAOA MaxCut circuit does not depend on the angles (cone_gates and
+    tight_cone_gates scan supports only); each tensor's data is either a
+    constant (ket0, Z, H) or a gate of one kind at one layer's angle.  Built
+    from a sentinel build with distinct angles per slot, then checked against
+    the real build element for element (no recipe on any mismatch)."""
+
+    def __init__(self, entries, sizes, idx):
+        self.entries = entries   # palette: (const array) or (kind, slot, adjoint, nq)
+        self.sizes = sizes
+        self.idx = idx           # per cone: int64 gather index into the palette vector
+
+    @staticmethod
+    def _angles(params):
+        # slot 2l: ZZ angle 2*gamma_l; slot 2l+1: RX angle 2*beta_l (src/circuits.py:161,163)
+        out = []
+        for gam, bet in zip(params.gammas, params.betas):
+            out += [2.0 * gam, 2.0 * bet]
+        return out
+
+    @classmethod
+    def build(cls, g, p, cone, edges, ref_raws, ref_params):
+        # sentinel angles: distinct, away from the real ones and from 0 / pi
+        sent = QaoaParams(p, [0.1234567 + 0.0713 * k for k in range(p)],
+                          [0.0517 + 0.0611 * k + 0.03 for k in range(p)])
+        slot_of = {a: i for i, a in enumerate(cls._angles(sent))}
+        if len(slot_of) != 2 * p:
+            return None
+        circ = qaoa_maxcut_circuit(g, sent)
+        rev = {id(arr): key for key, arr in _GATE_DATA.items()}
+        entries, sizes, where = [], [], {}
+        idx = []
+        for ci, e in enumerate(edges):
+            net = extract_lightcone(circ, e, cone=cone).network
+            rev.update({id(arr): key for key, arr in _GATE_DATA.items()})
+            parts = []
+            for t in net.tensors:
+                d = t.data
+                key = rev.get(id(d))
+                if key is None:   # ket0 / Z vectors (an uncached gate array fails the check below)
+                    ent, const = ("const", id(d)), d
+                else:
+                    kind, angle, adjoint, nq = key
+                    if angle is None:
+                        ent, const = ("const", id(d)), d
+                    else:
+                        slot = slot_of.get(angle)
+                        if slot is None:
+                            return None
+                        ent, const = (kind, slot, adjoint, nq), None
+                j = where.get(ent)
+                if j is None:
+                    j = where[ent] = len(entries)
+                    entries.append(const if const is not None else ent)
+                    sizes.append(int(d.size))
+                parts.append(j)
+            idx.append(parts)
+        offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        gidx = [np.concatenate([np.arange(offs[j], offs[j + 1]) for j in parts]) if parts else np.zeros(0, np.int64)
+                for parts in idx]
+        rec = cls(entries, sizes, gidx)
+        try:
+            got = rec.raws(ref_params)
+        except Exception:
+            return None
+        if len(got) != len(ref_raws) or any(a.shape != b.shape or not np.array_equal(a, b)
+                                            for a, b in zip(got, ref_raws)):
+            return None
+        return rec
+
+    def raws(self, params):
+        ang = self._angles(params)
+        vecs = []
+        for ent in self.entries:
+            if isinstance(ent, np.ndarray):
+                vecs.append(np.asarray(ent, np.complex128).ravel())
+            else:
+                kind, slot, adjoint, nq = ent
+                vecs.append(_gate_data(kind, tuple(range(nq)), ang[slot], adjoint).ravel())
+        pal = np.concatenate(vecs)
+        return [pal[i] for i in self.idx]
 
 
 def qaoa_energy_detailed(
@@ -379,6 +466,20 @@ def qaoa_energy_detailed(
     import dataclasses
     from . import distributed as D
     backend = backend or Backend()
+    # angle sweep fast path: same graph, depth and options as a previous call
+    # -> restage the cones' inputs from the angle recipe (no circuit / network
+    # rebuild), reuse plans and device programs
+    fkey = None
+    if not simplify:
+        fkey = (g.n_nodes, tuple(g.edges), params.p, cone, heuristic, mem_cap, slice_target, backend.dtype,
+                backend.threshold, backend.profile, n_gpus, id(group) if group is not None else None, balance_ranks)
+        rec = _ENERGY_RECIPES.get(fkey)
+        if rec is not None:
+            plan0, cache, recipe = rec
+            plan = dataclasses.replace(plan0, raws=recipe.raws(params))
+            values, stats = D.run_units(plan, backend, group=group, n_gpus=n_gpus, cache=cache)
+            return [(lc.edge, _check_residue(lc.edge, values[ci], backend.dtype), stats[ci])
+                    for ci, lc in enumerate(plan0.cones)]
     circuit = qaoa_maxcut_circuit(g, params)
     cones = [extract_lightcone(circuit, e, cone=cone, simplify=simplify) for e in g.edges]
     # the index structure of the cones does not depend on the angles: plans and
@@ -400,6 +501,12 @@ def qaoa_energy_detailed(
         hit = (dataclasses.replace(hit[0], cones=list(cones), raws=raws), hit[1])
     plan, cache = hit
     values, stats = D.run_units(plan, backend, group=group, n_gpus=n_gpus, cache=cache)
+    if fkey is not None and fkey not in _ENERGY_RECIPES:
+        recipe = _AngleRecipe.build(g, params.p, cone, [lc.edge for lc in cones], plan.raws, params)
+        if recipe is not None:
+            _ENERGY_RECIPES[fkey] = (plan, cache, recipe)
+            while len(_ENERGY_RECIPES) > 2:
+                _ENERGY_RECIPES.pop(next(iter(_ENERGY_RECIPES)))
     out = []
     for ci, lc in enumerate(cones):
         out.append((lc.edge, _check_residue(lc.edge, values[ci], backend.dtype), stats[ci]))

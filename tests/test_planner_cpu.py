@@ -375,3 +375,36 @@ def test_wave_aware_tiles(monkeypatch):
         L0 = E._tile_bits(w, [(1 << w) - 1], [1], "complex64", 0)[0]
         L1 = E._tile_bits(w, [(1 << w) - 1], [1], "complex64", slots)[0]
         assert L0 - 2 <= L1 <= L0 and L1 >= min(w, E.MIN_TILE_BITS["complex64"])
+
+
+@pytest.mark.parametrize("cone,p", [("tight", 1), ("tight", 3), ("reference", 2)])
+def test_energy_angle_recipe_restages_exact_inputs(monkeypatch, cone, p):
+    """qaoa_energy angle sweeps: after the first call, the cones' inputs are
+    restaged from the angle recipe (no circuit / network rebuild); they equal
+    the inputs of freshly built lightcones element for element."""
+    from paper_2210_15874_b200 import distributed as D
+    from paper_2210_15874_b200 import tn_build as T
+    seen = {}
+
+    def fake_run_units(plan, backend, group=None, n_gpus=None, cache=None):
+        seen["raws"] = plan.raws
+        return [0j] * len(plan.cones), [[] for _ in plan.cones]
+
+    monkeypatch.setattr(D, "run_units", fake_run_units)
+    T._ENERGY_RECIPES.clear()
+    g = Q.random_regular_graph(14, 3, seed=3)
+    be = Q.Backend.b200(dtype="complex64")
+    Q.qaoa_energy(g, Q.QaoaParams.seeded(p, 0), be, cone=cone)
+    assert len(T._ENERGY_RECIPES) == 1
+    for seed in (1, 2):
+        params = Q.QaoaParams.seeded(p, seed)
+        Q.qaoa_energy(g, params, be, cone=cone)
+        c = Q.qaoa_maxcut_circuit(g, params)
+        for e, got in zip(g.edges, seen["raws"]):
+            ref = np.concatenate([np.asarray(t.data, np.complex128).ravel()
+                                  for t in Q.extract_lightcone(c, e, cone=cone).network.tensors])
+            assert np.array_equal(got, ref)
+    # simplified networks merge gates: no recipe
+    T._ENERGY_RECIPES.clear()
+    Q.qaoa_energy(g, Q.QaoaParams.seeded(p, 0), be, cone=cone, simplify=True)
+    assert len(T._ENERGY_RECIPES) == 0
