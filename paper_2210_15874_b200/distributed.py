@@ -197,6 +197,9 @@ def run_local(plan: UnitPlan, mine, backend: Backend, device: int, budget_bytes=
     import torch
     be = Backend(backend.kind, backend.threshold, backend.dtype, device, backend.profile)
     key = ("batches", tuple(mine), device, be.dtype, be.profile)
+    skey = ("streamed", tuple(mine), device, be.dtype, be.profile)
+    if cache is not None and skey in cache:
+        return _run_streamed(plan, None, be, device, cache[skey])
     if cache is not None and key in cache:
         built = cache[key]
     else:
@@ -204,8 +207,14 @@ def run_local(plan: UnitPlan, mine, backend: Backend, device: int, budget_bytes=
             free, _ = torch.cuda.mem_get_info(device)
             budget_bytes = int(0.6 * free)
         batches = list(_batches(mine, plan, be, budget_bytes))
-        if len(batches) > 1:   # does not fit at once: stream the batches, keep nothing
-            return _run_streamed(plan, batches, be, device)
+        if len(batches) > 1:
+            # does not fit at once: stream the batches through one arena; only
+            # the host programs are kept for the next call on this structure
+            progs = []
+            out = _run_streamed(plan, batches, be, device, progs)
+            if cache is not None:
+                cache[skey] = progs
+            return out
         built = []
         for batch in batches:
             insts = [E.Instance(plan.templates[plan.units[u].cone], plan.units[u].assignment) for u in batch]
@@ -228,13 +237,14 @@ def run_local(plan: UnitPlan, mine, backend: Backend, device: int, budget_bytes=
     return vals, stats
 
 
-def _run_streamed(plan, batches, be, device):
+def _run_streamed(plan, batches, be, device, progs):
     """Batches that do not fit in HBM together, run one after another through
     one shared arena: batch k+1's Program (host planning, the expensive part)
     and Executor (graph build from host tables, pinned uploads) are prepared
     while batch k runs, then queued behind it on the same stream; batch k's
     results are read after k+1 was submitted.  The arena grows (after a wait)
-    when a batch needs more."""
+    when a batch needs more.  `progs`: [(Program, batch)] — filled when
+    `batches` is given, replayed (no host planning) when `batches` is None."""
     import torch
     from .ordering import ref_stats
     tdt = torch.complex64 if be.dtype == "complex64" else torch.complex128
@@ -251,9 +261,17 @@ def _run_streamed(plan, batches, be, device):
             el = (np.maximum(t1[ex.prog.bucket_gid[k]] - t0[ex.prog.bucket_gid[k]], 0) if be.profile else None)
             stats.setdefault(ci, []).extend(ref_stats(plan.templates[ci], be, el))
 
-    for batch in batches:
-        insts = [E.Instance(plan.templates[plan.units[u].cone], plan.units[u].assignment) for u in batch]
-        prog = E.Program(insts, be.dtype)
+    work = progs if batches is None else batches
+    if batches is None and progs:   # replay: the largest arena up front (no mid-stream waits)
+        arena = torch.empty(max(pr.arena_elems for pr, _ in progs), dtype=tdt, device=torch.device("cuda", device))
+    for item in work:
+        if batches is None:
+            prog, batch = item
+        else:
+            batch = item
+            insts = [E.Instance(plan.templates[plan.units[u].cone], plan.units[u].assignment) for u in batch]
+            prog = E.Program(insts, be.dtype)
+            progs.append((prog, batch))
         if arena is None or arena.numel() < prog.arena_elems:
             if prev is not None:
                 finish(*prev)

@@ -254,10 +254,15 @@ def test_streamed_batches_shared_arena():
         one, _ = D.run_local(plan, mine, be, 0, budget_bytes=1 << 40)
         # ascending unit sizes: every few batches need a bigger arena
         mine_sorted = sorted(mine, key=lambda u: plan.units[u].cost)
-        streamed, _ = D.run_local(plan, mine_sorted, be, 0, budget_bytes=1)
+        cache = {}
+        streamed, _ = D.run_local(plan, mine_sorted, be, 0, budget_bytes=1, cache=cache)
         assert set(streamed) == set(one)
         for u in mine:
             assert abs(streamed[u] - one[u]) <= tol * 1e-2
+        # the next call on the same structure replays the kept host programs
+        assert any(k[0] == "streamed" for k in cache)
+        again, _ = D.run_local(plan, mine_sorted, be, 0, budget_bytes=1, cache=cache)
+        assert again == streamed
         zz = [0j] * len(cones)
         for u, unit in enumerate(plan.units):
             zz[unit.cone] += streamed[u]
