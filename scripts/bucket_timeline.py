@@ -76,10 +76,11 @@ while cur is not None:
     path.append(cur)
     ps = producers(cur)
     cur = max(ps, key=lambda g: gid_rows[g][1]) if ps else None
-print("critical path (first -> last): start end dur | w k L tiles nmem | node kind variant")
+fam = ex.node_kernels(io=False)   # the kernel family the graph actually runs per node
+print("critical path (first -> last): start end dur | w k L tiles nmem | node kernel variant")
 for gid in reversed(path):
     b = B[gid]
     s_, e_ = gid_rows[gid]
     ni, kind, var = node_of[gid]
     print(f"  {s_/1e3:7.1f} {e_/1e3:7.1f} {(e_-s_)/1e3:6.1f} | {int(b['w']):3d} {int(b['k'])} {int(b['tile_bits']):2d} "
-          f"{int(b['n_tiles']):5d} {int(b['n_mem'])} | node {ni:3d} {'K2' if kind == 0 else 'K1'} {var:#x}")
+          f"{int(b['n_tiles']):5d} {int(b['n_mem'])} | node {ni:3d} {fam[ni]} {var:#x}")
