@@ -261,6 +261,7 @@ def _run_streamed(plan, batches, be, device, progs):
             el = (np.maximum(t1[ex.prog.bucket_gid[k]] - t0[ex.prog.bucket_gid[k]], 0) if be.profile else None)
             stats.setdefault(ci, []).extend(ref_stats(plan.templates[ci], be, el))
 
+    ex = None
     work = progs if batches is None else batches
     if batches is None and progs:   # replay: the largest arena up front (no mid-stream waits)
         arena = torch.empty(max(pr.arena_elems for pr, _ in progs), dtype=tdt, device=torch.device("cuda", device))
@@ -276,7 +277,8 @@ def _run_streamed(plan, batches, be, device, progs):
             if prev is not None:
                 finish(*prev)
                 prev = None
-            arena = None
+            ex = None      # the last executor holds the old arena too
+            arena = None   # freed before the larger one is allocated
             arena = torch.empty(prog.arena_elems, dtype=tdt, device=torch.device("cuda", device))
         ex = E.Executor(prog, device=device, timing=be.profile, arena=arena)
         ex.submit([plan.raws[plan.units[u].cone] for u in batch])

@@ -68,10 +68,11 @@ def _tensor_align(size):
 
 
 KMAX = N.MAX_SUMMED
-# summed indices of a merged large item (measured: complex64 cfg-2 0.318 ->
-# 0.308 ms with 2, 45-cone graph +1 %; complex128 is best with 3)
+# summed indices of a merged large item: 3 at both dtypes (complex64 with
+# the K4 expansion kernel: cfg-2 0.2487 -> 0.2480 ms, 45-cone graph 9.03 ->
+# 8.80 ms, cfg-3 0.267 -> 0.262 s, cfg-4 8.63 -> 8.04 s against 2)
 _KL = os.environ.get("QTN_KMAX_LARGE")
-KMAX_LARGE = {"complex64": int(_KL) if _KL else 2, "complex128": int(_KL) if _KL else 3}
+KMAX_LARGE = {"complex64": int(_KL) if _KL else 3, "complex128": int(_KL) if _KL else 3}
 SMALL_PROD_ELEMS = 1024   # smem products per round of a small tile (csrc)
 VEC = {"complex64": 2, "complex128": 1}
 # merge cost model (seconds).  Effective constants, tuned end to end on the
