@@ -86,9 +86,11 @@ VEC = {"complex64": 2, "complex128": 1}
 HOP_S = float(os.environ.get("QTN_HOP_S", 8.0e-6))        # K1 graph node
 HOP_K2_S = float(os.environ.get("QTN_HOP_K2_S", 0.8e-6))   # item inside a K2 stage
 # K1 hop in wave-aware plans (one contraction per graph, nothing to overlap a
-# hop with): measured end to end, c64 5 us (cfg-2 0.2516 -> 0.2478 ms), c128
-# keeps 8 us (5 us was 1.4 % slower)
-HOP_SINGLE_S = {"complex64": float(os.environ.get("QTN_HOP_SINGLE_C64_S", 5.0e-6)),
+# hop with), measured end to end: c64 3 us — cfg-2 0.2484 (5 us) -> 0.2366 ms;
+# over the 40 widest N=30 p=4 tight cones the sum is flat (3 us 12.51 ms,
+# 5 us 12.49 ms, 8 us 12.61 ms; scripts/hop_check.py); c128 keeps 8 us (5 us
+# was 1.4 % slower on cfg-2)
+HOP_SINGLE_S = {"complex64": float(os.environ.get("QTN_HOP_SINGLE_C64_S", 3.0e-6)),
                 "complex128": float(os.environ.get("QTN_HOP_SINGLE_C128_S", 8.0e-6))}
 BW_BPS = float(os.environ.get("QTN_BW_BPS", 5.5e12))
 _TERMS_SCALE = float(os.environ.get("QTN_TERMS_SCALE", 1.0))
