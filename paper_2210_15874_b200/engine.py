@@ -82,8 +82,10 @@ VEC = {"complex64": 2, "complex128": 1}
 # block evaluates ~5e9 member-terms/s (complex64); a small-tile round is
 # L2-latency bound (~0.65 us per dependent member load, r01 K2 timeline).
 # Tuned values: cfg-2 0.327 -> 0.318 ms, 45-cone graph 10.4 -> 9.5 ms, cfg-3
-# 0.286 -> 0.267 s.  QTN_* environment overrides are for A/B sweeps.
-HOP_S = float(os.environ.get("QTN_HOP_S", 8.0e-6))        # K1 graph node
+# 0.286 -> 0.267 s.  Re-swept with K4 and 3-index large merges: multi-
+# instance plans charge 12 us (45-cone graph 8.80 -> 8.52 ms; cfg-3 / cfg-4
+# unchanged within 0.6 %).  QTN_* environment overrides are for A/B sweeps.
+HOP_S = float(os.environ.get("QTN_HOP_S", 12.0e-6))       # K1 graph node (multi-instance programs)
 HOP_K2_S = float(os.environ.get("QTN_HOP_K2_S", 0.8e-6))   # item inside a K2 stage
 # K1 hop in wave-aware plans (one contraction per graph, nothing to overlap a
 # hop with), measured end to end: c64 3 us — cfg-2 0.2484 (5 us) -> 0.2366 ms;
