@@ -1222,7 +1222,10 @@ int qtn_graph_create_host(const qtn_program_t* p, const qtn_bucket_t* items, con
       std::vector<unsigned char> plan(qtn_k4_plan_bytes());
       const void* fn = nullptr;
       int grid = 0, smem = 0;
-      static const int k4_all = getenv_int("QTN_K4_ALL", 0);   // A/B: non-expansion items too
+      // non-expansion items too: complex128 by default (cfg-2 0.3575 -> 0.3519 ms),
+      // not complex64 (its streaming items stay faster in K1); QTN_K4_ALL overrides
+      static const int k4_all_env = getenv_int("QTN_K4_ALL", -1);
+      const bool k4_all = k4_all_env >= 0 ? k4_all_env != 0 : p->dtype == QTN_C128;
       if (qtn_k4_node(&d, k4_all ? 0 : k4_min_e, p->timing, nd.first, plan.data(), &fn, &grid, &smem) == QTN_OK) {
         specs[i].k3plan = std::move(plan);
         specs[i].fn = fn;
