@@ -80,8 +80,27 @@ __device__ __forceinline__ void cfma(T& acc, T a, T b) {
   acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
 }
 
+// complex64 variants are compiled for >= 4 resident blocks (<= 64 registers:
+// cfg-2 0.2395 -> 0.2346 ms, the default heuristic picked 32 registers with
+// spills); complex128 keeps the default (4 blocks measured 1.3 % slower)
+#ifndef K4_C64_MINB
+#define K4_C64_MINB 4
+#endif
+
 template <typename R, int K, int NE>
-__global__ void __launch_bounds__(NT) k4_kernel(const __grid_constant__ Plan P) {
+__device__ __forceinline__ void k4_body(const Plan& P);
+
+template <typename R, int K, int NE>
+__global__ void __launch_bounds__(NT, K4_C64_MINB) k4_kernel_c64(const __grid_constant__ Plan P) {
+  k4_body<R, K, NE>(P);
+}
+template <typename R, int K, int NE>
+__global__ void __launch_bounds__(NT) k4_kernel_c128(const __grid_constant__ Plan P) {
+  k4_body<R, K, NE>(P);
+}
+
+template <typename R, int K, int NE>
+__device__ __forceinline__ void k4_body(const Plan& P) {
   using T = typename Cx<R>::T;
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   constexpr int NS = 1 << K;
@@ -204,14 +223,22 @@ __global__ void __launch_bounds__(NT) k4_kernel(const __grid_constant__ Plan P) 
   }
 }
 
+template <typename R, int K, int NE>
+const void* fn_k() {
+  if constexpr (sizeof(R) == 4)
+    return (const void*)k4_kernel_c64<R, K, NE>;
+  else
+    return (const void*)k4_kernel_c128<R, K, NE>;
+}
+
 template <typename R, int K>
 const void* fn_ne(int ne) {
   switch (ne) {
-    case 0: return (const void*)k4_kernel<R, K, 0>;
-    case 1: return (const void*)k4_kernel<R, K, 1>;
-    case 2: return (const void*)k4_kernel<R, K, 2>;
-    case 3: return (const void*)k4_kernel<R, K, 3>;
-    default: return (const void*)k4_kernel<R, K, 4>;
+    case 0: return fn_k<R, K, 0>();
+    case 1: return fn_k<R, K, 1>();
+    case 2: return fn_k<R, K, 2>();
+    case 3: return fn_k<R, K, 3>();
+    default: return fn_k<R, K, 4>();
   }
 }
 
