@@ -233,8 +233,15 @@ def run_local(plan: UnitPlan, mine, backend: Backend, device: int, budget_bytes=
             ci = plan.units[u].cone
             tm = plan.templates[ci]
             el = np.maximum(t1[prog.bucket_gid[k]] - t0[prog.bucket_gid[k]], 0) if be.profile else None
-            stats.setdefault(ci, []).extend(ref_stats(tm, be, el))
+            stats.setdefault(ci, []).extend(ref_stats(tm, be, el) if be.profile else _plain_stats(tm, be))
     return vals, stats
+
+
+def _plain_stats(tmpl, be):
+    """BucketStats without timings depend on the plan only (immutable): built
+    once per template (ordering._stats does the same for contract_network)."""
+    from .ordering import _stats
+    return _stats(tmpl, None, be)
 
 
 def _run_streamed(plan, batches, be, device, progs):
@@ -259,7 +266,8 @@ def _run_streamed(plan, batches, be, device, progs):
             vals[u] = complex(res[k])
             ci = plan.units[u].cone
             el = (np.maximum(t1[ex.prog.bucket_gid[k]] - t0[ex.prog.bucket_gid[k]], 0) if be.profile else None)
-            stats.setdefault(ci, []).extend(ref_stats(plan.templates[ci], be, el))
+            tm = plan.templates[ci]
+            stats.setdefault(ci, []).extend(ref_stats(tm, be, el) if be.profile else _plain_stats(tm, be))
 
     ex = None
     work = progs if batches is None else batches

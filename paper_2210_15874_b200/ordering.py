@@ -366,6 +366,8 @@ def _stats(tmpl, ex, backend, inst=0):
     key = (id(tmpl), backend.threshold)
     hit = _NOPROFILE_STATS.get(key)
     if hit is None or hit[0] is not tmpl:
+        if len(_NOPROFILE_STATS) > 4096:
+            _NOPROFILE_STATS.clear()
         hit = _NOPROFILE_STATS[key] = (tmpl, ref_stats(tmpl, backend))
     return list(hit[1])
 
