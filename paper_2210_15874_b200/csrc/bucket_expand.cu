@@ -40,6 +40,24 @@
 
 int qtn_internal_set_error(int code, const char* msg);
 
+// QTN_DEBUG build: bounds-check every member / product-table / result index
+#ifdef QTN_DEBUG
+#define K4_CHECK(cond, ...)                                                        \
+  do {                                                                             \
+    if (!(cond)) {                                                                 \
+      printf("K4_CHECK %s:%d (block %d thread %d): ", __FILE__, __LINE__,          \
+             (int)blockIdx.x, (int)threadIdx.x);                                   \
+      printf(__VA_ARGS__);                                                         \
+      printf("\n");                                                               \
+      __trap();                                                                    \
+    }                                                                              \
+  } while (0)
+#else
+#define K4_CHECK(cond, ...) \
+  do {                      \
+  } while (0)
+#endif
+
 namespace qtn_k4 {
 
 constexpr int NT = 256;
@@ -56,6 +74,8 @@ struct Plan {
   int32_t nm, k, nE, nF, nH, iB;
   int32_t nHF;                          // tile-id bits other members carry (the highest nHF of nH)
   int64_t n_tiles;
+  int64_t out_elems;                    // 2^w
+  int64_t span[MAXM];                   // elements each member spans (QTN_DEBUG bounds checks)
   int64_t hs[MAXM + 1][MAXH];           // per member (and out, index nm): stride of tile bit j
   uint32_t fs[MAXM][MAXFB];             // F entry bit q (s bits first) -> member stride
   int64_t bs[MAXKS];                    // B strides of the summed bits
@@ -181,7 +201,11 @@ __device__ __forceinline__ void k4_body(const Plan& P) {
     T bv[NS];
     const T* bp = Bm + bb + boff;
 #pragma unroll
-    for (int s = 0; s < NS; ++s) bv[s] = __ldg(bp + soffB[s]);
+    for (int s = 0; s < NS; ++s) {
+      K4_CHECK(bb + boff + soffB[s] >= 0 && bb + boff + soffB[s] < P.span[P.iB], "B element %lld of %lld",
+               (long long)(bb + boff + soffB[s]), (long long)P.span[P.iB]);
+      bv[s] = __ldg(bp + soffB[s]);
+    }
     if ((h >> shf) != fkey) {
       fkey = h >> shf;
       __syncthreads();   // previous F no longer read
@@ -199,6 +223,8 @@ __device__ __forceinline__ void k4_body(const Plan& P) {
         for (int j = 0; j < nm; ++j) {
           if (j == P.iB) continue;
           const T* mp = reinterpret_cast<const T*>(P.mptr[j]);
+          K4_CHECK(sbase[j] + LUT[j * 128 + lo] + LUT[j * 128 + 64 + hi] < P.span[j], "member %d element %lld", j,
+                   (long long)(sbase[j] + LUT[j * 128 + lo] + LUT[j * 128 + 64 + hi]));
           v = cmul(v, __ldg(mp + sbase[j] + LUT[j * 128 + lo] + LUT[j * 128 + 64 + hi]));
         }
         F[x] = v;
@@ -208,10 +234,13 @@ __device__ __forceinline__ void k4_body(const Plan& P) {
     T* op = out + obase + ob;
 #pragma unroll
     for (int e = 0; e < NEV; ++e) {
+      K4_CHECK(fe[e] + NS <= nfe, "F entry %d of %d", fe[e] + NS, nfe);
       const T* fp = F + fe[e];
       T acc = cmul(bv[0], fp[0]);
 #pragma unroll
       for (int s = 1; s < NS; ++s) cfma(acc, bv[s], fp[s]);
+      K4_CHECK(obase + ob + oe[e] >= 0 && obase + ob + oe[e] < P.out_elems, "result %lld of %lld",
+               (long long)(obase + ob + oe[e]), (long long)P.out_elems);
       op[oe[e]] = acc;
     }
   }
@@ -339,6 +368,12 @@ int make_plan(const qtn_bucket_desc_t* d, int min_e, Plan* P, int* smem) {
   P->nH = nh;
   P->nHF = nhf;
   P->n_tiles = (int64_t)1 << nh;
+  P->out_elems = (int64_t)1 << w;
+  for (int i = 0; i < nm; ++i) {
+    int64_t sp = 1;
+    for (int b = 0; b < w + k; ++b) sp += d->mem[i].strides[b];
+    P->span[i] = sp;
+  }
   for (int i = 0; i < nm; ++i) {
     if (i == iB) continue;
     for (int q = 0; q < k; ++q) P->fs[i][q] = (uint32_t)d->mem[i].strides[w + q];
