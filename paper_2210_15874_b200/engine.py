@@ -109,6 +109,9 @@ MIN_TILE_BITS = {"complex64": 9, "complex128": 8}   # vector path needs VEC*NT r
 # complex64 flat over 12..16, complex128 best at 16: 0.473 -> 0.452 ms)
 _SIB = os.environ.get("QTN_SMALL_ITER")
 SMALL_ITER_BITS = {"complex64": int(_SIB) if _SIB else 12, "complex128": int(_SIB) if _SIB else 16}
+# single-contraction (wave-aware) complex64 plans: one bit lower (cfg-2 0.2366
+# -> 0.2337 ms; flat over the 40 widest N=30 p=4 cones, 12.513 vs 12.506 ms)
+SMALL_ITER_BITS_SINGLE = {"complex64": int(_SIB) if _SIB else 11, "complex128": SMALL_ITER_BITS["complex128"]}
 SMALL_TILE_BITS = {"complex64": 8, "complex128": 7}  # K2 tiles: below one vector step
 # QTN_MERGE=0 disables chain merging (A/B measurements)
 MERGE_DEFAULT = os.environ.get("QTN_MERGE", "1") != "0"
@@ -292,13 +295,14 @@ def _cost_of(it, dtype, small_iter_bits=None, slots=0):
                       hop=HOP_SINGLE_S[dtype] if slots else HOP_S, nm_eff=nm_eff)
 
 
-def small_iter_bits_for(threshold, dtype="complex64"):
+def small_iter_bits_for(threshold, dtype="complex64", single=False):
     """Backend.threshold (result width at or below which a bucket runs in the
     batched small-bucket schedule, the analogue of the reference's Mixed
     threshold, src/tensor_core.py:176-184) -> iteration bits (w + k) of the
-    K2 routing rule; None -> the measured per-dtype default."""
+    K2 routing rule; None -> the measured per-dtype default (`single`: for a
+    program that runs one contraction alone, see SMALL_ITER_BITS_SINGLE)."""
     if threshold is None:
-        return SMALL_ITER_BITS[norm_dtype(dtype)]
+        return (SMALL_ITER_BITS_SINGLE if single else SMALL_ITER_BITS)[norm_dtype(dtype)]
     return int(threshold) + 1
 
 
@@ -326,7 +330,7 @@ def plan_template(index_sets, order, dtype, fixed=(), merge=None, small_iter_bit
     keep the largest tiles."""
     dtype = norm_dtype(dtype)
     merge = MERGE_DEFAULT if merge is None else merge
-    sib = SMALL_ITER_BITS[dtype] if small_iter_bits is None else int(small_iter_bits)
+    sib = small_iter_bits_for(None, dtype, wave_aware) if small_iter_bits is None else int(small_iter_bits)
     fixed = list(dict.fromkeys(int(f) for f in fixed))
     sc, a = N.plan_build([tuple(int(i) for i in s) for s in index_sets], order, fixed, _plan_params(dtype, merge, sib, wave_aware))
     ncanon = len(a["gdst"])
@@ -355,7 +359,7 @@ def plan_template_py(index_sets, order, dtype, fixed=(), merge=None, small_iter_
     small_iter_bits: items with w + k <= this run in a K2 small stage
     (default SMALL_ITER_BITS = Backend threshold 11 + 1)."""
     dtype = norm_dtype(dtype)
-    sib = SMALL_ITER_BITS[dtype] if small_iter_bits is None else int(small_iter_bits)
+    sib = small_iter_bits_for(None, dtype, wave_aware) if small_iter_bits is None else int(small_iter_bits)
     merge = MERGE_DEFAULT if merge is None else merge
     slots = WAVE_SLOTS[dtype] if wave_aware else 0
     fixed = set(int(f) for f in fixed)

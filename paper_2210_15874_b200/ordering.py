@@ -313,7 +313,7 @@ def _template_from(struct, plans, order, backend, fixed=()):
         # an unsliced contraction runs alone in its graph: wave-aware tiles;
         # the 2^s slices of contract_sliced run together in one program
         hit = E.plan_template(list(struct), order, backend.dtype, fixed,
-                              small_iter_bits=E.small_iter_bits_for(backend.threshold, backend.dtype),
+                              small_iter_bits=E.small_iter_bits_for(backend.threshold, backend.dtype, not fixed),
                               wave_aware=not fixed)
         PLAN_CACHE.put(key, hit)
     plans[okey] = (key, hit)
