@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define QTN_ABI_VERSION 8
+#define QTN_ABI_VERSION 9
 
 enum {
   QTN_OK = 0,
@@ -128,6 +128,13 @@ typedef struct {
   unsigned long long* timing;   /* optional: 2 per bucket (first start, last end, ns) */
   int64_t arena_elems;          /* arena size in elements (bounds checks of the
                                    QTN_DEBUG build; 0 = unchecked)             */
+  /* complex64 programs: the input region [0, n_in_elems) of the arena also
+   * as complex128 (the gate tensors before narrowing).  K2 stages compute in
+   * double precision and read input members from here, so the gates enter
+   * the contraction unrounded; only intermediates are stored as complex64.
+   * NULL / 0 = inputs as stored in the arena (complex128 programs). */
+  const void* inputs_hi;
+  int64_t n_in_elems;
 } qtn_program_t;
 
 /* Execution node of a program graph.

@@ -26,7 +26,7 @@ QTN_FINALIZE = -1
 MAX_MEMBERS = 8
 MAX_WIDTH = 40
 MAX_SUMMED = 6
-ABI_VERSION = 8
+ABI_VERSION = 9
 QTN_NODE_SMALL = 0
 QTN_NODE_LARGE = 1
 QTN_VARIANT_GENERIC = -1
@@ -90,6 +90,7 @@ class ProgramC(ctypes.Structure):
         ("buckets", ctypes.c_void_p), ("members", ctypes.c_void_p), ("deps", ctypes.c_void_p),
         ("tick_begin", ctypes.c_void_p), ("ctrl", ctypes.c_void_p), ("arena", ctypes.c_void_p),
         ("results", ctypes.c_void_p), ("timing", ctypes.c_void_p), ("arena_elems", ctypes.c_int64),
+        ("inputs_hi", ctypes.c_void_p), ("n_in_elems", ctypes.c_int64),
     ]
 
 

@@ -89,6 +89,7 @@ constexpr int MAXM = QTN_MAX_MEMBERS;   // members per item
 constexpr int MAXS = 16;                // vector steps per tile: 2^L / (VEC * NT)
 constexpr int MAXNS = 1 << QTN_MAX_SUMMED;
 constexpr int SMALL_PROD_ELEMS = 1024;  // smem products per round of a small tile
+constexpr int K2_HI_SLOT = 64;          // staged double-precision input member (rank <= 6)
 
 template <typename R> struct Cx;
 template <> struct Cx<float> {
@@ -110,6 +111,11 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 }
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+
+__device__ __forceinline__ double2 widen(float2 a) { return make_double2((double)a.x, (double)a.y); }
+__device__ __forceinline__ double2 widen(double2 a) { return a; }
+__device__ __forceinline__ void narrow(double2 a, float2& o) { o = make_float2((float)a.x, (float)a.y); }
+__device__ __forceinline__ void narrow(double2 a, double2& o) { o = a; }
 
 __device__ __forceinline__ void split(float4 v, float2 (&e)[2]) {
   e[0] = make_float2(v.x, v.y);
@@ -223,6 +229,7 @@ struct SmallCtx {
   int32_t pc[MAXM];
   int32_t pclo[MAXM];
   int16_t sig[MAXM][MAXNS];
+  int32_t hmode[MAXM];   // 1: input member staged unrounded in shi (complex64 programs, rank <= 6)
   int32_t item;
   int32_t tick;
   int32_t next;
@@ -234,11 +241,22 @@ template <typename R>
 __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_t first, int32_t count,
                                                    int32_t n_tickets, uint32_t* ctl) {
   using T = typename Cx<R>::T;
+  // complex64 programs may carry unrounded inputs (P.inputs_hi)
+  constexpr bool HI = Cx<R>::VEC == 2;
+  // K2 computes in double at both element types: products and the in-order
+  // sum over assignments are rounded once, when the result is stored; input
+  // members of complex64 programs come unrounded from P.inputs_hi
+  using D = double2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* sprod = reinterpret_cast<T*>(smem_raw);
+  D* sprod = reinterpret_cast<D*>(smem_raw);
   __shared__ SmallCtx S;
+  // unrounded input members of the current item (complex64 programs), one
+  // slot of K2_HI_SLOT elements per member
+  double2* shi = reinterpret_cast<double2*>(smem_raw + SMALL_PROD_ELEMS * sizeof(D));
   const T* A = reinterpret_cast<const T*>(P.arena);
   T* Aw = reinterpret_cast<T*>(P.arena);
+  const double2* Ahi = reinterpret_cast<const double2*>(P.inputs_hi);
+  const uint64_t n_hi = (HI && Ahi) ? (uint64_t)P.n_in_elems : 0ull;
   uint32_t* done = P.ctrl + 2 * P.n_nodes;
   const int tid = threadIdx.x;
   const int last_item = first + count - 1;
@@ -306,6 +324,17 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
         S.pc[tid] = __popcll(m.mask);
         S.pclo[tid] = __popc((uint32_t)(m.mask & lowmask));
         for (int q = 0; q < (1 << k); ++q) S.sig[tid][q] = (int16_t)pext32((uint32_t)q, m.smask);
+        const int lg = __popcll(m.mask) + __popc(m.smask);
+        S.hmode[tid] = (HI && m.off < n_hi && lg <= 6) ? 1 : 0;
+      }
+      if (HI && n_hi) {
+        // stage the item's (small) input members unrounded
+        for (int e = tid; e < nm * K2_HI_SLOT; e += NT) {
+          const qtn_member_t m = P.members[S.b.mem_begin + e / K2_HI_SLOT];
+          const int q = e % K2_HI_SLOT;
+          const int lg = __popcll(m.mask) + __popc(m.smask);
+          if (HI && m.off < n_hi && lg <= 6 && q < (1 << lg)) shi[e] = __ldg(Ahi + m.off + q);
+        }
       }
       for (int d = tid; d < S.b.n_dep; d += NT) {
         const qtn_dep_t dp = P.deps[S.b.dep_begin + d];
@@ -328,8 +357,8 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
         for (int i = 0; i < S.b.n_mem; ++i) {
           const qtn_member_t m = P.members[S.b.mem_begin + i];
           QTN_CHECK(QTN_ARENA_OK(P, m.off), "finaliser member %d off %lld", i, (long long)m.off);
-          const T v = __ldcg(A + m.off);
-          const double vr = (double)v.x, vi = (double)v.y;
+          const double2 v = (HI && m.off < n_hi) ? __ldg(Ahi + m.off) : widen(__ldcg(A + m.off));
+          const double vr = v.x, vi = v.y;
           const double nr = re * vr - im * vi;
           const double ni = re * vi + im * vr;
           re = nr;
@@ -345,13 +374,16 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
       const int nelem = 1 << L;
       if (tid < nm) S.base[tid] = S.off[tid] + (pext64((uint64_t)h, S.mhi[tid]) << S.pclo[tid]);
       __syncthreads();
+      uint32_t hbits = 0;   // staged unrounded input members (bit i = member i)
+      if (HI && n_hi)
+        for (int i = 0; i < nm; ++i) hbits |= (uint32_t)S.hmode[i] << i;
       T* out = Aw + S.b.out_off + (uint64_t)h * (uint64_t)nelem;
       // threads cover (element, assignment) pairs, UJ per thread per round;
       // every member's loads of a round are issued before any multiply (one
       // L2 round trip per round instead of one per member)
       constexpr int UJ = 2;
       const int chunk = max(1, min(ns, SMALL_PROD_ELEMS / nelem));
-      T acc = T{};
+      D acc = D{};
       for (int s0 = 0; s0 < ns; s0 += chunk) {
         const int cs = min(chunk, ns - s0);
         const int nu = cs * nelem;
@@ -363,6 +395,9 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
             ue[j] = u & (nelem - 1);
             us[j] = s0 + (u >> L);
           }
+          // every member load of the round in flight together (input members
+          // of complex64 programs: the narrowed copy, replaced at multiply
+          // time by the unrounded value staged in shi / read from inputs_hi)
           T x[MAXM][UJ];
 #pragma unroll
           for (int i = 0; i < MAXM; ++i) {
@@ -372,18 +407,35 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
                 const uint64_t o = S.base[i] + ((uint64_t)S.sig[i][us[j]] << S.pc[i]) +
                                    (S.pclo[i] == L ? (uint64_t)ue[j] : (uint64_t)pext32((uint32_t)ue[j], S.mlo[i]));
                 QTN_CHECK(QTN_ARENA_OK(P, o), "small item %d member %d off %lld", cur, i, (long long)o);
-                x[i][j] = __ldcg(A + o);
+                if (HI && ((hbits >> i) & 1u)) {
+                  // staged input member: its element index rides in the x
+                  // slot; the unrounded value replaces it at multiply time
+                  x[i][j].x = __int_as_float((int)(o - S.off[i]));
+                } else {
+                  x[i][j] = __ldcg(A + o);
+                }
               }
             }
           }
 #pragma unroll
           for (int j = 0; j < UJ; ++j) {
-            T prod = x[0][j];
+            D prod = D{};
 #pragma unroll
-            for (int i = 1; i < MAXM; ++i)
-              if (i < nm) prod = cmul(prod, x[i][j]);
+            for (int i = 0; i < MAXM; ++i) {
+              if (i < nm) {
+                D xi;
+                if (HI && ((hbits >> i) & 1u)) {
+                  const int e = __float_as_int(x[i][j].x);
+                  QTN_CHECK(e >= 0 && e < K2_HI_SLOT, "hi member %d index %d", i, e);
+                  xi = shi[i * K2_HI_SLOT + e];
+                } else {
+                  xi = widen(x[i][j]);
+                }
+                prod = i == 0 ? xi : cmul(prod, xi);
+              }
+            }
             if (u0 + j * NT < nu) {
-              QTN_CHECK((u0 + j * NT + 1) * (int)sizeof(T) <= (int)dyn_smem_bytes(), "sprod %d", u0 + j * NT);
+              QTN_CHECK((u0 + j * NT + 1) * (int)sizeof(D) <= (int)dyn_smem_bytes(), "sprod %d", u0 + j * NT);
               sprod[u0 + j * NT] = prod;
             }
           }
@@ -394,7 +446,7 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
         __syncthreads();
       }
       QTN_CHECK(QTN_ARENA_OK(P, S.b.out_off + (uint64_t)h * nelem + nelem - 1), "small item %d out", cur);
-      if (tid < nelem) out[tid] = acc;
+      if (tid < nelem) narrow(acc, out[tid]);
     }
     __syncthreads();
     if (tid == 0) {

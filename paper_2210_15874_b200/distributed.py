@@ -272,7 +272,7 @@ def _run_streamed(plan, batches, be, device, progs):
     ex = None
     work = progs if batches is None else batches
     if batches is None and progs:   # replay: the largest arena up front (no mid-stream waits)
-        arena = torch.empty(max(pr.arena_elems for pr, _ in progs), dtype=tdt, device=torch.device("cuda", device))
+        arena = torch.empty(max(pr.device_elems for pr, _ in progs), dtype=tdt, device=torch.device("cuda", device))
     for item in work:
         if batches is None:
             prog, batch = item
@@ -281,13 +281,13 @@ def _run_streamed(plan, batches, be, device, progs):
             insts = [E.Instance(plan.templates[plan.units[u].cone], plan.units[u].assignment) for u in batch]
             prog = E.Program(insts, be.dtype)
             progs.append((prog, batch))
-        if arena is None or arena.numel() < prog.arena_elems:
+        if arena is None or arena.numel() < prog.device_elems:
             if prev is not None:
                 finish(*prev)
                 prev = None
             ex = None      # the last executor holds the old arena too
             arena = None   # freed before the larger one is allocated
-            arena = torch.empty(prog.arena_elems, dtype=tdt, device=torch.device("cuda", device))
+            arena = torch.empty(prog.device_elems, dtype=tdt, device=torch.device("cuda", device))
         ex = E.Executor(prog, device=device, timing=be.profile, arena=arena)
         ex.submit([plan.raws[plan.units[u].cone] for u in batch])
         if prev is not None:

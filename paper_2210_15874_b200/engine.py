@@ -74,6 +74,7 @@ KMAX = N.MAX_SUMMED
 _KL = os.environ.get("QTN_KMAX_LARGE")
 KMAX_LARGE = {"complex64": int(_KL) if _KL else 3, "complex128": int(_KL) if _KL else 3}
 SMALL_PROD_ELEMS = 1024   # smem products per round of a small tile (csrc)
+K2_HI_SLOT = 64           # staged unrounded input member per K2 item (csrc)
 VEC = {"complex64": 2, "complex128": 1}
 # merge cost model (seconds).  Effective constants, tuned end to end on the
 # B200 (sweep over hop cost and term rate, profiles/r01_configs.md): a K1
@@ -740,6 +741,11 @@ class Program:
         for g in in_small:
             out_elem[g] += small_base
         self.arena_elems = max(_align(small_base + small_pool.top, 32), 32)
+        # complex64: the input region also as complex128 in front of the arena
+        # (qtn_program_t.inputs_hi; K2 stages read the gates unrounded) —
+        # counted in arena elements: 2 complex64 slots per complex128 value
+        self.hi_elems = 2 * n_in if self.dtype == "complex64" else 0
+        self.device_elems = self.hi_elems + self.arena_elems
         deps_all = [sorted(set(prods[g]) | war[g]) for g in range(len(keys))]
 
         # ---- nodes: large items alone, small items in stages ----
@@ -801,7 +807,8 @@ class Program:
             assert gids == list(range(first, first + count))
             tick = 0
             is_stage = nd["kind"] == small_kind
-            node_smem = SMALL_PROD_ELEMS * esz if is_stage else 0
+            # K2 stage: double-precision products + staged unrounded input members
+            node_smem = SMALL_PROD_ELEMS * 16 + N.MAX_MEMBERS * K2_HI_SLOT * 16 if is_stage else 0
             variant = 0
             for gid in gids:
                 (_, i, b), g = item_keys[gid]
@@ -888,8 +895,12 @@ class Executor:
     every run is one cudaGraphLaunch.
 
     arena: optional caller-owned element buffer (dtype of the program, at
-    least prog.arena_elems) shared by executors that run one after another on
-    one stream — stream order keeps a later upload behind earlier kernels."""
+    least prog.device_elems) shared by executors that run one after another on
+    one stream — stream order keeps a later upload behind earlier kernels.
+
+    Device buffer layout: [complex128 input image (complex64 programs only) |
+    arena = input region + intermediates]; the pinned host image has the same
+    [hi | lo] layout, so every upload is one copy."""
 
     def __init__(self, prog: Program, device=0, timing=False, arena=None):
         import torch
@@ -917,12 +928,13 @@ class Executor:
             self.tables = torch.from_numpy(host).pin_memory().to(dev, non_blocking=True)
             base = self.tables.data_ptr()
             if arena is not None:
-                if arena.dtype != tdt or arena.device != dev or arena.numel() < prog.arena_elems:
-                    raise ValueError(f"arena: need {prog.arena_elems} {tdt} elements on {dev}, got "
+                if arena.dtype != tdt or arena.device != dev or arena.numel() < prog.device_elems:
+                    raise ValueError(f"arena: need {prog.device_elems} {tdt} elements on {dev}, got "
                                      f"{arena.numel()} {arena.dtype} on {arena.device}")
-                self.arena = arena
+                self.buf = arena
             else:
-                self.arena = torch.empty(prog.arena_elems, dtype=tdt, device=dev)
+                self.buf = torch.empty(prog.device_elems, dtype=tdt, device=dev)
+            self.arena = self.buf[prog.hi_elems:]
             self.results = torch.zeros(2 * max(1, len(prog.instances)), dtype=torch.float64, device=dev)
             self.results_host = torch.zeros_like(self.results, device="cpu").pin_memory()
             self.timing = None
@@ -930,7 +942,17 @@ class Executor:
                 self.timing = torch.zeros(2 * max(1, prog.n_buckets), dtype=torch.int64, device=dev)
                 self.timing_init = torch.zeros_like(self.timing)
                 self.timing_init[0::2] = np.iinfo(np.int64).max
-            self.img_pinned = torch.zeros(max(1, prog.n_input_elems), dtype=tdt).pin_memory()
+            esz = ELEM_BYTES[prog.dtype]
+            n_in = prog.n_input_elems
+            self.img_bytes = n_in * esz + (n_in * 16 if prog.hi_elems else 0)
+            self.img_pinned = torch.zeros(max(16, self.img_bytes), dtype=torch.uint8).pin_memory()
+            v = self.img_pinned.numpy()
+            if prog.hi_elems:
+                self._img_hi = v[:16 * n_in].view(np.complex128)
+                self._img_lo = v[16 * n_in: 16 * n_in + esz * n_in].view(np.complex64)
+            else:
+                self._img_hi = None
+                self._img_lo = v[:esz * n_in].view(np.complex64 if prog.dtype == "complex64" else np.complex128)
             c = N.ProgramC()
             c.dtype = DTYPE_CODE[prog.dtype]
             c.n_buckets = prog.n_buckets
@@ -947,6 +969,8 @@ class Executor:
             c.results = self.results.data_ptr()
             c.timing = self.timing.data_ptr() if timing else None
             c.arena_elems = prog.arena_elems
+            c.inputs_hi = self.buf.data_ptr() if prog.hi_elems else None
+            c.n_in_elems = n_in if prog.hi_elems else 0
             self.c = c
             self.done = torch.cuda.Event()
         self._graph = None
@@ -1007,15 +1031,25 @@ class Executor:
         into canonical layout (and narrowed) straight into the pinned staging
         buffer, then one H2D copy; alignment padding is never read."""
         self._staged = None
-        view = self.img_pinned.numpy()
+        self._gather(raw_parts)
+        if self.img_bytes:
+            self.buf.view(self.torch.uint8)[:self.img_bytes].copy_(self.img_pinned[:self.img_bytes],
+                                                                   non_blocking=True)
+
+    def _gather(self, raw_parts):
+        """Canonical-layout gather of the raw inputs into the pinned image
+        (complex128 image first when the program keeps one, then the arena's
+        input region in the program's element type)."""
         parts = self.prog.img_src_parts
         if len(parts) == 1:
-            view[self.prog.img_dst] = raw_parts[0][parts[0]]
+            vals = raw_parts[0][parts[0]]
         elif parts:
-            view[self.prog.img_dst] = np.concatenate([raw[s] for raw, s in zip(raw_parts, parts)])
-        n = self.prog.n_input_elems
-        if n:
-            self.arena[:n].copy_(self.img_pinned[:n], non_blocking=True)
+            vals = np.concatenate([raw[s] for raw, s in zip(raw_parts, parts)])
+        else:
+            return
+        if self._img_hi is not None:
+            self._img_hi[self.prog.img_dst] = vals
+        self._img_lo[self.prog.img_dst] = vals
 
     def launch(self, stream=None):
         torch = self.torch
@@ -1047,14 +1081,13 @@ class Executor:
         graph launch and one stream synchronisation."""
         g = self.graph_io
         if g is None:
-            esz = self.arena.element_size()
             # the finalisers write the result slots straight into the pinned
             # (device-mapped) host buffer: no download node after the last kernel
             c_io = N.ProgramC.from_buffer_copy(self.c)
             c_io.results = self.results_host.data_ptr()
             self.c_io = c_io
-            io = N.GraphIOC(h2d_src=self.img_pinned.data_ptr(), h2d_dst=self.arena.data_ptr(),
-                            h2d_bytes=int(self.prog.n_input_elems) * esz, d2h_src=None, d2h_dst=None, d2h_bytes=0)
+            io = N.GraphIOC(h2d_src=self.img_pinned.data_ptr(), h2d_dst=self.buf.data_ptr(),
+                            h2d_bytes=int(self.img_bytes), d2h_src=None, d2h_dst=None, d2h_bytes=0)
             g = self.graph_io = self._create_graph(io, c_io)
         return g
 
@@ -1077,12 +1110,7 @@ class Executor:
                 all(a is b and not a.flags.writeable for a, b in zip(self._staged, raw_parts)))
         if not same:
             self._staged = None
-            view = self.img_pinned.numpy()
-            parts = self.prog.img_src_parts
-            if len(parts) == 1:
-                view[self.prog.img_dst] = raw_parts[0][parts[0]]
-            elif parts:
-                view[self.prog.img_dst] = np.concatenate([raw[p_] for raw, p_ in zip(raw_parts, parts)])
+            self._gather(raw_parts)
             self._staged = list(raw_parts)
         if self.timing is not None:
             self.timing.copy_(self.timing_init, non_blocking=True)

@@ -3,7 +3,12 @@
 Executes the planner's tables with the exact semantics the CUDA program
 kernel implements (csrc/qtn_b200.cu): buckets in ticket order, member offset
 off + (pext(s, smask) << popc(mask)) + pext(r, mask), out = sum_s prod_i,
-finaliser = product of rank-0 values.  Lets the planner be checked on CPU."""
+finaliser = product of rank-0 values.  Lets the planner be checked on CPU.
+
+Precision model of complex64 programs (qtn_program_t.inputs_hi): K2 stage
+items (small nodes) and finalisers compute in double, reading input members
+of rank <= 6 unrounded; large items compute in complex64 from the narrowed
+arena; every stored intermediate is complex64."""
 import numpy as np
 
 from paper_2210_15874_b200 import _native as N
@@ -24,6 +29,8 @@ def run_program(prog, raw_parts):
     srcs = [raw[s] for raw, s in zip(raw_parts, prog.img_src_parts)]
     if srcs:
         A[prog.img_dst] = np.concatenate(srcs)
+    n_hi = prog.n_input_elems if prog.dtype == "complex64" else 0
+    hi = A[:n_hi].copy()
     if prog.dtype == "complex64":
         A = A.astype(np.complex64)
     res = np.zeros(len(prog.instances), np.complex128)
@@ -34,7 +41,8 @@ def run_program(prog, raw_parts):
         for d in prog.node_deps[nd["dep_begin"]: nd["dep_begin"] + nd["n_dep"]]:
             assert int(d) in node_done and int(d) < ni, "graph dependency not earlier"
         items = range(int(nd["first"]), int(nd["first"]) + int(nd["count"]))
-        if nd["kind"] == N.QTN_NODE_SMALL:
+        small = nd["kind"] == N.QTN_NODE_SMALL
+        if small:
             items = sorted(items, key=lambda g: int(B[g]["tick_begin"]))
         for g in items:
             b = B[g]
@@ -44,7 +52,8 @@ def run_program(prog, raw_parts):
             if b["w"] == N.QTN_FINALIZE:
                 v = 1 + 0j
                 for m in mem:
-                    v *= complex(A[int(m["off"])])
+                    o = int(m["off"])
+                    v *= complex(hi[o] if o < n_hi else A[o])
                 res[int(b["slot"])] = v
             else:
                 w, k = int(b["w"]), int(b["k"])
@@ -55,11 +64,16 @@ def run_program(prog, raw_parts):
                     for m in mem:
                         mask, smask = int(m["mask"]), int(m["smask"])
                         pc = bin(mask).count("1")
-                        x = A[int(m["off"]) + (int(pext_vec(np.array([s]), smask)[0]) << pc) + pext_vec(r, mask)]
+                        o = int(m["off"]) + (int(pext_vec(np.array([s]), smask)[0]) << pc) + pext_vec(r, mask)
+                        if small and n_hi:
+                            staged = int(m["off"]) < n_hi and pc + bin(smask).count("1") <= 6
+                            x = hi[o] if staged else A[o].astype(np.complex128)
+                        else:
+                            x = A[o]
                         p = x.copy() if p is None else p * x
                     acc = p if acc is None else acc + p
                 o = int(b["out_off"])
-                A[o: o + (1 << w)] = acc
+                A[o: o + (1 << w)] = acc.astype(A.dtype)
             done.add(int(g))
         node_done.add(ni)
     return res

@@ -95,7 +95,9 @@ def test_cfg2_lightcone(ci):
     assert abs(v128.real - rec["zz"][0]) <= 1e-10
     assert [s.width for s in st] == rec["widths"]
     v64, _ = Q.contract_network(lc.network, order, C64)
-    assert abs(v64.real - rec["zz"][0]) <= 1e-5
+    # north star: complex64 relative error <= 1e-5 on the lightcone value
+    # (the gates enter K2 unrounded, qtn_program_t.inputs_hi)
+    assert abs(v64.real - rec["zz"][0]) <= 1e-5 * abs(rec["zz"][0])
     # repeated launches of the cached program (self-resetting control block)
     for _ in range(3):
         again, _ = Q.contract_network(lc.network, order, C64)

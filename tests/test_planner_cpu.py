@@ -408,3 +408,25 @@ def test_energy_angle_recipe_restages_exact_inputs(monkeypatch, cone, p):
     T._ENERGY_RECIPES.clear()
     Q.qaoa_energy(g, Q.QaoaParams.seeded(p, 0), be, cone=cone, simplify=True)
     assert len(T._ENERGY_RECIPES) == 0
+
+
+@pytest.mark.parametrize("ci", [0, 1])
+def test_c64_precision_model_cfg2(ci):
+    """The complex64 precision model (emulator docstring: K2 in double from
+    unrounded gates, large items in complex64) meets the north star's 1e-5
+    RELATIVE bar on both cfg-2 cones; narrowing the gates before K2 (the
+    round-1 path) does not on (0, 15) — the gates' rounding is coherent
+    across their many copies."""
+    g, graph, params = _cfg("cfg2")
+    rec = g["cones"][ci]
+    lc = Q.extract_lightcone(Q.qaoa_maxcut_circuit(graph, params), tuple(rec["edge"]), cone="tight")
+    t = E.plan_template([x.indices for x in lc.network.tensors], rec["order"], "complex64", wave_aware=True)
+    prog = E.Program([E.Instance(t)], "complex64")
+    raw = np.concatenate([np.asarray(x.data).ravel() for x in lc.network.tensors])
+    want = rec["zz"][0]
+    v = run_program(prog, [raw])[0]
+    assert abs(v.real - want) <= 1e-5 * abs(want)
+    if ci == 1:
+        narrowed = raw.astype(np.complex64).astype(np.complex128)
+        v0 = run_program(prog, [narrowed])[0]
+        assert abs(v0.real - want) > 1e-5 * abs(want)
