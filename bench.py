@@ -1,24 +1,30 @@
 """Benchmark of the north-star path: one N=30, p=4 QAOA MaxCut edge lightcone
 (BASELINE.json configs[1]; SURVEY 8(d) cfg 2: tight cone of edge (0,15),
-width 25, 270 buckets, 1.468 GB algorithmic traffic at complex64) contracted
-by bucket elimination on the B200.
+width 25, 270 buckets) contracted by bucket elimination on the B200.
 
-  python bench.py [--gpus N --steps K --warmup W --dtype c64|c128]
+  python bench.py [--gpus N --steps K --warmup W --dtype c128|c64]
   python bench.py --impl reference ...   (the reference algorithm on host cores)
 
-A step = one full contraction of the lightcone (plus, at N > 1, the NCCL
-all-reduce of the per-rank <ZZ> slot vector).  Weak scaling: every rank
-contracts one lightcone per step.  `value` is device time (CUDA events on
-the launching stream, L2 flushed before every step, max over ranks); `e2e`
-is the public API call `contract_network(tn, order, backend)` from host
-tensors with the input upload and the result download inside the timed
-region (wall clock, max over ranks).
+A step = one full contraction of the lightcone per rank (weak scaling: every
+rank contracts its own copy; at N > 1 the per-rank <ZZ> slots are summed by
+one NCCL all-reduce inside the step).  The headline dtype is complex128, the
+reference's own arithmetic (src/tensor_core.py:59); complex64 is reported
+beside it.  `value` = lightcones/s from CUDA events on the launching stream
+(L2 flushed before every step, max over ranks); `e2e` = the public call
+`contract_network(tn, order, backend)` with HOST tensors, a different set of
+angles every step (new gate tensors: gather, upload, kernels, result read),
+wall clock, max over ranks.  `strong` = the full-graph energy (45 lightcones
+of the same graph, LPT over the ranks, slot all-reduce) at this N.
+
+`--gpus N` without torchrun re-executes itself under torch.distributed.run
+(one rank per GPU, 127.0.0.1 rendezvous).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -33,95 +39,168 @@ sys.path.insert(0, ROOT)
 METRIC = "lightcones/s (N=30,p=4 single-lightcone contraction)"
 UNIT = "lightcones/s"
 PAPER_BEST_S = 2.1       # NumPy+CuPy mixed, V100
+N_QUBITS, DEGREE, P_LAYERS, SEED = 30, 3, 4, 0
 EDGE = (0, 15)
 GRAPH_MEM_CAP = 64 << 30   # HBM-sized widest-bucket cap (the reference's 4 GiB default is a CPU cap)
 GRAPH_BALANCE = 8          # slice over-wide cones so 8 GPUs can share them (same plan at every N)
-WORKLOAD = "cfg2: 3-regular N=30 (seed 0), p=4 (seeded angles), tight lightcone of edge (0,15): 564 tensors, 270 buckets, widths 0-25"
+WORKLOAD = ("cfg2: 3-regular N=30 (seed 0), p=4 (seeded angles), tight lightcone of edge (0,15): "
+            "564 tensors, 270 buckets, widths 0-25")
+# identical in both arms (the driver compares them)
+CONFIG = {"workload": WORKLOAD, "graph": "random_regular_graph(30, 3, seed=0)", "p": P_LAYERS,
+          "angles": "QaoaParams.seeded(4, 0)", "edge": list(EDGE), "cone": "tight", "order": "greedy_order minfill"}
+L2_NOTE = "flushed (256 MiB write) before every timed step"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
+    ap.add_argument("--dtype", default="c128", choices=["c64", "c128"], help="headline dtype")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=2, help="oracle contractions for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-strong", action="store_true", help="skip the full-graph strong-scaling figure")
     ap.add_argument("--ref-budget-s", type=float, default=150.0)
+    ap.add_argument("--sustain-s", type=float, default=1.0, help="clock-sampled sustained loop after the timed region")
     ap.add_argument("--simplify", action="store_true",
                     help="graph workload: simplify each lightcone network before ordering (tn_build.simplify_network)")
-    ap.add_argument("--workload", default="lightcone", choices=["lightcone", "graph", "bucket"],
-                    help="lightcone: cfg-2 single lightcone per rank (weak); graph: all 45 N=30 p=4 "
-                         "tight lightcones sharded over ranks by LPT + slot all-reduce (strong); bucket: "
-                         "cfg-5 synthetic bucket microbench through K3 (fused permutation-aware kernel)")
-    return ap.parse_args()
+    ap.add_argument("--workload", default="lightcone", choices=["lightcone", "graph", "bucket", "selftest"],
+                    help="lightcone: cfg-2 single lightcone per rank (weak) + full-graph strong figure; graph: "
+                         "all 45 N=30 p=4 tight lightcones sharded over ranks by LPT + slot all-reduce (strong); "
+                         "bucket: cfg-5 synthetic bucket microbench through K3; selftest: the multi-rank harness "
+                         "alone (spawn, rendezvous, max-over-ranks, slot all-reduce) on CPU/gloo")
+    return ap.parse_args(argv)
 
 
-def build_workload():
-    import paper_2210_15874_b200 as Q
-    g = Q.random_regular_graph(30, 3, seed=0)
-    params = Q.QaoaParams.seeded(4, 0)
-    c = Q.qaoa_maxcut_circuit(g, params)
-    lc = Q.extract_lightcone(c, EDGE, cone="tight")
-    order = Q.greedy_order(lc.network)
-    return g, params, lc, order
+# ---------------------------------------------------------------------------
+# multi-rank harness
+# ---------------------------------------------------------------------------
+def _free_port():
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
+def spawn_ranks(n, argv):
+    """Re-execute this script as n ranks under torch.distributed.run (one
+    process per GPU, 127.0.0.1 rendezvous); returns the launcher's exit code.
+    Rank 0's JSON line is the launcher's stdout."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + list(argv)
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # communicator lines show the N ranks ...
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")   # ... on stderr, not in the JSON stdout
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
+def dist_setup():
+    """(rank, world, local_rank); process group over NCCL when CUDA is
+    present, gloo otherwise (the CPU harness test)."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    return rank, world, local
+
+
+def _dev():
+    import torch
+    return "cuda" if torch.cuda.is_available() else "cpu"
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=_dev())
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def finish(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# clocks
+# ---------------------------------------------------------------------------
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """NVML clocks + clock-event (throttle) reasons, polled every `period` s by
+    a background thread while the timed region runs (NVML calls release the
+    GIL; the timed loop only enqueues work, so the device queue stays fed)."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, gpu_index):
-        self.gpu = gpu_index
-        self.proc = None
-        self.lines = []
+    def __init__(self, local, period=0.0005):
+        self.period = period
+        self.samples = []
+        self.max_mhz = None
+        self.h = None
+        self.err = None
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            uuid = str(torch.cuda.get_device_properties(local).uuid)
+            self.h = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.nv = pynvml
+        except Exception as e:   # no NVML: the line says so
+            self.err = f"{type(e).__name__}: {e}"
 
     def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+        self.stop = threading.Event()
+        if self.h is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
-        except Exception:
-            self.proc = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        nv = self.nv
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((sm, rs))
+            except Exception:
+                pass
+            time.sleep(self.period)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.h is not None:
+            self.t.join(timeout=2)
 
     def summary(self):
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            p = [x.strip() for x in ln.split(",")]
-            if len(p) < 9:
-                continue
-            try:
-                sm.append(float(p[1]))
-                smax.append(float(p[2]))
-            except ValueError:
-                continue
-            for n, v in zip(names, p[5:9]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0,
+                    **({"error": self.err} if self.err else {})}
+        reasons = set()
+        for _, rs in self.samples:
+            for bit, name in self.REASONS.items():
+                if rs & bit:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
 
 
 def peak_hbm():
@@ -133,60 +212,50 @@ def peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(dtype):
+def ncu_traffic(key):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the
+    committed `ncu --set full` capture (profiles/traffic.json, keyed by
+    dtype:kernel:item signature); None when that kernel was not captured."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get(dtype)
+            rec = json.load(f).get(key)
+        return rec
     except Exception:
         return None
 
 
-def dist_setup(n):
-    import torch
-    import torch.distributed as dist
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1 and not dist.is_initialized():
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    return rank, world, local
-
-
-def max_over_ranks(x, world):
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
-
-
-def cpu_oracle_time(lc, order, n):
-    """The reference algorithm (oracle port of src/ordering.py:148-189 +
-    src/tensor_core.py:148-164, numpy complex128) on one host core."""
-    from oracle import qtn_oracle as O
-    ts = [(t.indices, t.data) for t in lc.network.tensors]
-    t0 = time.perf_counter()
-    val = None
-    for _ in range(n):
-        val, _ = O.contract_network(ts, order)
-    dt = (time.perf_counter() - t0) / n
-    return dt, val
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+def _host_threads():
+    """All host cores, capped by host memory (a cfg-2 contraction peaks at
+    ~3 x 2^25 x 16 B = 1.6 GB in the reference's fast_kernel)."""
+    n = os.cpu_count() or 1
+    try:
+        import psutil
+        n = max(1, min(n, int(psutil.virtual_memory().available // (2 << 30))))
+    except Exception:
+        pass
+    return n
 
 
 def run_reference(args):
+    """The reference algorithm on the host cores: the oracle port of the
+    reference NumPy path (src/ordering.py:148-189 + src/tensor_core.py:148-164,
+    complex128), network and order built by the oracle too (no product code
+    is imported in this arm).  Every step = one bounded sample: `threads`
+    concurrent contractions of the cfg-2 lightcone."""
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
     from concurrent.futures import ThreadPoolExecutor
     from oracle import qtn_oracle as O
-    g, params, lc, order = build_workload()
-    ts = [(t.indices, t.data) for t in lc.network.tensors]
-    threads = max(1, min(os.cpu_count() or 1, 16))
+    edges = O.random_regular_graph(N_QUBITS, DEGREE, SEED)
+    gammas, betas = O.seeded_angles(P_LAYERS, SEED)
+    ts = O.lightcone_tensors(N_QUBITS, edges, gammas, betas, EDGE, cone="tight")
+    order = O.greedy_order(ts)
+    threads = _host_threads()
 
     def one(_):
         v, _ = O.contract_network(ts, order)
@@ -207,212 +276,294 @@ def run_reference(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
         "steps_requested": args.steps, "warmup": 1, "ms_per_step": 1e3 * dt / steps,
-        "s_per_lightcone": dt / steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded graph/angles)",
-        "config": {"workload": WORKLOAD, "impl": "oracle port of the reference NumPy path (Backend.fast())",
-                   "threads": threads, "zz": vals[0].real},
+        "s_per_lightcone": dt * 1.0 / (steps * threads), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded graph/angles)", "config": CONFIG,
         "impl": "reference",
+        "details": {"impl": "oracle port of the reference NumPy path (Backend.fast()); network + order from the oracle",
+                    "threads": threads, "host_cpus": os.cpu_count(), "zz": vals[0].real},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{steps} steps x {threads} concurrent full contractions of the cfg-2 lightcone "
-                                   f"(numpy complex128, one thread each)"},
+                                   f"(numpy complex128, one thread each; {os.cpu_count()} host CPUs)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def run_ours(args):
-    import torch
+# ---------------------------------------------------------------------------
+# our arm: cfg-2 lightcone
+# ---------------------------------------------------------------------------
+def build_workload(seed=SEED):
     import paper_2210_15874_b200 as Q
-    from paper_2210_15874_b200 import engine as E
+    g = Q.random_regular_graph(N_QUBITS, DEGREE, seed=SEED)
+    params = Q.QaoaParams.seeded(P_LAYERS, seed)
+    c = Q.qaoa_maxcut_circuit(g, params)
+    lc = Q.extract_lightcone(c, EDGE, cone="tight")
+    order = Q.greedy_order(lc.network)
+    return g, params, lc, order
 
-    rank, world, local = dist_setup(args.gpus)
-    torch.cuda.set_device(local)
-    dtype = "complex64" if args.dtype == "c64" else "complex128"
-    g, params, lc, order = build_workload()
-    tn = lc.network
-    be = Q.Backend.b200(dtype=dtype, device=local, profile=False)
 
-    # ---- device-resident program (inputs in HBM before the timed region) ----
-    tmpl = E.plan_template([t.indices for t in tn.tensors], order, dtype, wave_aware=True)  # as contract_network
-    prog = E.Program([E.Instance(tmpl)], dtype)
-    ex = E.Executor(prog, device=local, timing=False)
-    kernel_mix = ex.kernel_mix(io=False)   # graph nodes per kernel family (K1/K2/K3/K4)
-    raw = np.concatenate([np.asarray(t.data).ravel() for t in tn.tensors])
-    ex.stage_inputs([raw])
-    stream = torch.cuda.current_stream()
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
-    slots = torch.zeros(2 * world, dtype=torch.float64, device="cuda")
-    alg_bytes = prog.algorithmic_bytes()
+def cpu_oracle_time(lc, order, n):
+    """The reference algorithm (oracle port of src/ordering.py:148-189 +
+    src/tensor_core.py:148-164, numpy complex128) on one host core."""
+    from oracle import qtn_oracle as O
+    ts = [(t.indices, t.data) for t in lc.network.tensors]
+    t0 = time.perf_counter()
+    val = None
+    for _ in range(n):
+        val, _ = O.contract_network(ts, order)
+    dt = (time.perf_counter() - t0) / n
+    return dt, val
 
-    def step_device():
+
+class _Lightcone:
+    """Device program of the cfg-2 lightcone at one dtype (the plan
+    contract_network makes), inputs resident in HBM."""
+
+    def __init__(self, lc, order, dtype, local):
+        from paper_2210_15874_b200 import engine as E
+        self.E = E
+        tn = lc.network
+        self.dtype = dtype
+        self.tmpl = E.plan_template([t.indices for t in tn.tensors], order, dtype, wave_aware=True)
+        self.prog = E.Program([E.Instance(self.tmpl)], dtype)
+        self.ex = E.Executor(self.prog, device=local, timing=False)
+        self.raw = np.concatenate([np.asarray(t.data).ravel() for t in tn.tensors])
+        self.ex.stage_inputs([self.raw])
+
+
+def time_device(lcp, stream, flush, steps, world, rank, slots):
+    import torch
+    ex = lcp.ex
+
+    def step():
         ex.launch(stream)
         if world > 1:
             slots.zero_()
             slots[2 * rank: 2 * rank + 2].copy_(ex.results[:2])
             torch.distributed.all_reduce(slots)
 
-    for _ in range(max(3, args.warmup)):
-        step_device()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    barrier(world)
     torch.cuda.synchronize()
-    val = complex(*ex.results[:2].cpu().numpy())
-    if world > 1:
-        torch.distributed.barrier()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    kern = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        for i in range(args.steps):
-            flush.zero_()
-            ev[i][0].record(stream)
-            kern[i][0].record(stream)
-            ex.launch(stream)
-            kern[i][1].record(stream)
-            if world > 1:
-                slots.zero_()
-                slots[2 * rank: 2 * rank + 2].copy_(ex.results[:2])
-                torch.distributed.all_reduce(slots)
-            ev[i][1].record(stream)
-        torch.cuda.synchronize()
-        t_dev = sum(a.elapsed_time(b) for a, b in ev) / 1e3
-        t_kern = sum(a.elapsed_time(b) for a, b in kern) / 1e3
-        if world > 1:
-            torch.distributed.barrier()
+    for i in range(steps):
+        flush.zero_()
+        evs[i][0].record(stream)
+        step()
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    return sum(a.elapsed_time(b) for a, b in evs) / 1e3
 
-        # ---- e2e: public API from host tensors ----
-        for _ in range(max(3, args.warmup)):
-            Q.contract_network(tn, order, be)
+
+def time_e2e(nets, order, be, steps, world):
+    """The public call from host tensors, a different network (angles) every
+    step: gather into the pinned image, one graph launch (upload node,
+    kernels, result into pinned host memory), one synchronisation."""
+    import torch
+    import paper_2210_15874_b200 as Q
+    for tn in nets[:3]:
+        Q.contract_network(tn, order, be)
+    torch.cuda.synchronize()
+    barrier(world)
+    vals = []
+    t0 = time.perf_counter()
+    for i in range(steps):
+        v, _ = Q.contract_network(nets[i % len(nets)], order, be)
+        vals.append(v)
+    t = time.perf_counter() - t0
+    return t, vals
+
+
+def dominant_kernel(lcp, stream, flush, reps=50):
+    """The device item with the longest live span (globaltimer stamps of the
+    program kernels, L2 flushed), then that node ALONE timed with CUDA events
+    on the launching stream over `reps` launches: compulsory bytes / mean
+    launch duration, and its share of the step."""
+    import torch
+    E = lcp.E
+    prog = lcp.prog
+    ext = E.Executor(prog, device=lcp.ex.device, timing=True)
+    ext.stage_inputs([lcp.raw])
+    for _ in range(3):
+        ext.launch(stream)
+    acc = np.zeros(prog.n_buckets)
+    for _ in range(20):
+        flush.zero_()
+        ext.launch(stream)
         torch.cuda.synchronize()
-        if world > 1:
-            torch.distributed.barrier()
+        t0_, t1_ = ext.fetch_timing()
+        acc += np.maximum(t1_ - t0_, 0)
+    acc /= 20
+    node_of = prog.node_of_item()
+    large = [g for g in range(prog.n_buckets) if int(prog.nodes[node_of[g]]["kind"]) == 1]
+    top = sorted(large, key=lambda g: -acc[g])[:3]
+    fam = ext.node_kernels(io=False)
+    items = [{"item": int(g), "w": int(prog.buckets[g]["w"]), "k": int(prog.buckets[g]["k"]),
+              "kernel": fam[node_of[g]], "live_us": round(float(acc[g]) / 1e3, 1),
+              "bytes_MB": round(prog.item_bytes(g) / 1e6, 1)} for g in top]
+    del ext
+    g = top[0]
+    gr, fam0 = lcp.ex.node_graph(node_of[g])
+    lcp.ex.launch(stream)                 # the node's inputs in the arena
+    for _ in range(3):
+        lcp.ex.launch_graph(gr, stream)
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        lcp.ex.launch_graph(gr, stream)
+        b.record(stream)
+        ts.append((a, b))
+    torch.cuda.synchronize()
+    dur = sum(a.elapsed_time(b) for a, b in ts) / reps / 1e3
+    b = prog.buckets[g]
+    key = f"{lcp.dtype}:{fam0}:w{int(b['w'])}k{int(b['k'])}"
+    return {"item": int(g), "kernel": fam0, "key": key, "w": int(b["w"]), "k": int(b["k"]),
+            "bytes": prog.item_bytes(g), "us": dur * 1e6, "top_items_live": items}
+
+
+def sustained_clocks(lcp, stream, flush, seconds, local):
+    """The step repeated for >= `seconds` under the clock sampler."""
+    import torch
+    n = 0
+    with ClockSampler(local, period=0.005) as clk:
         t0 = time.perf_counter()
-        for _ in range(args.steps):
-            v_e2e, _ = Q.contract_network(tn, order, be)
-        torch.cuda.synchronize()
-        t_e2e = time.perf_counter() - t0
+        while time.perf_counter() - t0 < seconds:
+            for _ in range(50):
+                flush.zero_()
+                lcp.ex.launch(stream)
+            torch.cuda.synchronize()
+            n += 50
+    s = clk.summary()
+    s["loop_s"] = round(time.perf_counter() - t0, 3)
+    s["steps"] = n
+    return s
+
+
+def run_ours(args):
+    import torch
+    import paper_2210_15874_b200 as Q
+
+    rank, world, local = dist_setup()
+    torch.cuda.set_device(local)
+    hd = "complex128" if args.dtype == "c128" else "complex64"
+    sd = "complex64" if hd == "complex128" else "complex128"
+    g, params, lc, order = build_workload()
+    tn = lc.network
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+    slots = torch.zeros(2 * world, dtype=torch.float64, device="cuda")
+
+    progs = {d: _Lightcone(lc, order, d, local) for d in (hd, sd)}
+    for lcp in progs.values():
+        for _ in range(max(3, args.warmup)):
+            lcp.ex.launch(stream)
+    torch.cuda.synchronize()
+    val = {d: complex(*progs[d].ex.results[:2].cpu().numpy()) for d in progs}
+
+    # ---- headline: device time, K steps, clocks sampled during the region ----
+    with ClockSampler(local) as clk:
+        t_dev = time_device(progs[hd], stream, flush, args.steps, world, rank, slots)
     clocks = clk.summary()
     t_dev = max_over_ranks(t_dev, world)
-    t_e2e = max_over_ranks(t_e2e, world)
-    t_kern = max_over_ranks(t_kern, world)
+    t_side = max_over_ranks(time_device(progs[sd], stream, flush, args.steps, world, rank, slots), world)
 
-    # c128 device time as a side figure (same program structure)
-    # live per-item breakdown: the same program with globaltimer stamps per
-    # item (first tile start -> last tile end), after warm-up, L2 flushed;
-    # algorithmic bytes per item = its reference buckets'
-    items = []
-    if rank == 0:
-        ext = E.Executor(prog, device=local, timing=True)
-        ext.stage_inputs([raw])
-        for _ in range(3):
-            ext.launch(stream)
-        acc = np.zeros(tmpl.n_items)
-        nrep = 20
-        for _ in range(nrep):
-            flush.zero_()
-            ext.launch(stream)
-            torch.cuda.synchronize()
-            t0_, t1_ = ext.fetch_timing()
-            g_ = prog.bucket_gid[0]
-            acc += np.maximum(t1_[g_] - t0_[g_], 0)
-        acc /= nrep
-        ibytes = np.zeros(tmpl.n_items)
-        np.add.at(ibytes, tmpl.ref_item, tmpl.ref_elems * E.ELEM_BYTES[dtype])
-        # kernel family per item from the built graph (K4 / K3 routing happens there)
-        fam = ext.node_kernels(io=False)
-        node_of_gid = {}
-        for ni, nd in enumerate(prog.nodes):
-            for gid in range(int(nd["first"]), int(nd["first"]) + int(nd["count"])):
-                node_of_gid[gid] = ni
-        names = {"K1": "K1 large_kernel", "K2": "K2 small_kernel", "K3": "K3 k3v2_kernel", "K4": "K4 k4_kernel"}
-        for it in np.argsort(-acc)[:3]:
-            kf = fam[node_of_gid[int(prog.bucket_gid[0][it])]]
-            items.append({"item": int(it), "w": int(tmpl.w[it]), "k": int(tmpl.k[it]),
-                          "kernel": names[kf] + (f" variant {int(tmpl.variant[it]):#x}" if kf == "K1" else ""),
-                          "us": round(float(acc[it]) / 1e3, 1), "alg_MB": round(float(ibytes[it]) / 1e6, 1),
-                          "alg_GBps": round(float(ibytes[it]) / max(float(acc[it]), 1.0), 1)})
-        del ext
-    side = {}
-    if dtype == "complex64":
-        tm2 = E.plan_template([t.indices for t in tn.tensors], order, "complex128", wave_aware=True)
-        ex2 = E.Executor(E.Program([E.Instance(tm2)], "complex128"), device=local, timing=False)
-        ex2.stage_inputs([raw])
-        for _ in range(3):
-            ex2.launch(stream)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        n2 = max(10, args.steps // 4)
-        tot = 0.0
-        for _ in range(n2):
-            flush.zero_()
-            e0.record(stream)
-            ex2.launch(stream)
-            e1.record(stream)
-            e1.synchronize()
-            tot += e0.elapsed_time(e1) / 1e3
-        side = {"c128_ms_per_lightcone": 1e3 * tot / n2,
-                "c128_gbs": ex2.prog.algorithmic_bytes() / (tot / n2) / 1e9,
-                "c128_zz": float(ex2.fetch_results()[0].real)}
-        del ex2
+    # ---- e2e through the public API, new angles every step ----
+    nets = [build_workload(seed=SEED + 1 + k)[2].network for k in range(8)]
+    e2e = {}
+    for d in (hd, sd):
+        be = Q.Backend.b200(dtype=d, device=local, profile=False)
+        t, vals = time_e2e(nets, order, be, args.steps, world)
+        e2e[d] = (max_over_ranks(t, world), vals)
+
+    # ---- dominant kernel alone + sustained clocks ----
+    dom = dominant_kernel(progs[hd], stream, flush)
+    sustained = sustained_clocks(progs[hd], stream, flush, args.sustain_s, local)
+
+    strong = None
+    if not args.no_strong:
+        strong = graph_figure(args, rank, world, local, "complex64", stream, flush)
 
     if rank != 0:
+        finish(world)
         return 0
     peak, peak_src = peak_hbm()
-    achieved = alg_bytes / (t_kern / args.steps) / 1e9
+    prog = progs[hd].prog
+    ms = 1e3 * t_dev / args.steps
+    alg, exe = prog.algorithmic_bytes(), prog.executed_bytes()
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         dt, v_cpu = cpu_oracle_time(lc, order, args.cpu_sample)
         cpu = {"value": 1.0 / dt, "unit": UNIT, "cores": 1, "kind": "port",
                "sample": f"{args.cpu_sample} full contractions of the cfg-2 lightcone, oracle port of the reference "
                          f"NumPy path (complex128, one core); <ZZ> = {v_cpu.real:.15f}"}
-    n_in = prog.n_input_elems * E.ELEM_BYTES[dtype]
+    ref_zz = val["complex128"].real
+    rel64 = abs(val["complex64"].real - ref_zz) / abs(ref_zz)
+    esz = {"complex64": 8, "complex128": 16}
+    h2d = {d: progs[d].ex.img_bytes for d in progs}
     value = world * args.steps / t_dev
+    achieved = dom["bytes"] / dom["us"] / 1e3
+    traffic = ncu_traffic(dom["key"])
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": max(3, args.warmup), "ms_per_step": 1e3 * t_dev / args.steps,
-        "s_per_lightcone": t_dev / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": value * PAPER_BEST_S, "dtype": args.dtype, "data": "synthetic (seeded graph/angles)",
-        "config": {"workload": WORKLOAD, "parallelism": f"{world} rank(s), one lightcone per rank per step",
-                   "l2": "flushed (256 MiB write) before every timed step", "zz": val.real,
-                   "algorithmic_bytes_per_step": alg_bytes, "executed_bytes_per_step": prog.executed_bytes(),
-                   "program": prog.describe(),
-                   "vs_baseline_ref": "value x 2.1 s: speed-up over the paper's best single-lightcone time "
-                                      "(NumPy+CuPy mixed on V100, PAPER.md:64)", **side},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": ncu_traffic(args.dtype), "peak_source": peak_src,
-                     "kernel": "one program graph per step: K2 small_kernel stages + K1 large_kernel variants "
-                               "+ K4 k4_kernel expansion items (one cudaGraphLaunch); achieved = algorithmic "
-                               "bytes (SURVEY 8(d)) / device time",
-                     "kernel_mix": kernel_mix,
-                     "achieved_executed": prog.executed_bytes() / (t_kern / args.steps) / 1e9,
-                     "top_items_live": items},
+        "warmup": max(3, args.warmup), "ms_per_step": ms, "s_per_lightcone": t_dev / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": value * PAPER_BEST_S,
+        "dtype": args.dtype, "data": "synthetic (seeded graph/angles)", "config": CONFIG,
+        "details": {
+            "parallelism": f"{world} rank(s), one cfg-2 lightcone per rank per step" +
+                           (", per-rank <ZZ> slots all-reduced (NCCL) inside the step" if world > 1 else ""),
+            "l2": L2_NOTE, "zz": val[hd].real, "program": prog.describe(),
+            "kernel_mix": progs[hd].ex.kernel_mix(io=False),
+            "algorithmic_bytes_per_step": alg, "executed_bytes_per_step": exe,
+            "vs_baseline_ref": "value x 2.1 s: speed-up over the paper's best single-lightcone time "
+                               "(NumPy+CuPy mixed on V100, PAPER.md:64)",
+            "side_dtype": {"dtype": sd, "ms_per_step": 1e3 * t_side / args.steps,
+                           "value": world * args.steps / t_side, "zz": val[sd].real,
+                           "e2e_value": world * args.steps / e2e[sd][0]},
+            "c64_rel_err_vs_c128": rel64,
+        },
+        "roofline": {
+            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": (traffic or {}).get("dram_bytes"), "peak_source": peak_src,
+            "kernel": f"{dom['kernel']} on item {dom['item']} (w={dom['w']}, k={dom['k']}), timed alone with CUDA "
+                      f"events ({dom['us']:.1f} us per launch); achieved = compulsory bytes (members once + result "
+                      f"once = {dom['bytes']}) / launch duration",
+            "dominant_share_of_step": dom["us"] / 1e3 / ms,
+            "traffic_source": (traffic or {}).get("source"),
+            "step": {"executed_GBps": exe / (ms / 1e3) / 1e9, "frac_executed": exe / (ms / 1e3) / 1e9 / peak,
+                     "frac_vs_unfused": alg / (ms / 1e3) / 1e9 / peak,
+                     "note": "whole step at ms_per_step: executed = bytes the fused items must move; unfused = "
+                             "SURVEY 8(d) algorithmic bytes (every reference bucket's members + result, incl. "
+                             "intermediates the merged items never write)"},
+            "top_items_live": dom["top_items_live"],
+        },
         "cpu_baseline": cpu,
-        "e2e": {"value": world * args.steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": n_in,
-                "d2h_bytes_per_step": 16, "s_per_lightcone": t_e2e / args.steps,
-                "call": "paper_2210_15874_b200.contract_network(tn, order, Backend.b200(...)) from host Tensors",
-                "zz": v_e2e.real},
+        "e2e": {"value": world * args.steps / e2e[hd][0], "unit": UNIT, "h2d_bytes_per_step": h2d[hd],
+                "d2h_bytes_per_step": 16, "s_per_lightcone": e2e[hd][0] / args.steps,
+                "call": "paper_2210_15874_b200.contract_network(tn_k, order, Backend.b200(...)) from host Tensors, "
+                        "tn_k = the lightcone at QaoaParams.seeded(4, 1 + k % 8): new gate tensors every step",
+                "h2d_note": f"input image per step ({'complex128 + complex64 copies' if hd == 'complex64' else 'complex128'})"},
         "gpu_launches": args.steps * prog.n_nodes,
         "gpu_launches_note": f"{prog.n_nodes} kernels per step, issued as one CUDA graph launch",
         "clocks": clocks,
+        "clocks_sustained": sustained,
+        "strong": strong,
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.destroy_process_group()
+    finish(world)
     return 0
 
 
-def run_graph(args):
-    """Full MaxCut energy of the N=30, p=4 graph: 45 tight lightcones as
-    (cone) units, LPT-sharded over ranks, each rank's units batched into
-    device programs, per-step slot-vector all-reduce (NCCL at N > 1)."""
-    import torch
-    import torch.distributed as dist
+# ---------------------------------------------------------------------------
+# full graph (strong scaling)
+# ---------------------------------------------------------------------------
+def graph_setup(args, rank, world, local, dtype):
     import paper_2210_15874_b200 as Q
     from paper_2210_15874_b200 import distributed as D
-
-    rank, world, local = dist_setup(args.gpus)
-    torch.cuda.set_device(local)
-    dtype = "complex64" if args.dtype == "c64" else "complex128"
-    g = Q.random_regular_graph(30, 3, seed=0)
-    params = Q.QaoaParams.seeded(4, 0)
+    g = Q.random_regular_graph(N_QUBITS, DEGREE, seed=SEED)
+    params = Q.QaoaParams.seeded(P_LAYERS, SEED)
     be = Q.Backend.b200(dtype=dtype, device=local, profile=False)
     t0 = time.perf_counter()
     c = Q.qaoa_maxcut_circuit(g, params)
@@ -422,11 +573,19 @@ def run_graph(args):
     owner = D.lpt_assign([u.cost for u in plan.units], world)
     mine = [u for u in range(len(plan.units)) if owner[u] == rank]
     prep = D.prepare_local(plan, mine, be, local)
+    return g, params, be, cones, plan, prep, t_plan
+
+
+def graph_figure(args, rank, world, local, dtype, stream, flush):
+    """Full-graph energy (45 tight cones, LPT over the ranks, slot all-reduce)
+    device throughput at this N — the strong-scaling figure."""
+    import torch
+    import torch.distributed as dist
+    from paper_2210_15874_b200 import distributed as D
+    g, params, be, cones, plan, prep, t_plan = graph_setup(args, rank, world, local, dtype)
     n_units = len(plan.units)
     slots = torch.zeros(2 * n_units, dtype=torch.float64, device="cuda")
     idx = [torch.tensor([2 * u + q for u in batch for q in (0, 1)], device="cuda") for _, batch in prep.batches]
-    stream = torch.cuda.current_stream()
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     def step():
         D.launch_prepared(prep, stream)
@@ -436,31 +595,50 @@ def run_graph(args):
         if world > 1:
             dist.all_reduce(slots)
 
-    for _ in range(max(3, args.warmup)):
+    for _ in range(3):
         step()
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    with ClockSampler(local) as clk:
-        for i in range(args.steps):
-            flush.zero_()
-            evs[i][0].record(stream)
-            step()
-            evs[i][1].record(stream)
-        torch.cuda.synchronize()
-    t_dev = sum(a.elapsed_time(b) for a, b in evs) / 1e3
-    t_dev = max_over_ranks(t_dev, world)
+    barrier(world)
+    steps = max(3, min(args.steps, 20))
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
+        flush.zero_()
+        evs[i][0].record(stream)
+        step()
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    t = max_over_ranks(sum(a.elapsed_time(b) for a, b in evs) / 1e3, world)
     v = slots.cpu().numpy()
     zz = [0j] * len(cones)
     for u, unit in enumerate(plan.units):
         zz[unit.cone] += complex(v[2 * u], v[2 * u + 1])
     energy = sum(0.5 * (1 - z.real) for z in zz)
-    # e2e: the public API call qaoa_energy — first (cold) call with host
-    # planning, then an angle sweep (new angles every call: new tensors,
-    # same structure; plans and device programs reused, inputs re-staged)
-    if world > 1:
-        dist.barrier()
+    return {"metric": "lightcones/s (N=30,p=4 full-graph energy, 45 tight lightcones)",
+            "value": len(cones) * steps / t, "ms_per_energy": 1e3 * t / steps, "n_gpus": world, "dtype": dtype,
+            "scaling": "strong", "units": n_units, "energy": energy, "steps": steps,
+            "lpt_makespan_share": round(_lpt_share([u.cost for u in plan.units], world), 4),
+            "host_plan_s": round(t_plan, 3)}
+
+
+def run_graph(args):
+    """Full MaxCut energy of the N=30, p=4 graph: 45 tight lightcones as
+    (cone, slice) units, LPT-sharded over ranks, each rank's units batched
+    into device programs, per-step slot-vector all-reduce (NCCL at N > 1)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2210_15874_b200 as Q
+
+    rank, world, local = dist_setup()
+    torch.cuda.set_device(local)
+    dtype = "complex64" if args.dtype == "c64" else "complex128"
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    with ClockSampler(local) as clk:
+        fig = graph_figure(args, rank, world, local, dtype, stream, flush)
+    g = Q.random_regular_graph(N_QUBITS, DEGREE, seed=SEED)
+    params = Q.QaoaParams.seeded(P_LAYERS, SEED)
+    be = Q.Backend.b200(dtype=dtype, device=local, profile=False)
+    barrier(world)
     grp = dist.group.WORLD if world > 1 else None
     t0 = time.perf_counter()
     e_api = Q.qaoa_energy(g, params, be, cone="tight", group=grp, simplify=args.simplify, mem_cap=GRAPH_MEM_CAP,
@@ -470,49 +648,37 @@ def run_graph(args):
     n_sweep = max(2, min(args.steps, 5))
     t0 = time.perf_counter()
     for k in range(n_sweep):
-        Q.qaoa_energy(g, Q.QaoaParams.seeded(4, 100 + k), be, cone="tight", group=grp, simplify=args.simplify,
-                      mem_cap=GRAPH_MEM_CAP, balance_ranks=GRAPH_BALANCE)
+        Q.qaoa_energy(g, Q.QaoaParams.seeded(P_LAYERS, 100 + k), be, cone="tight", group=grp,
+                      simplify=args.simplify, mem_cap=GRAPH_MEM_CAP, balance_ranks=GRAPH_BALANCE)
     torch.cuda.synchronize()
     t_api = max_over_ranks((time.perf_counter() - t0) / n_sweep, world)
-    in_bytes = sum(plan.templates[u.cone].n_in_elems for u in plan.units) * (8 if dtype == "complex64" else 16)
     if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
+        finish(world)
         return 0
-    alg = sum(E_alg(plan, dtype))
     peak, peak_src = peak_hbm()
-    value = len(cones) * args.steps / t_dev
     line = {
-        "metric": "lightcones/s (N=30,p=4 full-graph energy, 45 lightcones)", "value": value, "unit": "lightcones/s",
-        "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": 1e3 * t_dev / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": args.dtype,
-        "data": "synthetic (seeded graph/angles)",
+        "metric": fig["metric"], "value": fig["value"], "unit": UNIT, "n_gpus": world, "steps": fig["steps"],
+        "warmup": 3, "ms_per_step": fig["ms_per_energy"], "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded graph/angles)",
         "config": {"workload": "graph: all 45 tight lightcones of the cfg-2 graph, over-wide cones sliced for 8-way "
-                               "balance, LPT over ranks, slot all-reduce",
-                   "lpt_makespan_share": {str(n): round(_lpt_share([u.cost for u in plan.units], n), 4)
-                                          for n in (1, 2, 4, 8)},
-                   "energy": energy, "units": n_units, "host_plan_s": t_plan,
-                   "l2": "flushed (256 MiB write) before every timed step"},
-        "roofline": {"bound": "hbm", "achieved": alg / (t_dev / args.steps) / 1e9 / world, "peak": peak,
-                     "unit": "GB/s", "frac": alg / (t_dev / args.steps) / 1e9 / world / peak, "traffic": None,
-                     "peak_source": peak_src, "note": "per-GPU average"},
+                               "balance, LPT over ranks, slot all-reduce", "l2": L2_NOTE},
+        "details": fig,
+        "roofline": None,
         "cpu_baseline": None,
-        "e2e": {"value": len(cones) / t_api, "unit": UNIT, "h2d_bytes_per_step": in_bytes,
-                "d2h_bytes_per_step": 16 * n_units,
-                "call": f"qaoa_energy(g, QaoaParams.seeded(4, 100+k), backend, cone='tight', simplify={args.simplify}): "
-                        f"angle sweep of {n_sweep} calls (every call: the cones' input tensors for the new angles "
-                        "(from the angle recipe; lightcone networks rebuilt only with simplify), host gather, upload "
-                        "and result read-back; plans and CUDA graphs reused)",
-                "cold_call_s": t_cold, "energy": e_api},
-        "gpu_launches": args.steps * sum(ex.prog.n_nodes for ex, _ in prep.batches),
+        "e2e": {"value": 45 / t_api, "unit": UNIT, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+                "call": f"qaoa_energy(g, QaoaParams.seeded(4, 100+k), backend, cone='tight'): angle sweep of "
+                        f"{n_sweep} calls", "cold_call_s": t_cold, "energy": e_api},
+        "gpu_launches": None,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    finish(world)
     return 0
 
 
+# ---------------------------------------------------------------------------
+# cfg-5 bucket microbench (K3)
+# ---------------------------------------------------------------------------
 BUCKET_CASES = [(w, cls, k) for w in (24, 26, 28) for cls, k in (("A", 3), ("A", 6), ("B", 2))]
 
 
@@ -520,7 +686,7 @@ def run_bucket(args):
     """cfg 5 (BASELINE.json configs[4]): synthetic buckets of random complex
     tensors over binary indices in random axis permutations, one bucket index
     contracted by K3 (csrc/bucket_strided.cu).  A step = one launch per case
-    of BUCKET_CASES; value = algorithmic bytes of all cases / device time
+    of BUCKET_CASES; value = compulsory bytes of all cases / device time
     (every member read once, result written once; inputs > L2 and L2
     flushed between launches)."""
     import torch
@@ -529,7 +695,7 @@ def run_bucket(args):
     from paper_2210_15874_b200 import engine as E
     from paper_2210_15874_b200 import workloads as W
 
-    rank, world, local = dist_setup(args.gpus)
+    rank, world, local = dist_setup()
     torch.cuda.set_device(local)
     dtype = "complex64" if args.dtype == "c64" else "complex128"
     esz = E.ELEM_BYTES[dtype]
@@ -548,8 +714,7 @@ def run_bucket(args):
         for c in cases:
             N.bucket_launch(c["desc"], stream.cuda_stream)
     torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
+    barrier(world)
     evs = []
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
@@ -566,7 +731,6 @@ def run_bucket(args):
         c["t"] += e0.elapsed_time(e1) / 1e3
     t_dev = max_over_ranks(sum(c["t"] for c in cases), world)
     tot_bytes = sum(c["bytes"] for c in cases) * args.steps
-    # e2e: the public call with host Tensors (upload members, download result)
     we, ke = 22, 3
     host = [Q.Tensor(i, d) for i, d in W.synthetic_bucket(we, ke, "A", 0)]
     be = Q.Backend.b200(dtype=dtype, device=local, profile=False)
@@ -575,10 +739,11 @@ def run_bucket(args):
     n_e2e = max(2, min(args.steps, 5))
     t0 = time.perf_counter()
     for _ in range(n_e2e):
-        res, _ = Q.contract_bucket(bh, be)
+        Q.contract_bucket(bh, be)
     t_e2e = max_over_ranks((time.perf_counter() - t0) / n_e2e, world)
     e2e_bytes = (sum(1 << len(t.indices) for t in host) + (1 << we)) * esz
     if rank != 0:
+        finish(world)
         return 0
     peak, peak_src = peak_hbm()
     value = world * tot_bytes / t_dev / 1e9
@@ -611,6 +776,27 @@ def run_bucket(args):
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
+    finish(world)
+    return 0
+
+
+def run_selftest(args):
+    """The multi-rank harness without a GPU (gloo): rendezvous, barrier,
+    max-over-ranks and the slot-vector all-reduce exactly as the GPU
+    workloads use them, on a deterministic per-rank value."""
+    import torch
+    import torch.distributed as dist
+    rank, world, _ = dist_setup()
+    t = max_over_ranks(0.001 * (rank + 1), world)
+    slots = torch.zeros(2 * world, dtype=torch.float64)
+    slots[2 * rank: 2 * rank + 2] = torch.tensor([rank + 1.0, -(rank + 1.0)], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(slots)
+    barrier(world)
+    if rank == 0:
+        print(json.dumps({"selftest": True, "n_ranks": world, "max_over_ranks": t,
+                          "slots": slots.tolist(), "backend": dist.get_backend() if world > 1 else None}), flush=True)
+    finish(world)
     return 0
 
 
@@ -625,15 +811,15 @@ def _lpt_share(costs, n):
     return max(load) / max(1, sum(costs))
 
 
-def E_alg(plan, dtype):
-    from paper_2210_15874_b200 import engine as E
-    return [E.algorithmic_bytes(plan.templates[u.cone], dtype) for u in plan.units]
-
-
-def main():
-    args = parse()
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus, argv)
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "selftest":
+        return run_selftest(args)
     if args.workload == "graph":
         return run_graph(args)
     if args.workload == "bucket":

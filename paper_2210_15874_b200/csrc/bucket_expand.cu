@@ -312,15 +312,33 @@ int make_plan(const qtn_bucket_desc_t* d, int min_e, Plan* P, int* smem) {
   }
   const qtn_bmember_t& B = d->mem[iB];
   int tb[TBB], nt = 0, eb[MAXE], ne = 0;
-  for (int b = 0; b < w; ++b) {
+  bool carried[64] = {};   // result bits some other member carries
+  for (int b = 0; b < w; ++b)
+    for (int i = 0; i < nm; ++i)
+      if (i != iB && d->mem[i].strides[b] != 0) carried[b] = true;
+  for (int b = 0; b < w; ++b)
     if (B.strides[b] == 0) {
       if (ne == MAXE) return fail(QTN_E_UNSUPPORTED, "K4: more than %d expansion bits", MAXE);
       eb[ne++] = b;
-    } else if (nt < TBB) {
-      tb[nt++] = b;
     }
+  if (w - ne < TBB) return fail(QTN_E_UNSUPPORTED, "K4: dominant member has %d result bits", best);
+  // Thread bits.  Lanes (the first 5): B's fastest axes first — one 32-byte
+  // sector of B per lane group (2 complex128 / 4 complex64 elements) — then
+  // B bits NO other member carries, so every lane of a warp reads the same
+  // product-table row (shared-memory broadcast instead of bank conflicts);
+  // then the remaining B bits, ascending.  Warps: the next 3.
+  {
+    bool used[64] = {};
+    const int sec = (int)(32 / esz);
+    auto take = [&](int b) { tb[nt++] = b; used[b] = true; };
+    for (int b = 0; b < w && nt < TBB; ++b)   // B's local axes 0 .. log2(sec)-1
+      if (B.strides[b] != 0 && B.strides[b] < sec) take(b);
+    for (int pass = 0; pass < 2; ++pass)
+      for (int b = 0; b < w && nt < 5; ++b)
+        if (B.strides[b] != 0 && !used[b] && (pass == 1 || !carried[b])) take(b);
+    for (int b = 0; b < w && nt < TBB; ++b)
+      if (B.strides[b] != 0 && !used[b]) take(b);
   }
-  if (nt < TBB) return fail(QTN_E_UNSUPPORTED, "K4: dominant member has %d result bits", best);
   if (ne < min_e) return fail(QTN_E_UNSUPPORTED, "K4: %d expansion bits", ne);
   // tile bits T = tb u eb; F bits = T bits any other member carries
   bool inT[64] = {};

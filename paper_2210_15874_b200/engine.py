@@ -880,11 +880,43 @@ class Program:
     def executed_bytes(self) -> int:
         return sum(executed_bytes(inst.template, self.dtype) for inst in self.instances)
 
+    def item_bytes(self, gid) -> int:
+        """Compulsory bytes of device item `gid`: each member read once, the
+        result written once (the item's roofline numerator)."""
+        b = self.buckets[gid]
+        if int(b["w"]) < 0:
+            return 0
+        mem = self.members[b["mem_begin"]: b["mem_begin"] + b["n_mem"]]
+        n = (1 << int(b["w"])) + sum(1 << (_popc(int(m["mask"])) + _popc(int(m["smask"]))) for m in mem)
+        return n * ELEM_BYTES[self.dtype]
+
+    def node_of_item(self):
+        """gid -> graph node index."""
+        out = {}
+        for ni, nd in enumerate(self.nodes):
+            for g in range(int(nd["first"]), int(nd["first"]) + int(nd["count"])):
+                out[g] = ni
+        return out
+
     def describe(self):
         kinds = self.nodes["kind"]
         return {"items": int(self.n_buckets), "nodes": int(self.n_nodes),
                 "small_stages": int((kinds == N.QTN_NODE_SMALL).sum()),
                 "large_items": int((kinds == N.QTN_NODE_LARGE).sum())}
+
+
+class _OwnedGraph:
+    """A qtn_graph_t destroyed with its Python owner."""
+
+    def __init__(self, g):
+        self.g = g
+
+    def __del__(self):
+        if self.g is not None and self.g.value:
+            try:
+                N.load().qtn_graph_destroy(self.g)
+            except Exception:
+                pass
 
 
 class Executor:
@@ -1007,6 +1039,32 @@ class Executor:
         c = (ctypes.c_int32 * max(n, 1))()
         N.check(N.load().qtn_graph_node_kinds(g, c, n))
         return [("K1", "K2", "K3", "K4")[c[i]] for i in range(n)]
+
+    def node_graph(self, ni):
+        """A graph of node `ni` alone (no dependencies; the same kernel and
+        launch configuration the program graph runs it with): times one
+        kernel in isolation, its inputs left in the arena by an earlier run."""
+        nd = np.array(self.prog.nodes[ni: ni + 1]).copy()
+        nd["dep_begin"] = 0
+        nd["n_dep"] = 0
+        if int(nd["kind"][0]) == N.QTN_NODE_SMALL:
+            raise ValueError("node_graph: K2 stages depend on their control words; time large nodes only")
+        deps = np.zeros(1, np.int32)
+        items = np.ascontiguousarray(self.prog.buckets)
+        mems = np.ascontiguousarray(self.prog.members)
+        g = ctypes.c_void_p()
+        with self.torch.cuda.device(self.device):
+            N.check(N.load().qtn_graph_create_host(
+                ctypes.byref(self.c), items.ctypes.data_as(ctypes.c_void_p), mems.ctypes.data_as(ctypes.c_void_p),
+                len(mems), nd.ctypes.data_as(ctypes.c_void_p), 1, deps.ctypes.data_as(ctypes.c_void_p), None,
+                ctypes.byref(g)))
+        kinds = (ctypes.c_int32 * 1)()
+        N.check(N.load().qtn_graph_node_kinds(g, kinds, 1))
+        return _OwnedGraph(g), ("K1", "K2", "K3", "K4")[kinds[0]]
+
+    def launch_graph(self, g, stream=None):
+        s = stream if stream is not None else self.torch.cuda.current_stream(self.device)
+        N.check(N.load().qtn_graph_launch(g.g, ctypes.c_void_p(s.cuda_stream)))
 
     @property
     def graph(self):

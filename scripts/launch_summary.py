@@ -1,23 +1,30 @@
-"""Per-kernel table of one cfg-2 program step from an ncu launch list
-(`ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
---csv --log-file ... python bench.py --steps 1 --warmup 1`): the first
-complex64 program launch (K2 small_kernel stages, K1 large_kernel items, K4
-k4_kernel expansion items),
-durations and DRAM bytes per kernel, cold-cache and serialised by ncu.
+"""Per-kernel table of ONE cfg-2 program step from an ncu launch list.
 
-usage: python scripts/launch_summary.py nodes.csv [graph.csv] > profiles/<name>.md"""
+    ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+        --clock-control none --csv --log-file nodes.csv \
+        python scripts/one_step.py c128          # exactly one program launch
+    python scripts/launch_summary.py nodes.csv <n_nodes> [c128|c64] > profiles/<name>.md
+
+Every kernel of this library is matched (K2 small_kernel, K1
+large_kernel_c64/_c128, K3 k3_kernel/k3v2_kernel, K4 k4_kernel_c64/_c128);
+the first <n_nodes> of them are the step (scripts/one_step.py prints the
+program's node count).  Times are ncu's: cold L2, serialised node by node —
+the SHARE of each kernel is what compares with the live bench."""
 import csv
 import re
 import sys
 
+FAMILIES = r"(small_kernel|large_kernel_c64|large_kernel_c128|k3v2_kernel|k3_kernel|k4_kernel_c64|k4_kernel_c128)"
+FAMILY_OF = {"small_kernel": "K2", "large_kernel_c64": "K1", "large_kernel_c128": "K1", "k3v2_kernel": "K3",
+             "k3_kernel": "K3", "k4_kernel_c64": "K4", "k4_kernel_c128": "K4"}
+
 
 def rows(path):
     with open(path) as f:
-        lines = [l for l in f if l.startswith('"')]
+        lines = [ln for ln in f if ln.startswith('"')]
     r = list(csv.reader(lines))
     h = r[0]
-    out = {}
-    order = []
+    out, order = {}, []
     for row in r[1:]:
         d = dict(zip(h, row))
         key = d["ID"]
@@ -25,52 +32,46 @@ def rows(path):
             out[key] = {"name": d["Kernel Name"], "grid": d["Grid Size"]}
             order.append(key)
         v = float(d["Metric Value"].replace(",", "")) if d["Metric Value"] else 0.0
-        unit = d["Metric Unit"]
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-                 "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}.get(unit, 1.0)
+                 "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}.get(d["Metric Unit"], 1.0)
         out[key][d["Metric Name"]] = v * scale
     return [out[k] for k in order]
 
 
+def family(name):
+    m = re.search(FAMILIES + r"\b", name)
+    return m.group(1) if m else None
+
+
 def short(name):
-    m = re.search(r"(large_kernel_c64|large_kernel_c128|large_kernel|small_kernel|k4_kernel|k3v2_kernel)<([^>]*)>", name)
-    return f"{m.group(1)}<{m.group(2).replace('(int)', '')}>" if m else name[:60]
+    m = re.search(FAMILIES + r"(<[^()]*>)?", name)
+    return (m.group(1) + (m.group(2) or "")).replace("(int)", "") if m else name[:60]
 
 
 def main():
     ks = rows(sys.argv[1])
-    fam = ("large_kernel_c64<", "large_kernel<float", "small_kernel<float", "k4_kernel<float", "k3v2_kernel<float")
-    ours = [k for k in ks if any(f in k["name"] for f in fam)]
-    # the first program launch: its node count (bench.py config.program.nodes)
-    n = int(sys.argv[3]) if len(sys.argv) > 3 else 21
+    n = int(sys.argv[2])
+    dt = sys.argv[3] if len(sys.argv) > 3 else "c128"
+    ours = [k for k in ks if family(k["name"])]
     step = ours[:n]
+    assert len(step) == n, f"launch list holds {len(step)} of our kernels, expected {n}"
     tot_t = sum(k["gpu__time_duration.sum"] for k in step)
-    tot_b = sum(k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"] for k in step)
-    print("# cfg-2 lightcone, one complex64 program step: per-kernel ncu launch list\n")
+    tot_b = sum(k.get("dram__bytes_read.sum", 0) + k.get("dram__bytes_write.sum", 0) for k in step)
+    print(f"# cfg-2 lightcone, one {dt} program step: per-kernel ncu launch list\n")
     print("Source: `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
-          "--clock-control none` of `bench.py --steps 1 --warmup 1` (graph nodes profiled one by one: "
-          "cold L2, serialised; shares, not absolute times, compare with the live bench).\n")
-    print("| # | kernel | grid | us | DRAM read MB | DRAM write MB | GB/s | share of step |")
-    print("|---|---|---|---|---|---|---|---|")
+          "--clock-control none` of `scripts/one_step.py` (exactly one program launch; graph nodes profiled one by "
+          "one: cold L2, serialised — shares, not absolute times, compare with the live bench).\n")
+    print("| # | family | kernel | grid | us | DRAM read MB | DRAM write MB | GB/s | share of step |")
+    print("|---|---|---|---|---|---|---|---|---|")
     for i, k in enumerate(step):
         t = k["gpu__time_duration.sum"]
-        b = k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"]
-        print(f"| {i} | {short(k['name'])} | {k['grid']} | {t * 1e6:.1f} | {k['dram__bytes_read.sum'] / 1e6:.1f} | "
-              f"{k['dram__bytes_write.sum'] / 1e6:.1f} | {b / t / 1e9:.0f} | {100 * t / tot_t:.1f}% |")
+        rd, wr = k.get("dram__bytes_read.sum", 0), k.get("dram__bytes_write.sum", 0)
+        print(f"| {i} | {FAMILY_OF[family(k['name'])]} | {short(k['name'])} | {k['grid']} | {t * 1e6:.1f} | "
+              f"{rd / 1e6:.1f} | {wr / 1e6:.1f} | {(rd + wr) / t / 1e9:.0f} | {100 * t / tot_t:.1f}% |")
     print(f"\nSum: {tot_t * 1e6:.1f} us serialised, {tot_b / 1e9:.3f} GB DRAM.")
     dom = max(step, key=lambda k: k["gpu__time_duration.sum"])
-    print(f"Dominant kernel: {short(dom['name'])}, {100 * dom['gpu__time_duration.sum'] / tot_t:.1f}% of the "
-          f"serialised step.")
-    if len(sys.argv) > 2 and sys.argv[2] != "-":
-        g = rows(sys.argv[2])
-        g = [k for k in g if k["name"] == "graph" and "dram__bytes_read.sum" in k]
-        if g:
-            # graph-level profiling: one row per graph launch; the first is the first c64 step
-            k = g[0]
-            b = k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"]
-            print(f"\nWhole graph (ncu --graph-profiling graph, first launch): {k['gpu__time_duration.sum'] * 1e6:.1f} us, "
-                  f"DRAM {b / 1e9:.3f} GB (read {k['dram__bytes_read.sum'] / 1e9:.3f}, write "
-                  f"{k['dram__bytes_write.sum'] / 1e9:.3f}).")
+    print(f"Dominant kernel: {FAMILY_OF[family(dom['name'])]} {short(dom['name'])}, "
+          f"{100 * dom['gpu__time_duration.sum'] / tot_t:.1f}% of the serialised step.")
 
 
 if __name__ == "__main__":
