@@ -10,7 +10,6 @@ per batch; the get-result scalar is the program's finaliser slot.
 from __future__ import annotations
 
 import heapq
-import operator
 import threading
 from collections import OrderedDict
 from dataclasses import dataclass
@@ -238,47 +237,28 @@ PLAN_CACHE = _PlanCache()
 
 
 class _NetworkInputs:
-    """Per-network host staging cache: the structure key (index tuples) and
-    the raw concatenation of the tensor data, valid while `tn.tensors` holds
-    the very same Tensor objects (Tensors are immutable — read-only data —
-    so identical objects mean identical values).  A network whose tensor list
-    was changed, or a new network (e.g. the next point of a parameter sweep),
-    is re-read.  Small LRU keyed by id(tn)."""
+    """Per-network host inputs: the structure (index tuples), the raw
+    concatenation of the tensor data (TensorNetwork.packed(), valid while
+    `tn.tensors` holds the very same immutable Tensor objects) and the plans
+    dict.  Plans are shared by every network of one structure (a parameter
+    sweep builds a new network per point with the same indices), so a new
+    network costs one structure lookup, not a re-plan."""
 
-    def __init__(self, cap=16):
+    def __init__(self, cap=64):
         self.cap = cap
-        self.d = OrderedDict()
+        self.plans = OrderedDict()   # structure -> {(order, fixed, dtype, threshold): (key, Template)}
         self.lock = threading.Lock()
 
-    @staticmethod
-    def _same(snap, ts):
-        # Tensor has identity equality, so list == list is an element-wise
-        # identity check in C (~1 us for cfg-2's 564 tensors)
-        try:
-            return snap == (ts if isinstance(ts, list) else list(ts))
-        except Exception:
-            return len(snap) == len(ts) and all(map(operator.is_, snap, ts))
-
     def get(self, tn):
-        ts = tn.tensors
+        snap, struct, raw = tn.packed()
         with self.lock:
-            hit = self.d.get(id(tn))
-            if hit is not None and hit[0] is tn and len(hit[1]) == len(ts) and self._same(hit[1], ts):
-                self.d.move_to_end(id(tn))
-                return hit[2], hit[3], hit[4]
-        snap = list(ts)
-        struct = tuple(t.indices for t in snap)
-        parts = [t.data.ravel() for t in snap]
-        raw = np.concatenate(parts) if parts else np.zeros(0, np.complex128)
-        if raw.dtype != np.complex128:
-            raw = raw.astype(np.complex128)
-        raw.setflags(write=False)
-        plans = {}   # (order, fixed, dtype) -> (key, template) for this network
-        with self.lock:
-            self.d[id(tn)] = (tn, snap, struct, raw, plans)
-            self.d.move_to_end(id(tn))
-            while len(self.d) > self.cap:
-                self.d.popitem(last=False)
+            plans = self.plans.get(struct)
+            if plans is None:
+                plans = self.plans[struct] = {}
+                while len(self.plans) > self.cap:
+                    self.plans.popitem(last=False)
+            else:
+                self.plans.move_to_end(struct)
         return struct, raw, plans
 
 

@@ -36,6 +36,27 @@ class TensorNetwork:
     tensors: list
     open_indices: tuple = ()
 
+    def packed(self):
+        """(snapshot, structure, raw): the tensor list as it stands, its index
+        tuples and the raw concatenation of the (immutable) tensor data — the
+        host image the device gather reads.  Cached while `tensors` holds the
+        very same Tensor objects; the network builders pack eagerly, so the
+        contraction call only validates the snapshot (one identity compare)."""
+        ts = self.tensors
+        pk = self.__dict__.get("_pk")
+        if pk is not None and len(pk[0]) == len(ts) and pk[0] == (ts if isinstance(ts, list) else list(ts)):
+            return pk
+        snap = list(ts)
+        struct = tuple(t.indices for t in snap)
+        parts = [np.asarray(t.data).ravel() for t in snap]
+        raw = np.concatenate(parts) if parts else np.zeros(0, np.complex128)
+        if raw.dtype != np.complex128:
+            raw = raw.astype(np.complex128)
+        raw.setflags(write=False)
+        pk = (snap, struct, raw)
+        self.__dict__["_pk"] = pk
+        return pk
+
     def all_indices(self):
         ids = set()
         for t in self.tensors:
@@ -125,7 +146,9 @@ def amplitude_network(c: Circuit, bitstring) -> TensorNetwork:
         proj = np.zeros(2, dtype=np.complex128)
         proj[b] = 1.0
         ts.append(Tensor((wires.live[q],), proj))
-    return TensorNetwork(ts)
+    tn = TensorNetwork(ts)
+    tn.packed()
+    return tn
 
 
 @dataclass(frozen=True)
@@ -222,7 +245,9 @@ def _sandwich(gates, edge, qubits) -> TensorNetwork:
         _add_gate(ts, wires, g, adjoint=True)
     for q in qs:
         ts.append(Tensor((wires.live[q],), _KET0))
-    return TensorNetwork(ts)
+    tn = TensorNetwork(ts)
+    tn.packed()
+    return tn
 
 
 def zz_sandwich_network(c: Circuit, edge, prune: bool = True) -> TensorNetwork:
