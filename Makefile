@@ -5,18 +5,18 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude
 LIB := paper_2210_15874_b200/lib/libqtn_b200.so
 CSRC := paper_2210_15874_b200/csrc
-SRC := $(CSRC)/qtn_b200.cu $(CSRC)/bucket_strided.cu $(CSRC)/bucket_expand.cu $(CSRC)/planner.cpp $(CSRC)/plan_template.cpp
+SRC := $(CSRC)/qtn_b200.cu $(CSRC)/bucket_strided.cu $(CSRC)/bucket_expand.cu $(CSRC)/bucket_stream.cu $(CSRC)/planner.cpp $(CSRC)/plan_template.cpp
 OBJDIR := build/obj
 OBJ := $(patsubst $(CSRC)/%,$(OBJDIR)/%.o,$(SRC))
 DBGOBJ := $(patsubst $(CSRC)/%,$(OBJDIR)/debug/%.o,$(SRC))
 
 all: $(LIB)
 
-$(OBJDIR)/%.o: $(CSRC)/% include/qtn_b200.h
+$(OBJDIR)/%.o: $(CSRC)/% include/qtn_b200.h $(CSRC)/knobs.h
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) $(EXTRA) -c -o $@ $<
 
-$(OBJDIR)/debug/%.o: $(CSRC)/% include/qtn_b200.h
+$(OBJDIR)/debug/%.o: $(CSRC)/% include/qtn_b200.h $(CSRC)/knobs.h
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -DQTN_DEBUG -c -o $@ $<
 

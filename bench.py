@@ -445,6 +445,7 @@ def sustained_clocks(lcp, stream, flush, seconds, local):
 def run_ours(args):
     import torch
     import paper_2210_15874_b200 as Q
+    from paper_2210_15874_b200 import _native as N
 
     rank, world, local = dist_setup()
     torch.cuda.set_device(local)
@@ -516,6 +517,7 @@ def run_ours(args):
                            (", per-rank <ZZ> slots all-reduced (NCCL) inside the step" if world > 1 else ""),
             "l2": L2_NOTE, "zz": val[hd].real, "program": prog.describe(),
             "kernel_mix": progs[hd].ex.kernel_mix(io=False),
+            "route_config": N.route_config(),
             "algorithmic_bytes_per_step": alg, "executed_bytes_per_step": exe,
             "vs_baseline_ref": "value x 2.1 s: speed-up over the paper's best single-lightcone time "
                                "(NumPy+CuPy mixed on V100, PAPER.md:64)",

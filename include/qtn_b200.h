@@ -163,6 +163,10 @@ typedef struct qtn_graph qtn_graph_t;
 
 /* ABI version (QTN_ABI_VERSION). */
 int qtn_abi_version(void);
+/* The routing / tuning knobs in effect ("name=value ..."): measured defaults,
+ * overridden only by validated QTN_* environment variables read once per
+ * process (csrc/knobs.h). */
+const char* qtn_route_config(void);
 /* Last error message of the calling thread ("" if none). */
 const char* qtn_last_error(void);
 /* Number of visible CUDA devices (0 on a CPU-only host; never fails). */
@@ -201,11 +205,11 @@ int qtn_graph_create_host(const qtn_program_t* prog, const qtn_bucket_t* host_it
 /* Launch the instantiated graph (one call per program execution). */
 int qtn_graph_launch(qtn_graph_t* g, void* stream);
 int qtn_graph_destroy(qtn_graph_t* g);
-/* Kernel mix of a built graph: counts[4] = nodes run by K1 (fused large-item
- * kernels), K2 (small-item stages), K3 (permutation-aware bucket kernel) and
- * K4 (expansion-item kernel). */
+/* Kernel mix of a built graph: counts[5] = nodes run by K1 (fused large-item
+ * kernels), K2 (small-item stages), K3 (permutation-aware bucket kernel), K4
+ * (expansion-item kernel) and K5 (streaming-item kernel). */
 int qtn_graph_kinds(const qtn_graph_t* g, int32_t* counts);
-/* Per node (n = the graph's node count): 0 K1, 1 K2, 2 K3, 3 K4. */
+/* Per node (n = the graph's node count): 0 K1, 1 K2, 2 K3, 3 K4, 4 K5. */
 int qtn_graph_node_kinds(const qtn_graph_t* g, int32_t* kinds, int32_t n);
 /* Host planning (no device needed): the greedy min-fill (heuristic 0) or
  * min-degree (1) elimination order of a network given as CSR index lists
@@ -313,6 +317,14 @@ int qtn_bucket_plan(const qtn_bucket_desc_t* desc, int32_t* info);
  * table (csrc/bucket_expand.cu).  Program graphs route their expansion items
  * here (QTN_K4).  QTN_E_UNSUPPORTED when the bucket is not such an expansion. */
 int qtn_bucket_expand(const qtn_bucket_desc_t* desc, int32_t min_e, void* stream);
+
+/* ---- K5: a streaming bucket (one member carries every result bit) ----
+ * Same contraction for a descriptor in which one member carries all w
+ * result bits (k in 1..3, at most 4 members carry result bits, w >= 8 / 9 at
+ * complex128 / complex64): that member is streamed once, the others read
+ * directly through L1/L2 (csrc/bucket_stream.cu).  Program graphs route
+ * their streaming items here (QTN_K5).  QTN_E_UNSUPPORTED otherwise. */
+int qtn_bucket_stream(const qtn_bucket_desc_t* desc, void* stream);
 
 #ifdef __cplusplus
 }

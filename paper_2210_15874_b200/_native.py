@@ -30,6 +30,8 @@ ABI_VERSION = 9
 QTN_NODE_SMALL = 0
 QTN_NODE_LARGE = 1
 QTN_VARIANT_GENERIC = -1
+# graph node kernel families (qtn_graph_node_kinds codes 0..4)
+KERNEL_FAMILIES = ("K1", "K2", "K3", "K4", "K5")
 
 # every symbol include/qtn_b200.h declares
 EXPORTS = (
@@ -43,6 +45,8 @@ EXPORTS = (
     "qtn_graph_create_host",
     "qtn_graph_kinds",
     "qtn_bucket_expand",
+    "qtn_bucket_stream",
+    "qtn_route_config",
     "qtn_graph_node_kinds",
     "qtn_graph_launch",
     "qtn_graph_destroy",
@@ -150,6 +154,10 @@ def load(path: str = LIB_PATH):
     lib.qtn_graph_node_kinds.argtypes = [vp, vp, i32]
     lib.qtn_bucket_expand.restype = ctypes.c_int
     lib.qtn_bucket_expand.argtypes = [ctypes.POINTER(BucketDescC), i32, vp]
+    lib.qtn_bucket_stream.restype = ctypes.c_int
+    lib.qtn_bucket_stream.argtypes = [ctypes.POINTER(BucketDescC), vp]
+    lib.qtn_route_config.restype = ctypes.c_char_p
+    lib.qtn_route_config.argtypes = []
     lib.qtn_graph_kinds.restype = ctypes.c_int
     lib.qtn_graph_kinds.argtypes = [vp, vp]
     lib.qtn_graph_create_host.restype = ctypes.c_int
@@ -265,6 +273,19 @@ def bucket_expand_launch(desc, stream, min_e=0):
     descriptor is not an expansion of one dominant member)."""
     lib = require_device()
     check(lib.qtn_bucket_expand(ctypes.byref(desc), int(min_e), ctypes.c_void_p(stream)))
+
+
+def bucket_stream_launch(desc, stream):
+    """K5 on one streaming bucket (QTN_E_UNSUPPORTED -> NativeError when no
+    member carries every result bit)."""
+    lib = require_device()
+    check(lib.qtn_bucket_stream(ctypes.byref(desc), ctypes.c_void_p(stream)))
+
+
+def route_config() -> dict:
+    """The routing / tuning knobs in effect (qtn_route_config)."""
+    txt = load().qtn_route_config().decode()
+    return {k: int(v) for k, v in (kv.split("=") for kv in txt.split())}
 
 
 def plan_build(index_lists, order, fixed, params):

@@ -29,6 +29,7 @@
 // out[r] = prod_i m_i(s=0, r) + prod_i m_i(s=1, r), members multiplied in
 // bucket order (the reference's buf *= T_i, then buf.sum(axis=0)).
 #include "qtn_b200.h"
+#include "knobs.h"
 
 #include <cuda_runtime.h>
 
@@ -727,7 +728,7 @@ int make_plan(const qtn_bucket_desc_t* d, Plan* P, int* smem_bytes) {
   // ---- tile bits ----
   // A thread owns results tid + j * NT: tile bits 0..7 ("core") come from
   // tid, bits 8.. ("j bits") from j < NJ = 8 (c64) / 4 (c128).
-  static const int tcap_env = getenv("QTN_K3_TCAP") ? atoi(getenv("QTN_K3_TCAP")) : 0;
+  const int tcap_env = qtn_knobs().k3_tcap;
   // local bits (tile + summed) stay <= 13: the staging tables are 6 + 7 bits
   const int tcap = std::min(std::min(d->dtype == QTN_C64 ? 11 : 10, 13 - ks), tcap_env > 0 ? tcap_env : 99);
   const int nt_target = std::min(tcap, w);
@@ -749,7 +750,7 @@ int make_plan(const qtn_bucket_desc_t* d, Plan* P, int* smem_bytes) {
     }
     return tot;
   };
-  static const int budget_kb = getenv("QTN_K3_STAGE_KB") ? atoi(getenv("QTN_K3_STAGE_KB")) : 40;
+  const int budget_kb = qtn_knobs().k3_stage_kb;
   const int64_t budget = (budget_kb * 1024) / esz;   // one stage; two are resident
   auto add = [&](int b, bool check) {
     if (b >= w || inT[b] || nt >= tcap) return false;
@@ -766,7 +767,7 @@ int make_plan(const qtn_bucket_desc_t* d, Plan* P, int* smem_bytes) {
   int ord[MAXM];
   for (int i = 0; i < nm; ++i) ord[i] = i;
   std::stable_sort(ord, ord + nm, [&](int a, int b) { return rank[a] > rank[b]; });
-  static const int run_bytes = getenv("QTN_K3_RUN") ? atoi(getenv("QTN_K3_RUN")) : 128;
+  const int run_bytes = qtn_knobs().k3_run;
   const int64_t run_target = std::max(1, run_bytes / esz);
   for (int oi = 0; oi < nm; ++oi) {
     const qtn_bmember_t& m = d->mem[ord[oi]];
@@ -792,14 +793,14 @@ int make_plan(const qtn_bucket_desc_t* d, Plan* P, int* smem_bytes) {
   for (int i = 1; i < nm; ++i)
     if (__builtin_popcount(member_tbits(i)) > __builtin_popcount(member_tbits(imax))) imax = i;
   bool folded[MAXM] = {};
-  static const bool v2_off = getenv("QTN_K3_V1") && atoi(getenv("QTN_K3_V1"));
+  const bool v2_off = qtn_knobs().k3_v1 != 0;
   if (!v2_off) {
     int cand[MAXM], nc = 0;
     for (int i = 0; i < nm; ++i)
       if (i != imax && rank[i] <= 12) cand[nc++] = i;
     std::stable_sort(cand, cand + nc,
                      [&](int a, int b) { return __builtin_popcount(member_tbits(a)) < __builtin_popcount(member_tbits(b)); });
-    static const int ulim_env = getenv("QTN_K3_ULIM") ? atoi(getenv("QTN_K3_ULIM")) : 5;
+    const int ulim_env = qtn_knobs().k3_ulim;
     const int ulim = std::min(ulim_env, std::max(0, core - 2));
     uint32_t U = 0;
     for (int c = 0; c < nc; ++c) {
@@ -842,7 +843,7 @@ int make_plan(const qtn_bucket_desc_t* d, Plan* P, int* smem_bytes) {
       if (folded[i]) avoid_f |= member_bits(i);
     avoid = avoid_f;
     // level 2: F and one staged member invariant, when enough bits remain for j
-    static const bool inv2_off = getenv("QTN_K3_INV2") && atoi(getenv("QTN_K3_INV2")) == 0;
+    const bool inv2_off = qtn_knobs().k3_inv2 == 0;
     if (!inv2_off && nb >= 2 && inv_cand >= 0) {
       const uint64_t a2 = avoid_f | member_bits(inv_cand);
       int free_bits = 0;

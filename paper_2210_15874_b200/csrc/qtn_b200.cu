@@ -34,6 +34,7 @@
 //
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo ...
 #include "qtn_b200.h"
+#include "knobs.h"
 
 #include <cuda_runtime.h>
 
@@ -1072,6 +1073,9 @@ int qtn_internal_set_error(int code, const char* msg) { return set_err(code, "%s
 // members K1 would gather per tile
 size_t qtn_k3_plan_bytes();
 size_t qtn_k4_plan_bytes();
+size_t qtn_k5_plan_bytes();
+int qtn_k5_node(const qtn_bucket_desc_t* d, unsigned long long* timing, int32_t item, void* plan, const void** fn,
+                int* grid, int* smem);
 int qtn_k4_node(const qtn_bucket_desc_t* d, int min_e, unsigned long long* timing, int32_t item, void* plan,
                 const void** fn, int* grid, int* smem);
 int qtn_k3_node(const qtn_bucket_desc_t* d, unsigned long long* timing, int32_t item, void* plan, const void** fn,
@@ -1079,10 +1083,36 @@ int qtn_k3_node(const qtn_bucket_desc_t* d, unsigned long long* timing, int32_t 
 
 namespace {
 
-int getenv_int(const char* name, int dflt) {
+// one knob: the environment value if it parses as an integer in [lo, hi],
+// else the default (a rejected value is reported once on stderr)
+int knob(const char* name, int dflt, int lo, int hi) {
   const char* v = getenv(name);
-  return v && v[0] ? atoi(v) : dflt;
+  if (!v || !v[0]) return dflt;
+  char* end = nullptr;
+  const long x = strtol(v, &end, 10);
+  if (*end != '\0' || x < lo || x > hi) {
+    fprintf(stderr, "qtn_b200: ignoring %s=%s (integer in [%d, %d] expected); using %d\n", name, v, lo, hi, dflt);
+    return dflt;
+  }
+  return (int)x;
 }
+
+QtnKnobs read_knobs() {
+  QtnKnobs k;
+  k.k3_route = knob("QTN_K3_ROUTE", -1, -1, 64);
+  k.k4_min_e = knob("QTN_K4", 1, 0, 4);
+  k.k4_all = knob("QTN_K4_ALL", -1, -1, 1);
+  k.k5 = knob("QTN_K5", 1, 0, 1);
+  k.pdl = knob("QTN_PDL", 1, 0, 1);
+  k.k3_tcap = knob("QTN_K3_TCAP", 0, 0, 16);
+  k.k3_stage_kb = knob("QTN_K3_STAGE_KB", 40, 8, 200);
+  k.k3_run = knob("QTN_K3_RUN", 128, 16, 4096);
+  k.k3_v1 = knob("QTN_K3_V1", 0, 0, 1);
+  k.k3_ulim = knob("QTN_K3_ULIM", 5, 0, 8);
+  k.k3_inv2 = knob("QTN_K3_INV2", 1, 0, 1);
+  return k;
+}
+
 
 // Route a large item to K3?  QTN_K3_ROUTE: 0 never, 1 merged expansion items
 // (k >= 2, >= 2 varying staged members), 2 every large item, >= 10: every
@@ -1091,7 +1121,7 @@ int getenv_int(const char* name, int dflt) {
 // +2 %, cfg-3 +4 %); complex128 routes items of width >= 20 to K3 (cfg-2
 // 0.593 -> 0.497 ms, 45-cone graph +0.8 %).
 bool k3_route(const qtn_bucket_t& b, const qtn_member_t* mem, int dtype) {
-  static const int env = getenv_int("QTN_K3_ROUTE", -1);
+  const int env = qtn_knobs().k3_route;
   const int mode = env >= 0 ? env : (dtype == QTN_C64 ? 0 : 20);
   if (mode == 0 || b.w < 0 || b.k > 3 || b.w > 31 || b.n_mem > QTN_MAX_MEMBERS) return false;
   if (mode == 2) return true;
@@ -1125,16 +1155,35 @@ void k3_desc(const qtn_program_t* p, const qtn_bucket_t& b, const qtn_member_t* 
 
 }  // namespace
 
+const QtnKnobs& qtn_knobs() {
+  static const QtnKnobs k = read_knobs();   // thread-safe one-time init
+  return k;
+}
+
 struct qtn_graph {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
-  int32_t kinds[4] = {0, 0, 0, 0};   // nodes run by K1, K2, K3, K4
-  std::vector<int32_t> node_kind;    // per node: 0 K1, 1 K2, 2 K3, 3 K4
+  int32_t kinds[5] = {0, 0, 0, 0, 0};   // nodes run by K1, K2, K3, K4, K5
+  std::vector<int32_t> node_kind;       // per node: 0 K1, 1 K2, 2 K3, 3 K4, 4 K5
 };
 
 extern "C" {
 
 int qtn_abi_version(void) { return QTN_ABI_VERSION; }
+
+const char* qtn_route_config(void) {
+  static const std::string txt = [] {
+    const QtnKnobs& k = qtn_knobs();
+    char buf[512];
+    snprintf(buf, sizeof(buf),
+             "k3_route=%d k4_min_e=%d k4_all=%d k5=%d pdl=%d k3_tcap=%d k3_stage_kb=%d k3_run=%d k3_v1=%d k3_ulim=%d "
+             "k3_inv2=%d",
+             k.k3_route, k.k4_min_e, k.k4_all, k.k5, k.pdl, k.k3_tcap, k.k3_stage_kb, k.k3_run, k.k3_v1, k.k3_ulim,
+             k.k3_inv2);
+    return std::string(buf);
+  }();
+  return txt.c_str();
+}
 
 const char* qtn_last_error(void) { return g_err.c_str(); }
 
@@ -1239,8 +1288,8 @@ int qtn_graph_create_host(const qtn_program_t* p, const qtn_bucket_t* items, con
       return cuda_err(e, "cudaGraphAddMemcpyNode1D(h2d)");
     }
   }
-  const char* pdl_env = getenv("QTN_PDL");
-  const bool use_pdl = !(pdl_env && pdl_env[0] == '0');
+  const QtnKnobs& route = qtn_knobs();
+  const bool use_pdl = route.pdl != 0;
   for (int i = 0; i < n_nodes; ++i) {
     const qtn_node_t& nd = nodes[i];
     if (nd.kind == QTN_NODE_LARGE && (nd.first < 0 || nd.first >= p->n_buckets)) {
@@ -1263,11 +1312,31 @@ int qtn_graph_create_host(const qtn_program_t* p, const qtn_bucket_t* items, con
     }
     ++g->kinds[nd.kind == QTN_NODE_LARGE ? 0 : 1];
     g->node_kind.push_back(nd.kind == QTN_NODE_LARGE ? 0 : 1);
+    // K5: streaming items (one member carries every result bit)
+    bool k5 = false;
+    if (nd.kind == QTN_NODE_LARGE && p->arena && have_mems && route.k5 && items[nd.first].k >= 1) {
+      qtn_bucket_desc_t d;
+      k3_desc(p, items[nd.first], mems_ptr, &d);
+      std::vector<unsigned char> plan(qtn_k5_plan_bytes());
+      const void* fn = nullptr;
+      int grid = 0, smem = 0;
+      if (qtn_k5_node(&d, p->timing, nd.first, plan.data(), &fn, &grid, &smem) == QTN_OK) {
+        specs[i].k3plan = std::move(plan);
+        specs[i].fn = fn;
+        specs[i].grid = grid;
+        specs[i].smem = smem;
+        specs[i].args[0] = specs[i].k3plan.data();
+        k5 = true;
+        ++g->kinds[4];
+        --g->kinds[0];
+        g->node_kind.back() = 4;
+      }
+    }
     // K4: expansion items of one dominant member (QTN_K4 = fewest expansion
     // bits routed, 0 = never)
-    static const int k4_min_e = getenv_int("QTN_K4", 1);
+    const int k4_min_e = route.k4_min_e;
     bool k4 = false;
-    if (nd.kind == QTN_NODE_LARGE && p->arena && have_mems && k4_min_e > 0 && items[nd.first].k >= 1 &&
+    if (!k5 && nd.kind == QTN_NODE_LARGE && p->arena && have_mems && k4_min_e > 0 && items[nd.first].k >= 1 &&
         items[nd.first].w >= 12) {
       qtn_bucket_desc_t d;
       k3_desc(p, items[nd.first], mems_ptr, &d);
@@ -1276,7 +1345,7 @@ int qtn_graph_create_host(const qtn_program_t* p, const qtn_bucket_t* items, con
       int grid = 0, smem = 0;
       // non-expansion items too: complex128 by default (cfg-2 0.3575 -> 0.3519 ms),
       // not complex64 (its streaming items stay faster in K1); QTN_K4_ALL overrides
-      static const int k4_all_env = getenv_int("QTN_K4_ALL", -1);
+      const int k4_all_env = route.k4_all;
       const bool k4_all = k4_all_env >= 0 ? k4_all_env != 0 : p->dtype == QTN_C128;
       if (qtn_k4_node(&d, k4_all ? 0 : k4_min_e, p->timing, nd.first, plan.data(), &fn, &grid, &smem) == QTN_OK) {
         specs[i].k3plan = std::move(plan);
@@ -1290,7 +1359,8 @@ int qtn_graph_create_host(const qtn_program_t* p, const qtn_bucket_t* items, con
         g->node_kind.back() = 3;
       }   // else: not an expansion item (K3 / K1 below)
     }
-    if (!k4 && nd.kind == QTN_NODE_LARGE && p->arena && have_mems && k3_route(items[nd.first], mems_ptr, p->dtype)) {
+    if (!k5 && !k4 && nd.kind == QTN_NODE_LARGE && p->arena && have_mems &&
+        k3_route(items[nd.first], mems_ptr, p->dtype)) {
       qtn_bucket_desc_t d;
       k3_desc(p, items[nd.first], mems_ptr, &d);
       specs[i].k3plan.resize(qtn_k3_plan_bytes());
@@ -1368,7 +1438,7 @@ int qtn_graph_launch(qtn_graph_t* g, void* stream) {
 
 int qtn_graph_kinds(const qtn_graph_t* g, int32_t* counts) {
   if (!g || !counts) return set_err(QTN_E_INVALID, "null argument");
-  for (int i = 0; i < 4; ++i) counts[i] = g->kinds[i];
+  for (int i = 0; i < 5; ++i) counts[i] = g->kinds[i];
   return QTN_OK;
 }
 

@@ -1025,12 +1025,12 @@ class Executor:
         return g
 
     def kernel_mix(self, io=True):
-        """{'K1', 'K2', 'K3', 'K4'}: graph nodes per kernel family (the
+        """{'K1', 'K2', 'K3', 'K4', 'K5'}: graph nodes per kernel family (the
         end-to-end graph when io, else the kernels-only graph)."""
         g = self._io_graph() if io else self.graph
-        c = (ctypes.c_int32 * 4)()
+        c = (ctypes.c_int32 * 5)()
         N.check(N.load().qtn_graph_kinds(g, c))
-        return dict(zip(("K1", "K2", "K3", "K4"), (int(x) for x in c)))
+        return dict(zip(N.KERNEL_FAMILIES, (int(x) for x in c)))
 
     def node_kernels(self, io=True):
         """Per graph node, the kernel family that runs it ('K1'..'K4')."""
@@ -1038,7 +1038,7 @@ class Executor:
         n = int(self.prog.n_nodes)
         c = (ctypes.c_int32 * max(n, 1))()
         N.check(N.load().qtn_graph_node_kinds(g, c, n))
-        return [("K1", "K2", "K3", "K4")[c[i]] for i in range(n)]
+        return [N.KERNEL_FAMILIES[c[i]] for i in range(n)]
 
     def node_graph(self, ni):
         """A graph of node `ni` alone (no dependencies; the same kernel and
@@ -1060,7 +1060,7 @@ class Executor:
                 ctypes.byref(g)))
         kinds = (ctypes.c_int32 * 1)()
         N.check(N.load().qtn_graph_node_kinds(g, kinds, 1))
-        return _OwnedGraph(g), ("K1", "K2", "K3", "K4")[kinds[0]]
+        return _OwnedGraph(g), N.KERNEL_FAMILIES[kinds[0]]
 
     def launch_graph(self, g, stream=None):
         s = stream if stream is not None else self.torch.cuda.current_stream(self.device)
