@@ -79,7 +79,7 @@ typedef struct {
 
 /* One work item: a (merged) bucket contraction (w >= 0) or an instance
  * finaliser (w == QTN_FINALIZE) that multiplies rank-0 values into a result
- * slot — the get-result step (src/ordering.py:167-170,183-184).  56 bytes. */
+ * slot — the get-result step (src/ordering.py:167-170,183-184).  64 bytes. */
 #define QTN_FINALIZE (-1)
 typedef struct {
   uint64_t out_off;   /* element offset of the result in the arena          */
@@ -97,7 +97,17 @@ typedef struct {
   uint32_t stmask;    /* tile bits each thread walks sequentially (vector
                          path; 0 = default).  Members not carrying any of
                          them are multiplied once per tile and reused.       */
+  int32_t group;      /* K2 stages: > 0 on the root of a CTA group — the
+                         `group` items ending here (a subtree of the in-tree,
+                         numbered consecutively, children first) run in ONE
+                         block on one ticket, every non-root result kept in
+                         shared memory (double) at element offset out_off;
+                         members with cls & QTN_K2_SMEM read it there.  0
+                         otherwise.                                         */
+  int32_t reserved;
 } qtn_bucket_t;
+/* K2 group member read from the group's shared-memory results (cls bit). */
+#define QTN_K2_SMEM 0x80000000u
 
 /* Dependency: wait until bucket `bucket` has completed `need` tiles. */
 typedef struct {

@@ -67,13 +67,15 @@ PLAN_ARRAYS = ("w", "k", "L", "level", "out_off", "mem_ptr", "mem_kind", "mem_re
 BUCKET_DT = np.dtype([
     ("out_off", "<u8"), ("w", "<i4"), ("tile_bits", "<i4"), ("k", "<i4"), ("mem_begin", "<i4"),
     ("n_mem", "<i4"), ("dep_begin", "<i4"), ("n_dep", "<i4"), ("tick_begin", "<i4"),
-    ("n_tiles", "<i4"), ("slot", "<i4"), ("smem_elems", "<i4"), ("stmask", "<u4"),
+    ("n_tiles", "<i4"), ("slot", "<i4"), ("smem_elems", "<i4"), ("stmask", "<u4"), ("group", "<i4"),
+    ("reserved", "<i4"),
 ])
+QTN_K2_SMEM = 0x80000000
 MEMBER_DT = np.dtype([("off", "<u8"), ("mask", "<u8"), ("smask", "<u4"), ("cls", "<u4")])
 NODE_DT = np.dtype([("kind", "<i4"), ("first", "<i4"), ("count", "<i4"), ("n_tickets", "<i4"),
                     ("variant", "<i4"), ("dep_begin", "<i4"), ("n_dep", "<i4"), ("smem_bytes", "<i4")])
 DEP_DT = np.dtype([("bucket", "<i4"), ("need", "<i4")])
-assert BUCKET_DT.itemsize == 56 and MEMBER_DT.itemsize == 24 and DEP_DT.itemsize == 8
+assert BUCKET_DT.itemsize == 64 and MEMBER_DT.itemsize == 24 and DEP_DT.itemsize == 8
 assert NODE_DT.itemsize == 32
 
 

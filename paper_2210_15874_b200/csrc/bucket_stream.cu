@@ -66,6 +66,7 @@ struct Plan {
   void* out;
   const void* mptr[MAXM];      // loaded members first (B = 0), then uniform members
   int32_t nm, nv, k, w, L, b0, nsb;    // b0: first thread bit (1 = complex64 pairs); nsb: step bits (L = b0 + 8 + nsb)
+  int32_t b_stream;            // B carries every result bit: read once, streaming loads (else re-read via L1/L2)
   int32_t pair[MAXV];          // c64: member j reads a (v = 0, 1) pair as one 16-byte vector
   int32_t bcast[MAXV];         // c64: member j does not carry result bit 0 (one value for the pair)
   int64_t n_tiles;
@@ -185,7 +186,7 @@ __device__ __forceinline__ void k5_body(const Plan& P) {
                      "member %d element %lld", j, (long long)(p - reinterpret_cast<const T*>(P.mptr[j])));
             if (VEC == 2) {
               if (P.pair[j]) {
-                const V v = j == 0 ? ld_stream(reinterpret_cast<const V*>(p)) : __ldg(reinterpret_cast<const V*>(p));
+                const V v = (j == 0 && P.b_stream) ? ld_stream(reinterpret_cast<const V*>(p)) : __ldg(reinterpret_cast<const V*>(p));
                 const T* e = reinterpret_cast<const T*>(&v);
                 x[uu][j][s][0] = e[0];
                 x[uu][j][s][VEC - 1] = e[VEC - 1];
@@ -197,7 +198,7 @@ __device__ __forceinline__ void k5_body(const Plan& P) {
                 x[uu][j][s][VEC - 1] = __ldg(p + P.rs[j][0]);
               }
             } else {
-              x[uu][j][s][0] = j == 0 ? ld_stream(p) : __ldg(p);
+              x[uu][j][s][0] = (j == 0 && P.b_stream) ? ld_stream(p) : __ldg(p);
             }
           }
         }
@@ -283,8 +284,10 @@ int sm_count() {
 }
 
 // Plan K5 for `d`: QTN_E_UNSUPPORTED unless one member carries every result
-// bit and at most MAXV members carry result bits.
-int make_plan(const qtn_bucket_desc_t* d, Plan* P) {
+// bit (or, max_e > 0, all but at most max_e of them: the dominant member is
+// then re-read through L1/L2 once per missing-bit assignment) and at most
+// MAXV members carry result bits.
+int make_plan(const qtn_bucket_desc_t* d, int max_e, Plan* P) {
   memset(P, 0, sizeof(*P));
   const int w = d->w, k = d->k, nm = d->n_mem;
   if (d->dtype != QTN_C64 && d->dtype != QTN_C128) return fail(QTN_E_INVALID, "K5: bad dtype");
@@ -293,14 +296,15 @@ int make_plan(const qtn_bucket_desc_t* d, Plan* P) {
   const int vb = c64 ? 1 : 0;
   if (k < 1 || k > MAXKS || nm < 1 || nm > MAXM || w < vb + 8 || w > 40)
     return fail(QTN_E_UNSUPPORTED, "K5: w=%d k=%d n_mem=%d", w, k, nm);
-  // dominant member: carries every result bit
-  int iB = -1;
-  for (int i = 0; i < nm && iB < 0; ++i) {
+  // dominant member: the most result bits (the first such member)
+  int iB = -1, best = -1;
+  for (int i = 0; i < nm; ++i) {
     int c = 0;
     for (int b = 0; b < w; ++b) c += d->mem[i].strides[b] != 0;
-    if (c == w) iB = i;
+    if (c > best) best = c, iB = i;
   }
-  if (iB < 0) return fail(QTN_E_UNSUPPORTED, "K5: no member carries every result bit");
+  if (best < w - max_e) return fail(QTN_E_UNSUPPORTED, "K5: no member carries every result bit");
+  P->b_stream = best == w ? 1 : 0;
   // loaded members: B first, then the others with result bits (member order)
   int ord[MAXM], nv = 0, nmo = 0;
   ord[nv++] = iB;
@@ -372,11 +376,11 @@ size_t qtn_k5_plan_bytes() { return sizeof(qtn_k5::Plan); }
 
 // Program-graph node for one item (qtn_graph_create_host): QTN_E_UNSUPPORTED
 // when no member carries every result bit.
-int qtn_k5_node(const qtn_bucket_desc_t* d, unsigned long long* timing, int32_t item, void* plan, const void** fn,
-                int* grid, int* smem) {
+int qtn_k5_node(const qtn_bucket_desc_t* d, int max_e, unsigned long long* timing, int32_t item, void* plan,
+                const void** fn, int* grid, int* smem) {
   using namespace qtn_k5;
   Plan* P = reinterpret_cast<Plan*>(plan);
-  int rc = make_plan(d, P);
+  int rc = make_plan(d, max_e, P);
   if (rc) return rc;
   P->timing = timing;
   P->item = item;
@@ -396,7 +400,7 @@ extern "C" int qtn_bucket_stream(const qtn_bucket_desc_t* d, void* stream) {
   static thread_local Plan P;
   const void* fn = nullptr;
   int grid = 0, smem = 0;
-  int rc = qtn_k5_node(d, nullptr, 0, &P, &fn, &grid, &smem);
+  int rc = qtn_k5_node(d, 0, nullptr, 0, &P, &fn, &grid, &smem);
   if (rc) return rc;
   void* args[] = {&P};
   const cudaError_t e = cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(NT), args, 0, (cudaStream_t)stream);

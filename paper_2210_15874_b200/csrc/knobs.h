@@ -13,7 +13,8 @@ struct QtnKnobs {
   int k3_route;     // QTN_K3_ROUTE  -1 default | 0 never | 1 merged expansions | 2 all large | >=10 width threshold
   int k4_min_e;     // QTN_K4        fewest expansion bits routed to K4 (0 = K4 off)
   int k4_all;       // QTN_K4_ALL    -1 default (complex128 only) | 0 | 1: non-expansion items to K4
-  int k5;           // QTN_K5        1: streaming items (a member carries every result bit) to K5 | 0 off
+  int k5;           // QTN_K5        1: streaming items (a member carries every result bit) to K5 | 2: also
+                    //               expansions (<= 4 missing bits) | 0 off
   int pdl;          // QTN_PDL       1: programmatic graph edges | 0 plain edges
   int k3_tcap;      // QTN_K3_TCAP   K3 tile-bit cap (0 = planner's choice)
   int k3_stage_kb;  // QTN_K3_STAGE_KB  K3 staging budget per block (KB)

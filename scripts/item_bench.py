@@ -39,7 +39,7 @@ for gid in range(prog.n_buckets):
     b["dep_begin"] = 0
     b["tick_begin"] = 0
     blob = np.zeros(4096, np.uint8)
-    blob[0:56] = np.frombuffer(b.tobytes(), np.uint8)
+    blob[0:N.BUCKET_DT.itemsize] = np.frombuffer(b.tobytes(), np.uint8)
     blob[64:64 + mem.nbytes] = np.frombuffer(mem.tobytes(), np.uint8)
     tab = torch.from_numpy(blob).cuda()
     base = tab.data_ptr()

@@ -20,7 +20,7 @@ def test_header_symbols_exported():
 
 
 def test_struct_layouts_match_header():
-    assert N.BUCKET_DT.itemsize == 56
+    assert N.BUCKET_DT.itemsize == 64
     assert N.MEMBER_DT.itemsize == 24
     assert ctypes.sizeof(N.ProgramC) == 6 * 4 + 8 * 8 + 8 + 8 + 8   # + inputs_hi, n_in_elems
     assert N.NODE_DT.itemsize == 32
