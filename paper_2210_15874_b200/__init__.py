@@ -46,6 +46,7 @@ from .ordering import (
     MemoryCapError,
     WidthProfile,
     contract_network,
+    contract_network_eager,
     contract_sliced,
     dry_run,
     get_result_data,
@@ -61,7 +62,7 @@ __all__ = [
     "Backend", "Bucket", "BucketStats", "Circuit", "DeviceTensor", "Gate", "Graph",
     "Lightcone", "MemoryCapError", "NativeError", "NativeUnavailable", "QaoaParams",
     "Tensor", "TensorNetwork", "WidthProfile", "amplitude_network", "cone_gates",
-    "contract_bucket", "contract_network", "contract_sliced", "dry_run",
+    "contract_bucket", "contract_network", "contract_network_eager", "contract_sliced", "dry_run",
     "extract_lightcone", "gate_diagonal", "gate_unitary", "get_result_data",
     "greedy_order", "line_graph", "memory_estimate", "parse_circuit", "parse_graph",
     "permute", "process_bucket", "qaoa_energy", "qaoa_energy_detailed",

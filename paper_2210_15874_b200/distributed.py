@@ -227,13 +227,14 @@ def run_local(plan: UnitPlan, mine, backend: Backend, device: int, budget_bytes=
         res = ex.run([plan.raws[plan.units[u].cone] for u in batch])
         if be.profile:
             t0, t1 = ex.fetch_timing()
-        from .ordering import ref_stats
+        from .ordering import _item_families, ref_stats
         for k, u in enumerate(batch):
             vals[u] = complex(res[k])
             ci = plan.units[u].cone
             tm = plan.templates[ci]
             el = np.maximum(t1[prog.bucket_gid[k]] - t0[prog.bucket_gid[k]], 0) if be.profile else None
-            stats.setdefault(ci, []).extend(ref_stats(tm, be, el) if be.profile else _plain_stats(tm, be))
+            stats.setdefault(ci, []).extend(ref_stats(tm, be, el, _item_families(ex, k)) if be.profile
+                                            else _plain_stats(tm, be))
     return vals, stats
 
 
@@ -253,7 +254,7 @@ def _run_streamed(plan, batches, be, device, progs):
     when a batch needs more.  `progs`: [(Program, batch)] — filled when
     `batches` is given, replayed (no host planning) when `batches` is None."""
     import torch
-    from .ordering import ref_stats
+    from .ordering import _item_families, ref_stats
     tdt = torch.complex64 if be.dtype == "complex64" else torch.complex128
     vals, stats = {}, {}
     arena, prev = None, None
@@ -267,7 +268,8 @@ def _run_streamed(plan, batches, be, device, progs):
             ci = plan.units[u].cone
             el = (np.maximum(t1[ex.prog.bucket_gid[k]] - t0[ex.prog.bucket_gid[k]], 0) if be.profile else None)
             tm = plan.templates[ci]
-            stats.setdefault(ci, []).extend(ref_stats(tm, be, el) if be.profile else _plain_stats(tm, be))
+            stats.setdefault(ci, []).extend(ref_stats(tm, be, el, _item_families(ex, k)) if be.profile
+                                            else _plain_stats(tm, be))
 
     ex = None
     work = progs if batches is None else batches

@@ -17,7 +17,8 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import engine as E
-from .tensor_core import Backend, BucketStats, DeviceTensor, Tensor, memory_estimate
+from . import tensor_core as _tc
+from .tensor_core import Backend, Bucket, BucketStats, DeviceTensor, Tensor, contract_bucket, memory_estimate
 from .tn_build import TensorNetwork
 
 DEFAULT_MEM_CAP = 4 << 30     # src/ordering.py:13
@@ -319,28 +320,47 @@ def _executor(key, progfn, backend, n_inst):
     return hit
 
 
-def ref_stats(tmpl, backend, item_elapsed=None):
+def ref_stats(tmpl, backend, item_elapsed=None, families=None):
     """One BucketStats per reference bucket (elimination order).  A merged
-    device item's time is reported on its final bucket (0 on the buckets it
-    absorbed)."""
+    device item's measured time is split over the buckets it computes in
+    proportion to their algorithmic elements; `families`:
+    the kernel family per device item (K1..K5) from the built graph."""
+    n = len(tmpl.ref_w)
     if item_elapsed is None:
-        el = np.zeros(len(tmpl.ref_w), np.int64)
+        el = np.zeros(n, np.int64)
     else:
-        el = np.where(tmpl.ref_last == 1, item_elapsed[tmpl.ref_item], 0)
-    # the route a bucket actually took: its item's kernel (K2 small stage or K1)
+        it = np.asarray(tmpl.ref_item)
+        wgt = np.asarray(tmpl.ref_elems, np.float64)
+        tot = np.zeros(tmpl.n_items)
+        np.add.at(tot, it, wgt)
+        el = np.floor(np.asarray(item_elapsed, np.float64)[it] * wgt / np.maximum(tot[it], 1.0)).astype(np.int64)
+        # the item's last bucket takes the rounding remainder: sums are exact
+        got = np.zeros(tmpl.n_items, np.int64)
+        np.add.at(got, it, el)
+        last = tmpl.ref_last == 1
+        el[last] += np.asarray(item_elapsed, np.int64)[it[last]] - got[it[last]]
+    # the route a bucket actually took: its item's kernel (K2 small stage or a fused kernel)
     small = tmpl.variant[tmpl.ref_item] == E.VARIANT_SMALL
-    return [BucketStats(width=int(w), elapsed_ns=int(e), backend_used="b200-small" if sm else "b200-large")
-            for w, e, sm in zip(tmpl.ref_w, el, small)]
+    fam = [families[int(i)] if families is not None else "" for i in tmpl.ref_item]
+    return [BucketStats(width=int(w), elapsed_ns=int(e), backend_used="b200-small" if sm else "b200-large",
+                        kernel=f) for w, e, sm, f in zip(tmpl.ref_w, el, small, fam)]
 
 
 _NOPROFILE_STATS = {}
+
+
+def _item_families(ex, inst=0):
+    """Kernel family (K1..K5) of every device item of instance `inst`."""
+    fam = ex.node_kernels(io=False)
+    node_of = ex.prog.node_of_item()
+    return [fam[node_of[int(g)]] for g in ex.prog.bucket_gid[inst]]
 
 
 def _stats(tmpl, ex, backend, inst=0):
     if backend.profile:
         t0, t1 = ex.fetch_timing()
         gids = ex.prog.bucket_gid[inst]
-        return ref_stats(tmpl, backend, np.maximum(t1[gids] - t0[gids], 0))
+        return ref_stats(tmpl, backend, np.maximum(t1[gids] - t0[gids], 0), _item_families(ex, inst))
     # widths are fixed by the plan; BucketStats are immutable, so the list is
     # built once per (template, threshold) and copied
     key = (id(tmpl), backend.threshold)
@@ -352,13 +372,53 @@ def _stats(tmpl, ex, backend, inst=0):
     return list(hit[1])
 
 
+def contract_network_eager(tn: TensorNetwork, order, backend: Backend = None, mem_cap: int = DEFAULT_MEM_CAP):
+    """The reference's own driver loop (src/ordering.py:148-189), one
+    `contract_bucket` call per non-empty bucket through this module's global
+    name — the reference's seam (src/ordering.py:10,181) for running the
+    driver on another process-bucket kernel (A/B tests monkeypatch
+    `ordering.contract_bucket`).  Same pre-checks, stats and result as
+    contract_network; the planned device program is the fast path."""
+    backend = backend or Backend()
+    if tn.open_indices:
+        raise ValueError("contract_network requires a closed network")
+    prof = dry_run(tn, order)      # raises for indices missing from the order
+    need = memory_estimate(prof.contraction_width, backend.dtype)
+    if need > mem_cap:
+        raise MemoryCapError(prof.contraction_width, need, mem_cap)
+    pos = {x: k for k, x in enumerate(order)}
+    buckets = {x: [] for x in order}
+    scalar = 1.0 + 0.0j
+    for t in tn.tensors:
+        if not t.indices:
+            scalar *= complex(np.asarray(t.data).reshape(()))
+        else:
+            buckets[min(t.indices, key=pos.__getitem__)].append(t)
+    stats = []
+    for idx in order:
+        members = buckets.pop(idx)
+        if not members:
+            continue
+        res, st = contract_bucket(Bucket(idx, members), backend)   # module-global lookup: the seam
+        stats.append(st)
+        if not res.indices:
+            scalar *= complex(np.asarray(res.data).reshape(()))
+        else:
+            buckets[min(res.indices, key=pos.__getitem__)].append(res)
+    return scalar, stats
+
+
 def contract_network(tn: TensorNetwork, order, backend: Backend = None, mem_cap: int = DEFAULT_MEM_CAP):
     """Full bucket elimination on the B200; returns (scalar, [BucketStats])
     (src/ordering.py:148-189).
 
     The network must be closed; a dry-run memory pre-check raises
     MemoryCapError before any device allocation.  Stats are one per non-empty
-    bucket in elimination order (width == dry-run width)."""
+    bucket in elimination order (width == dry-run width).  If this module's
+    `contract_bucket` has been replaced (the reference's A/B seam), the
+    bucket-by-bucket driver runs it instead (contract_network_eager)."""
+    if contract_bucket is not _tc.contract_bucket:
+        return contract_network_eager(tn, order, backend, mem_cap)
     backend = backend or Backend()
     if tn.open_indices:
         raise ValueError("contract_network requires a closed network")

@@ -184,13 +184,20 @@ class Bucket:
 
 @dataclass(frozen=True)
 class BucketStats:
-    """width = result rank; elapsed_ns = device time of the bucket (first tile
-    start -> last tile end, %globaltimer) or 0 when profiling is off;
-    backend_used = "b200-small" / "b200-large" (src/tensor_core.py:93-97)."""
+    """width = result rank (src/tensor_core.py:93-97); elapsed_ns = the
+    bucket's device time, 0 when profiling is off — the reference times every
+    bucket's kernel (185-187); here a device item may be a merged chain of
+    buckets, so its measured span (first tile start -> last tile end,
+    %globaltimer) is split over its buckets in proportion to their
+    algorithmic elements (the sum over an item's buckets is the item's time);
+    backend_used = the route, "b200-small" (batched K2 stage) or
+    "b200-large" (fused kernels) — the analogue of the reference's Mixed
+    reference/fast split; kernel = the kernel family that ran it (K1..K5)."""
 
     width: int
     elapsed_ns: int
     backend_used: str
+    kernel: str = ""
 
 
 def memory_estimate(width: int, dtype: str = "complex128") -> int:
@@ -317,8 +324,9 @@ def contract_bucket(b: Bucket, backend: Backend = None):
     result = DeviceTensor(res, out)
     if not any_dev:
         result = result.to_host()
+    # one fused K3 launch whatever the width (no small-bucket route here)
     return result, BucketStats(width=w, elapsed_ns=elapsed if backend.profile else 0,
-                               backend_used=backend.route(w))
+                               backend_used="b200-large", kernel="K3")
 
 
 # BASELINE.json vocabulary: "process-bucket"
