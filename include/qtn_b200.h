@@ -125,7 +125,8 @@ typedef struct {
   int32_t n_buckets;
   int32_t n_tickets;
   int32_t smem_bytes;           /* dynamic shared memory per block (staging)  */
-  int32_t grid;                 /* 0 = all resident blocks (occupancy)        */
+  int32_t grid;                 /* K2 stages: 0 = all resident blocks; > 0 caps
+                                   the persistent grid (schedule tests)        */
   int32_t n_nodes;              /* graph nodes (ctrl layout, see above)       */
   const qtn_bucket_t* buckets;
   const qtn_member_t* members;

@@ -1165,6 +1165,9 @@ int make_launch(const qtn_program_t* p, const qtn_node_t* nd, int ni, const K1It
     rc = resident_grid(L->fn, L->smem, &L->grid);
     if (rc) return rc;
     if (nd->n_tickets < L->grid) L->grid = nd->n_tickets > 0 ? nd->n_tickets : 1;
+    // prog->grid > 0 caps the stage's persistent grid (schedule-independence
+    // tests: any number of blocks must give the same bits)
+    if (p->grid > 0 && p->grid < L->grid) L->grid = p->grid;
     L->a0 = nd->first;
     L->a1 = nd->count;
     L->a2 = nd->n_tickets;
