@@ -335,22 +335,45 @@ def run_units(plan: UnitPlan, backend: Backend, group=None, n_gpus=None, cache=N
     ng = n_gpus or 1
     owner = lpt_assign(costs, ng)
     results = [None] * ng
-
-    def work(r):
-        mine = [u for u in range(n_units) if owner[u] == r]
-        with torch.cuda.device(r):
-            results[r] = run_local(plan, mine, backend, r, cache=cache) if mine else ({}, {})
-
+    stats = {}
     if ng > 1:
+        # one host thread per GPU; each device's unit values go into its own
+        # zero slot vector, summed across the devices by ONE NCCL all-reduce
+        # (single process, one communicator per device: ncclCommInitAll)
+        dev_slots = [None] * ng
+
+        def work(r):
+            mine = [u for u in range(n_units) if owner[u] == r]
+            with torch.cuda.device(r):
+                results[r] = run_local(plan, mine, backend, r, cache=cache) if mine else ({}, {})
+                sl = np.zeros(2 * n_units, np.float64)
+                for u, v in results[r][0].items():
+                    sl[2 * u], sl[2 * u + 1] = v.real, v.imag
+                dev_slots[r] = torch.from_numpy(sl).to(f"cuda:{r}")
+
         with ThreadPoolExecutor(max_workers=ng) as pool:
             list(pool.map(work, range(ng)))
+        slots = slot_allreduce_devices(dev_slots)
     else:
         results[0] = run_local(plan, list(range(n_units)), backend, backend.device, cache=cache)
-    slots = np.zeros(2 * n_units, np.float64)
-    stats = {}
-    for vals, st in results:
-        for u, v in vals.items():
+        slots = np.zeros(2 * n_units, np.float64)
+        for u, v in results[0][0].items():
             slots[2 * u], slots[2 * u + 1] = v.real, v.imag
+    for _, st in results:
         for ci, s in st.items():
             stats.setdefault(ci, []).extend(s)
     return _combine(plan, slots), [stats.get(ci, []) for ci in range(len(plan.cones))]
+
+
+def slot_allreduce_devices(dev_slots):
+    """Sum per-device slot vectors (float64, one per GPU of this process) with
+    a single-process NCCL all-reduce (torch.cuda.nccl: one communicator per
+    device); every slot has one non-zero contributor, so the sum is exact.
+    Returns the summed vector on the host."""
+    import torch
+    import torch.cuda.nccl as nccl
+    if not nccl.is_available(dev_slots):
+        raise RuntimeError("NCCL unavailable for the slot all-reduce")
+    nccl.all_reduce(dev_slots)
+    torch.cuda.synchronize(dev_slots[0].device)
+    return dev_slots[0].cpu().numpy()

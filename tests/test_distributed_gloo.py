@@ -116,3 +116,23 @@ def test_balance_slicing_spreads_the_heaviest_cone():
     own = D.lpt_assign(c8, 8)
     load = [sum(c for c, o in zip(c8, own) if o == r) for r in range(8)]
     assert max(load) <= 1.15 * sum(c8) / 8
+
+
+@pytest.mark.gpu
+def test_single_process_nccl_slot_allreduce():
+    """The single-process multi-GPU reduction (qaoa_energy(n_gpus=N)): one
+    NCCL all-reduce over per-device slot vectors; on a 1-GPU box the
+    communicator has one member — the code path and exactness still hold."""
+    import torch
+    from paper_2210_15874_b200 import distributed as D
+    n = torch.cuda.device_count()
+    vecs = []
+    for r in range(n):
+        v = torch.zeros(8, dtype=torch.float64, device=f"cuda:{r}")
+        v[2 * (r % 4)] = 1.0 + r
+        vecs.append(v)
+    out = D.slot_allreduce_devices(vecs)
+    want = np.zeros(8)
+    for r in range(n):
+        want[2 * (r % 4)] += 1.0 + r
+    assert np.array_equal(out, want)
