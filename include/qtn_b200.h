@@ -231,6 +231,20 @@ int qtn_graph_node_kinds(const qtn_graph_t* g, int32_t* kinds, int32_t n);
 int qtn_greedy_order(int32_t n_tensors, const int32_t* tensor_ptr, const int64_t* tensor_idx,
                      int32_t n_open, const int64_t* open_idx, int32_t heuristic,
                      int64_t* order_out, int32_t* n_out);
+/* Host dry run (no device): the reference's symbolic bucket replay
+ * (src/ordering.py:97-145) over CSR index lists with `fixed` (sliced) ids
+ * removed: widths_out[i] = width of the bucket of active_out[i] (the order
+ * without the fixed ids), *n_out = number of active ids.  widths_out and
+ * active_out must hold n_order entries. */
+int qtn_dry_run(int32_t n_tensors, const int32_t* tensor_ptr, const int64_t* tensor_idx, int32_t n_order,
+                const int64_t* order, int32_t n_fixed, const int64_t* fixed, int32_t* widths_out,
+                int64_t* active_out, int32_t* n_out);
+/* Host greedy slicing (src/ordering.py:192-230): while the dry run is wider
+ * than target_width, slice the smallest not-yet-sliced id of the widest
+ * (first widest) bucket's union.  sliced_out holds up to max_out ids. */
+int qtn_suggest_slicing(int32_t n_tensors, const int32_t* tensor_ptr, const int64_t* tensor_idx, int32_t n_order,
+                        const int64_t* order, int32_t target_width, int32_t max_out, int64_t* sliced_out,
+                        int32_t* n_out);
 /* ---- Host program planner (no device needed) ----
  * qtn_plan_build replays the bucket assignment of the reference's
  * contract_network (src/ordering.py:165-187) over index sets only, merges

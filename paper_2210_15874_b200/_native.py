@@ -52,6 +52,8 @@ EXPORTS = (
     "qtn_graph_destroy",
     "qtn_permute",
     "qtn_greedy_order",
+    "qtn_dry_run",
+    "qtn_suggest_slicing",
     "qtn_bucket",
     "qtn_bucket_plan",
     "qtn_plan_build",
@@ -172,6 +174,10 @@ def load(path: str = LIB_PATH):
     lib.qtn_graph_launch.argtypes = [ctypes.c_void_p, vp]
     lib.qtn_graph_destroy.restype = ctypes.c_int
     lib.qtn_graph_destroy.argtypes = [ctypes.c_void_p]
+    lib.qtn_dry_run.restype = ctypes.c_int
+    lib.qtn_dry_run.argtypes = [i32, vp, vp, i32, vp, i32, vp, vp, vp, ctypes.POINTER(i32)]
+    lib.qtn_suggest_slicing.restype = ctypes.c_int
+    lib.qtn_suggest_slicing.argtypes = [i32, vp, vp, i32, vp, i32, i32, vp, ctypes.POINTER(i32)]
     lib.qtn_greedy_order.restype = ctypes.c_int
     lib.qtn_greedy_order.argtypes = [i32, vp, vp, i32, vp, i32, vp, ctypes.POINTER(i32)]
     lib.qtn_permute.restype = ctypes.c_int
@@ -216,14 +222,9 @@ def require_device():
 def greedy_order(index_lists, open_indices=(), heuristic=0):
     """Host-side greedy elimination order (qtn_greedy_order); no device needed."""
     lib = load()
-    ptr = np.zeros(len(index_lists) + 1, np.int32)
-    flat = []
-    for t, ids in enumerate(index_lists):
-        flat.extend(ids)
-        ptr[t + 1] = len(flat)
-    idx = np.asarray(flat, dtype=np.int64)
+    ptr, idx = _csr(index_lists)
     opn = np.asarray(list(open_indices), dtype=np.int64)
-    n_distinct = len(set(flat)) if flat else 0
+    n_distinct = len(np.unique(idx)) if len(idx) else 0
     out = np.zeros(max(1, n_distinct), np.int64)
     n_out = ctypes.c_int32(0)
     check(lib.qtn_greedy_order(len(index_lists), ptr.ctypes.data_as(ctypes.c_void_p),
@@ -231,6 +232,46 @@ def greedy_order(index_lists, open_indices=(), heuristic=0):
                                opn.ctypes.data_as(ctypes.c_void_p) if len(opn) else None, heuristic,
                                out.ctypes.data_as(ctypes.c_void_p), ctypes.byref(n_out)))
     return out[: n_out.value].tolist()
+
+
+def _csr(index_lists):
+    ptr = np.zeros(len(index_lists) + 1, np.int32)
+    lens = [len(ids) for ids in index_lists]
+    if lens:
+        ptr[1:] = np.cumsum(lens)
+    flat = np.fromiter((i for ids in index_lists for i in ids), dtype=np.int64, count=int(ptr[-1]))
+    return ptr, flat
+
+
+def _vp(a):
+    return a.ctypes.data_as(ctypes.c_void_p) if len(a) else None
+
+
+def dry_run(index_lists, order, fixed=()):
+    """Host dry run (qtn_dry_run): (widths, active order); no device needed."""
+    lib = load()
+    ptr, flat = _csr(index_lists)
+    o = np.asarray(list(order), dtype=np.int64)
+    fx = np.asarray(list(fixed), dtype=np.int64)
+    widths = np.zeros(max(1, len(o)), np.int32)
+    active = np.zeros(max(1, len(o)), np.int64)
+    n = ctypes.c_int32(0)
+    check(lib.qtn_dry_run(len(index_lists), ptr.ctypes.data_as(ctypes.c_void_p), _vp(flat), len(o), _vp(o), len(fx),
+                          _vp(fx), widths.ctypes.data_as(ctypes.c_void_p), active.ctypes.data_as(ctypes.c_void_p),
+                          ctypes.byref(n)))
+    return widths[: n.value].tolist(), active[: n.value].tolist()
+
+
+def suggest_slicing(index_lists, order, target_width):
+    """Host greedy slicing (qtn_suggest_slicing); no device needed."""
+    lib = load()
+    ptr, flat = _csr(index_lists)
+    o = np.asarray(list(order), dtype=np.int64)
+    out = np.zeros(max(1, len(o)), np.int64)
+    n = ctypes.c_int32(0)
+    check(lib.qtn_suggest_slicing(len(index_lists), ptr.ctypes.data_as(ctypes.c_void_p), _vp(flat), len(o), _vp(o),
+                                  int(target_width), len(out), out.ctypes.data_as(ctypes.c_void_p), ctypes.byref(n)))
+    return out[: n.value].tolist()
 
 
 def permute(src_dtype, src_ptr, src_offset, dst_dtype, dst_ptr, rank, strides, stream):
@@ -293,14 +334,9 @@ def route_config() -> dict:
 def plan_build(index_lists, order, fixed, params):
     """Run the native planner; returns (scalars, {name: int64 array})."""
     lib = load()
-    ptr = np.zeros(len(index_lists) + 1, np.int32)
-    flat = []
-    for t, ids in enumerate(index_lists):
-        flat.extend(ids)
-        ptr[t + 1] = len(flat)
-    idx = np.asarray(flat, dtype=np.int64)
-    od = np.asarray([int(x) for x in order], dtype=np.int64)
-    fx = np.asarray([int(x) for x in fixed], dtype=np.int64)
+    ptr, idx = _csr(index_lists)
+    od = np.asarray(order, dtype=np.int64)
+    fx = np.asarray(fixed, dtype=np.int64)
     h = ctypes.c_void_p()
     rc = lib.qtn_plan_build(len(index_lists), ptr.ctypes.data_as(ctypes.c_void_p),
                             idx.ctypes.data_as(ctypes.c_void_p) if len(idx) else None, len(od),

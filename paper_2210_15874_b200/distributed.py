@@ -19,6 +19,7 @@ The reference parallelises the energy over lightcones with a thread pool
 """
 from __future__ import annotations
 
+import os
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 
@@ -26,6 +27,9 @@ import numpy as np
 
 from . import engine as E
 from .tensor_core import Backend, memory_estimate
+
+
+PLAN_THREADS = max(1, min(16, os.cpu_count() or 1))
 
 
 @dataclass
@@ -68,10 +72,14 @@ def plan_units(cones, backend: Backend, heuristic="minfill", mem_cap=4 << 30, sl
             tmpl = E.plan_template(ix, order, backend.dtype, fixed=sliced, small_iter_bits=sib)
         if memory_estimate(tmpl.max_width, backend.dtype) > mem_cap:
             raise MemoryCapError(tmpl.max_width, memory_estimate(tmpl.max_width, backend.dtype), mem_cap)
-        raw = np.concatenate([np.asarray(t.data, np.complex128).ravel() for t in tn.tensors])
+        raw = tn.packed()[2]      # the builders' packed host image (TensorNetwork.packed)
         return tmpl, sliced, raw
 
-    if n_workers > 1:
+    # the native planner calls (greedy_order, qtn_plan_build) release the GIL:
+    # plan the cones on host threads (at least PLAN_THREADS; the result does
+    # not depend on the thread count)
+    n_workers = max(int(n_workers or 1), PLAN_THREADS)
+    if n_workers > 1 and len(cones) > 1:
         with ThreadPoolExecutor(max_workers=n_workers) as pool:
             res = list(pool.map(one, cones))
     else:

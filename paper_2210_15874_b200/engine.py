@@ -345,7 +345,7 @@ def plan_template(index_sets, order, dtype, fixed=(), merge=None, small_iter_bit
     merge = MERGE_DEFAULT if merge is None else merge
     sib = small_iter_bits_for(None, dtype, wave_aware) if small_iter_bits is None else int(small_iter_bits)
     fixed = list(dict.fromkeys(int(f) for f in fixed))
-    sc, a = N.plan_build([tuple(int(i) for i in s) for s in index_sets], order, fixed, _plan_params(dtype, merge, sib, wave_aware))
+    sc, a = N.plan_build(index_sets, order, fixed, _plan_params(dtype, merge, sib, wave_aware))
     ncanon = len(a["gdst"])
     gfix = {f: a["gfix"][j * ncanon:(j + 1) * ncanon] for j, f in enumerate(fixed)}
     return Template(

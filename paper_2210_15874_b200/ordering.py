@@ -16,6 +16,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from . import _native as N
 from . import engine as E
 from . import tensor_core as _tc
 from .tensor_core import Backend, Bucket, BucketStats, DeviceTensor, Tensor, contract_bucket, memory_estimate
@@ -157,7 +158,31 @@ def _replay(index_sets, active, target_step=None):
 
 def dry_run(tn: TensorNetwork, order, fixed=()) -> WidthProfile:
     """Widths of every bucket without numeric work (src/ordering.py:119-145).
-    `fixed` indices are sliced out."""
+    `fixed` indices are sliced out.  Computed by the native host planner
+    (csrc/planner.cpp, qtn_dry_run); dry_run_py below is its checker."""
+    fixed = set(fixed)
+    missing = tn.all_indices() - set(order) - set(tn.open_indices) - fixed
+    if missing:
+        raise ValueError(f"order is missing indices: {sorted(missing)}")
+    widths, active = N.dry_run([t.indices for t in tn.tensors], order, sorted(fixed))
+    return WidthProfile(tuple(widths), tuple(active))
+
+
+def suggest_slicing(tn: TensorNetwork, order, target_width: int) -> list:
+    """Greedy slicing: while the profile is wider than the target, slice the
+    smallest not-yet-sliced id of the widest bucket's union (src/ordering.py:192-230).
+    Native host planner (csrc/planner.cpp, qtn_suggest_slicing);
+    suggest_slicing_py below is its checker."""
+    if target_width < 1:
+        raise ValueError("target_width must be >= 1")
+    missing = tn.all_indices() - set(order) - set(tn.open_indices)
+    if missing:
+        raise ValueError(f"order is missing indices: {sorted(missing)}")
+    return N.suggest_slicing([t.indices for t in tn.tensors], order, target_width)
+
+
+def dry_run_py(tn: TensorNetwork, order, fixed=()) -> WidthProfile:
+    """Python restatement of dry_run (the native planner's checker)."""
     fixed = set(fixed)
     active = [i for i in order if i not in fixed]
     missing = tn.all_indices() - set(order) - set(tn.open_indices) - fixed
@@ -167,14 +192,13 @@ def dry_run(tn: TensorNetwork, order, fixed=()) -> WidthProfile:
     return WidthProfile(tuple(_replay(sets, active)), tuple(active))
 
 
-def suggest_slicing(tn: TensorNetwork, order, target_width: int) -> list:
-    """Greedy slicing: while the profile is wider than the target, slice the
-    smallest not-yet-sliced id of the widest bucket's union (src/ordering.py:192-230)."""
+def suggest_slicing_py(tn: TensorNetwork, order, target_width: int) -> list:
+    """Python restatement of suggest_slicing (the native planner's checker)."""
     if target_width < 1:
         raise ValueError("target_width must be >= 1")
     sliced = []
     while True:
-        prof = dry_run(tn, order, fixed=sliced)
+        prof = dry_run_py(tn, order, fixed=sliced)
         if prof.contraction_width <= target_width:
             return sliced
         step = int(np.argmax(prof.per_bucket_widths))

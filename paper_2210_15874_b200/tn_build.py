@@ -171,6 +171,30 @@ def cone_gates(c: Circuit, edge) -> tuple:
     return tuple(kept), frozenset(support)
 
 
+_LAYERS_CACHE = {}   # id(circuit) -> (circuit, parsed): the last few circuits
+
+
+def _qaoa_layers_cached(c: Circuit):
+    """_qaoa_layers, memoised per circuit object (a cone is extracted per edge
+    of the same circuit; the parse is O(gates))."""
+    hit = _LAYERS_CACHE.get(id(c))
+    if hit is not None and hit[0] is c:
+        return hit[1]
+    parsed = _qaoa_layers(c)
+    if parsed is not None:
+        n = c.n_qubits
+        m = len(parsed[0])
+        gs = c.gates
+        # the circuit's own Gate objects per layer: ZZ by edge position, RX by qubit
+        zz = [gs[n + k * (m + n): n + k * (m + n) + m] for k in range(len(parsed[1]))]
+        rx = [gs[n + k * (m + n) + m: n + (k + 1) * (m + n)] for k in range(len(parsed[1]))]
+        parsed = (parsed[0], parsed[1], gs[:n], zz, rx)
+    if len(_LAYERS_CACHE) > 8:
+        _LAYERS_CACHE.clear()
+    _LAYERS_CACHE[id(c)] = (c, parsed)
+    return parsed
+
+
 def _qaoa_layers(c: Circuit):
     """Recognise a qaoa_maxcut_circuit: H layer, then p x [ZZ per edge, RX per
     qubit].  Returns (edges, [(gamma2, beta2)]) or None."""
@@ -212,20 +236,20 @@ def tight_cone_gates(c: Circuit, edge) -> tuple:
     88-97), then add their endpoints to S.  H on the final S.  Gates are
     returned in forward order (H, then per layer ZZ in edge order, RX in qubit
     order).  Raises ValueError if `c` is not a QAOA MaxCut circuit."""
-    parsed = _qaoa_layers(c)
+    parsed = _qaoa_layers_cached(c)
     if parsed is None:
         raise ValueError("tight cone needs a qaoa_maxcut_circuit")
-    edges, layers = parsed
+    edges, layers, hg, zzg, rxg = parsed     # the circuit's own (immutable) Gate objects
     support = set(edge)
     kept_layers = []
-    for zang, xang in reversed(layers):
-        rx = [Gate("RX", (q,), xang) for q in sorted(support)]
-        ek = [e for e in edges if e[0] in support or e[1] in support]
-        zz = [Gate("ZZ", e, zang) for e in ek]
-        for e in ek:
-            support.update(e)
+    for k in reversed(range(len(layers))):
+        rx = [rxg[k][q] for q in sorted(support)]
+        ei = [i for i, e in enumerate(edges) if e[0] in support or e[1] in support]
+        zz = [zzg[k][i] for i in ei]
+        for i in ei:
+            support.update(edges[i])
         kept_layers.append(zz + rx)
-    gates = [Gate("H", (q,)) for q in sorted(support)]
+    gates = [hg[q] for q in sorted(support)]
     for lay in reversed(kept_layers):
         gates.extend(lay)
     return tuple(gates), frozenset(support)

@@ -430,3 +430,40 @@ def test_c64_precision_model_cfg2(ci):
     want = rec["zz"][0]
     v = run_program(prog, [raw])[0]
     assert abs(v.real - want) <= 1e-5 * abs(want)
+
+
+def test_native_dry_run_and_slicing_match_python():
+    """qtn_dry_run / qtn_suggest_slicing (csrc/planner.cpp) against their
+    Python restatements (ordering.dry_run_py / suggest_slicing_py) on golden
+    amplitude networks, the cfg-3 reference cone and random networks."""
+    from paper_2210_15874_b200 import ordering as OR
+    nets = []
+    for rec in load_json("networks.json"):
+        tn = Q.amplitude_network(Q.Circuit(rec["n"], _gates(rec)), rec["bits"])
+        nets.append((tn, rec["order_minfill"], [rec.get("slice_target", 3), 2]))
+    g, graph, params = _cfg("cfg3")
+    lc = Q.extract_lightcone(Q.qaoa_maxcut_circuit(graph, params), tuple(g["ref_cone"]["edge"]))
+    nets.append((lc.network, g["ref_cone"]["order"], [20, 14]))
+    rng = np.random.default_rng(7)
+    for _ in range(20):
+        n_idx = int(rng.integers(6, 30))
+        ts = [Q.Tensor(tuple(int(x) for x in rng.choice(n_idx, size=int(rng.integers(1, 5)), replace=False)),
+                       np.ones((2,) * 1)) if False else None for _ in range(0)]
+        ts = []
+        for _ in range(int(rng.integers(5, 25))):
+            r = int(rng.integers(1, 5))
+            ids = tuple(int(x) for x in rng.choice(n_idx, size=r, replace=False))
+            ts.append(Q.Tensor(ids, np.ones((2,) * r)))
+        tn = Q.TensorNetwork(ts)
+        order = [int(x) for x in rng.permutation(sorted(tn.all_indices()))]
+        nets.append((tn, order, [2, 3, 4]))
+    for tn, order, targets in nets:
+        assert Q.dry_run(tn, order) == OR.dry_run_py(tn, order)
+        for t in targets:
+            sl = Q.suggest_slicing(tn, order, t)
+            assert sl == OR.suggest_slicing_py(tn, order, t)
+            assert Q.dry_run(tn, order, fixed=sl) == OR.dry_run_py(tn, order, fixed=sl)
+    with pytest.raises(ValueError, match="missing"):
+        Q.dry_run(nets[0][0], nets[0][1][:-1])
+    with pytest.raises(ValueError, match="target_width"):
+        Q.suggest_slicing(nets[0][0], nets[0][1], 0)
