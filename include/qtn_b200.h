@@ -97,17 +97,8 @@ typedef struct {
   uint32_t stmask;    /* tile bits each thread walks sequentially (vector
                          path; 0 = default).  Members not carrying any of
                          them are multiplied once per tile and reused.       */
-  int32_t group;      /* K2 stages: > 0 on the root of a CTA group — the
-                         `group` items ending here (a subtree of the in-tree,
-                         numbered consecutively, children first) run in ONE
-                         block on one ticket, every non-root result kept in
-                         shared memory (double) at element offset out_off;
-                         members with cls & QTN_K2_SMEM read it there.  0
-                         otherwise.                                         */
-  int32_t reserved;
+  int32_t reserved[2];
 } qtn_bucket_t;
-/* K2 group member read from the group's shared-memory results (cls bit). */
-#define QTN_K2_SMEM 0x80000000u
 
 /* Dependency: wait until bucket `bucket` has completed `need` tiles. */
 typedef struct {

@@ -69,10 +69,9 @@ PLAN_ARRAYS = ("w", "k", "L", "level", "out_off", "mem_ptr", "mem_kind", "mem_re
 BUCKET_DT = np.dtype([
     ("out_off", "<u8"), ("w", "<i4"), ("tile_bits", "<i4"), ("k", "<i4"), ("mem_begin", "<i4"),
     ("n_mem", "<i4"), ("dep_begin", "<i4"), ("n_dep", "<i4"), ("tick_begin", "<i4"),
-    ("n_tiles", "<i4"), ("slot", "<i4"), ("smem_elems", "<i4"), ("stmask", "<u4"), ("group", "<i4"),
-    ("reserved", "<i4"),
+    ("n_tiles", "<i4"), ("slot", "<i4"), ("smem_elems", "<i4"), ("stmask", "<u4"), ("reserved0", "<i4"),
+    ("reserved1", "<i4"),
 ])
-QTN_K2_SMEM = 0x80000000
 MEMBER_DT = np.dtype([("off", "<u8"), ("mask", "<u8"), ("smask", "<u4"), ("cls", "<u4")])
 NODE_DT = np.dtype([("kind", "<i4"), ("first", "<i4"), ("count", "<i4"), ("n_tickets", "<i4"),
                     ("variant", "<i4"), ("dep_begin", "<i4"), ("n_dep", "<i4"), ("smem_bytes", "<i4")])

@@ -231,125 +231,12 @@ struct SmallCtx {
   int32_t pclo[MAXM];
   int16_t sig[MAXM][MAXNS];
   int32_t hmode[MAXM];   // 1: input member staged unrounded in shi (complex64 programs, rank <= 6)
-  int32_t gflag[MAXM];   // CTA group: 1 = member is a group result in shared memory
   int32_t item;
   int32_t tick;
   int32_t next;
   int32_t last;
   int32_t item_end;   // first ticket after the current item
 };
-
-// K2 CTA group (see qtn_bucket_t.group): items g0 .. root back to back in
-// this block, every non-root result in shared memory (double).  Kept out of
-// line so the ticketed path keeps its own register allocation.
-template <typename R>
-__device__ __forceinline__ void k2_group(const qtn_program_t& P, SmallCtx& S, int root, uint32_t* done,
-                                      unsigned char* smem_raw) {
-  using T = typename Cx<R>::T;
-  using D = double2;
-  constexpr bool HI = Cx<R>::VEC == 2;
-  D* sprod = reinterpret_cast<D*>(smem_raw);
-  double2* shi = reinterpret_cast<double2*>(smem_raw + SMALL_PROD_ELEMS * sizeof(D));
-  D* gsm = reinterpret_cast<D*>(smem_raw + SMALL_PROD_ELEMS * sizeof(D) + MAXM * K2_HI_SLOT * sizeof(double2));
-  const T* A = reinterpret_cast<const T*>(P.arena);
-  T* Aw = reinterpret_cast<T*>(P.arena);
-  const double2* Ahi = reinterpret_cast<const double2*>(P.inputs_hi);
-  const uint64_t n_hi = (HI && Ahi) ? (uint64_t)P.n_in_elems : 0ull;
-  const int tid = threadIdx.x;
-  const int g0 = root - S.b.group + 1;
-  for (int gi = g0; gi <= root; ++gi) {
-    __syncthreads();   // the previous item is done with S and the staging areas
-    if (tid == 0) S.b = P.buckets[gi];
-    __syncthreads();
-    const int nm = S.b.n_mem;
-    const int L = S.b.tile_bits;
-    const int k = S.b.k;
-    if (tid < nm) {
-      const qtn_member_t m = P.members[S.b.mem_begin + tid];
-      const uint32_t lowmask = (1u << L) - 1u;
-      S.off[tid] = m.off;
-      S.mlo[tid] = (uint32_t)(m.mask & lowmask);
-      S.mhi[tid] = m.mask >> L;
-      S.pc[tid] = __popcll(m.mask);
-      S.pclo[tid] = __popc((uint32_t)(m.mask & lowmask));
-      for (int q = 0; q < (1 << k); ++q) S.sig[tid][q] = (int16_t)pext32((uint32_t)q, m.smask);
-      const int lg = __popcll(m.mask) + __popc(m.smask);
-      S.gflag[tid] = (m.cls & QTN_K2_SMEM) ? 1 : 0;
-      S.hmode[tid] = (!(m.cls & QTN_K2_SMEM) && lg <= 6) ? 1 : 0;   // small global member: staged
-    }
-    for (int d = tid; d < S.b.n_dep; d += NT) {
-      const qtn_dep_t dp = P.deps[S.b.dep_begin + d];
-      const uint32_t* c = done + dp.bucket;
-      int spins = 0;
-      while (ld_acquire(c) < (uint32_t)dp.need) {
-        if (++spins > 64) __nanosleep(32);
-      }
-    }
-    __syncthreads();
-    // small global members (gates, earlier results) staged as doubles:
-    // one round trip for all of them
-    for (int e = tid; e < nm * K2_HI_SLOT; e += NT) {
-      const int i = e / K2_HI_SLOT, q = e % K2_HI_SLOT;
-      if (S.hmode[i] && q < (1 << (S.pc[i] + __popc(P.members[S.b.mem_begin + i].smask)))) {
-        const uint64_t o = S.off[i] + q;
-        QTN_CHECK(QTN_ARENA_OK(P, o), "group item %d member %d off %lld", gi, i, (long long)o);
-        shi[e] = (HI && o < n_hi) ? __ldg(Ahi + o) : widen(__ldcg(A + o));
-      }
-    }
-    __syncthreads();
-    unsigned long long t_start = 0;
-    if (P.timing && tid == 0) t_start = globaltimer();
-    const int ns = 1 << k;
-    const int nelem = 1 << L;
-    const int chunk = max(1, min(ns, SMALL_PROD_ELEMS / nelem));
-    for (int h = 0; h < S.b.n_tiles; ++h) {
-      if (tid < nm) S.base[tid] = S.off[tid] + (pext64((uint64_t)h, S.mhi[tid]) << S.pclo[tid]);
-      __syncthreads();
-      D acc = D{};
-      for (int s0 = 0; s0 < ns; s0 += chunk) {
-        const int cs = min(chunk, ns - s0);
-        const int nu = cs * nelem;
-        for (int u = tid; u < nu; u += NT) {
-          const int ue = u & (nelem - 1);
-          const int us = s0 + (u >> L);
-          D prod = D{};
-          for (int i = 0; i < nm; ++i) {
-            const uint64_t o = S.base[i] + ((uint64_t)S.sig[i][us] << S.pc[i]) +
-                               (S.pclo[i] == L ? (uint64_t)ue : (uint64_t)pext32((uint32_t)ue, S.mlo[i]));
-            D x;
-            if (S.gflag[i]) {
-              x = gsm[o];
-            } else if (S.hmode[i]) {
-              x = shi[i * K2_HI_SLOT + (int)(o - S.off[i])];
-            } else {
-              QTN_CHECK(QTN_ARENA_OK(P, o), "group item %d member %d off %lld", gi, i, (long long)o);
-              x = (HI && o < n_hi) ? __ldg(Ahi + o) : widen(__ldcg(A + o));
-            }
-            prod = i == 0 ? x : cmul(prod, x);
-          }
-          sprod[u] = prod;
-        }
-        __syncthreads();
-        if (tid < nelem)
-          for (int c = 0; c < cs; ++c) acc = (s0 + c == 0) ? sprod[c * nelem + tid] : cadd(acc, sprod[c * nelem + tid]);
-        __syncthreads();
-      }
-      if (tid < nelem) {
-        const uint64_t o = S.b.out_off + (uint64_t)h * nelem + tid;
-        if (gi == root) {
-          QTN_CHECK(QTN_ARENA_OK(P, o), "group root %d out", gi);
-          narrow(acc, Aw[o]);
-        } else {
-          gsm[o] = acc;
-        }
-      }
-    }
-    if (P.timing && tid == 0) {
-      atomicMin(&P.timing[2 * gi], t_start);
-      atomicMax(&P.timing[2 * gi + 1], globaltimer());
-    }
-  }
-}
 
 template <typename R>
 __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_t first, int32_t count,
@@ -420,21 +307,6 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
     }
     __syncthreads();
     cur = S.item;
-    if (S.b.group > 0) {
-      // ---- CTA group: a subtree's items back to back in this block, every
-      // non-root result in shared memory (double), barriers instead of
-      // completion counters; the root's tiles are published at the end ----
-      if (tid == 0 && pend_cnt) {
-        publish_tiles(&done[pend_item], pend_cnt);
-        pend_cnt = 0;
-      }
-      k2_group<R>(P, S, cur, done, smem_raw);
-      const int root = cur;
-      __syncthreads();   // the root's stores before its publish
-      if (tid == 0) publish_tiles(&done[root], (uint32_t)S.b.n_tiles);
-      prepared = -1;
-      continue;
-    }
     if (cur != prepared) {
       // publish finished tiles of the previous item before any waiting
       if (tid == 0 && pend_cnt) {

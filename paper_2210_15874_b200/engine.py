@@ -75,18 +75,6 @@ _KL = os.environ.get("QTN_KMAX_LARGE")
 KMAX_LARGE = {"complex64": int(_KL) if _KL else 3, "complex128": int(_KL) if _KL else 3}
 SMALL_PROD_ELEMS = 1024   # smem products per round of a small tile (csrc)
 K2_HI_SLOT = 64           # staged unrounded input member per K2 item (csrc)
-# K2 CTA groups: a subtree of small items run by ONE block, non-root results
-# in shared memory (double).  Budget per block and the cost model that
-# decides a group: a ticketed K2 item on a dependency chain costs ~3 us
-# (ticket, item/member/dependency loads, member loads, publish: ~5 dependent
-# L2 round trips, r02 timeline); inside a group an item costs a barrier and
-# its rounds of (element, assignment) units from shared memory.
-K2_GROUP_SMEM = 64 * 1024
-K2_GROUPS = os.environ.get("QTN_K2_GROUPS", "0") != "0"   # experimental: off until the batched group prologue lands
-K2_CHAIN_ITEM_S = 3.0e-6
-K2_GROUP_ITEM_S = 0.35e-6
-K2_GROUP_ROUND_S = 0.06e-6     # one round = 2 x NT (element, assignment) units
-K2_GROUP_MAX_ITER_BITS = 12    # w + k of a group item: one block does all its units
 VEC = {"complex64": 2, "complex128": 1}
 # merge cost model (seconds).  Effective constants, tuned end to end on the
 # B200 (sweep over hop cost and term rate, profiles/r01_configs.md): a K1
@@ -660,65 +648,6 @@ def template_peak_elems(t: Template) -> int:
     return pool.top
 
 
-def _plan_groups(items, keys, tls, prods, groups, group_of):
-    """CTA groups of one K2 stage (items in topological order).  Top-down:
-    an unassigned item g (not a finaliser) grows a group over its in-stage
-    producers (an in-tree: each has g's group as its only consumer) whose
-    results fit K2_GROUP_SMEM as doubles, smallest first; the group is kept
-    when one block running its items back to back beats the ticketed chain
-    (K2_CHAIN_ITEM_S per item of its deepest path)."""
-    inset = set(items)
-
-    def wk(g):
-        _, i, b = keys[g]
-        return tls[i]["w"][b], tls[i]["k"][b]
-
-    def big_inputs(g):
-        # members a group block would read straight from global memory inside
-        # its unit loop (rank > 6: not staged) — latency-bound there
-        _, i, b = keys[g]
-        tl = tls[i]
-        return sum(1 for j in range(tl["mem_ptr"][b], tl["mem_ptr"][b + 1])
-                   if _popc(int(tl["mem_mask"][j])) + _popc(int(tl["mem_smask"][j])) > 6)
-
-    def fits(x):
-        w, k = wk(x)
-        return w + k <= K2_GROUP_MAX_ITER_BITS
-
-    for g in reversed(items):
-        if g in group_of or keys[g][2] < 0 or not fits(g):
-            continue
-        members, used = [], 0
-
-        def grow(x):
-            nonlocal used
-            kids = sorted((p for p in prods[x] if p in inset and p not in group_of and keys[p][2] >= 0 and fits(p)),
-                          key=lambda p: wk(p)[0])
-            d = 0
-            for c in kids:
-                size = 16 << wk(c)[0]
-                if used + size > K2_GROUP_SMEM:
-                    continue
-                used += size
-                d = max(d, grow(c))
-                members.append(c)
-            return d + 1
-
-        dmax = grow(g)
-        grp = members + [g]
-        # every big member must be a group result (shared memory)
-        inner = set(grp)
-        if len(grp) < 2 or any(big_inputs(x) > sum(1 for p in prods[x] if p in inner) for x in grp):
-            continue
-        cost = sum(K2_GROUP_ITEM_S + -(-(1 << sum(wk(x))) // (2 * NT)) * K2_GROUP_ROUND_S for x in grp)
-        if cost >= dmax * K2_CHAIN_ITEM_S:
-            continue
-        # children first: post-order (members were appended after their own kids)
-        groups[g] = grp
-        for x in grp:
-            group_of[x] = g
-
-
 @dataclass
 class Instance:
     template: Template
@@ -844,26 +773,6 @@ class Program:
                 nodes.append({"kind": N.QTN_NODE_LARGE, "items": [g], "deps": set(ext)})
                 node_of[g] = len(nodes) - 1
 
-        # ---- K2 CTA groups (subtrees of small items in one block) ----
-        groups = {}          # root g -> [g ...] children first, root last
-        group_of = {}        # g -> root g
-        if K2_GROUPS and not self.reuse:
-            for nd in nodes:
-                if nd["kind"] == N.QTN_NODE_SMALL:
-                    _plan_groups(nd["items"], keys, tls, prods, groups, group_of)
-            for nd in nodes:
-                if nd["kind"] != N.QTN_NODE_SMALL or not any(g in groups for g in nd["items"]):
-                    continue
-                order_ = []
-                for g in nd["items"]:
-                    if g in groups:
-                        order_.extend(groups[g])
-                    elif g not in group_of:
-                        order_.append(g)
-                assert sorted(order_) == sorted(nd["items"])
-                nd["items"] = order_
-                nd["groups"] = True
-
         # ---- final item numbering: node by node (stage items contiguous) ----
         new_of = {}
         for nd in nodes:
@@ -898,30 +807,20 @@ class Program:
             assert gids == list(range(first, first + count))
             tick = 0
             is_stage = nd["kind"] == small_kind
-            # K2 stage: double-precision products + staged unrounded input
-            # members (+ the CTA groups' shared-memory results)
+            # K2 stage: double-precision products + staged unrounded input members
             node_smem = SMALL_PROD_ELEMS * 16 + N.MAX_MEMBERS * K2_HI_SLOT * 16 if is_stage else 0
-            if nd.get("groups"):
-                node_smem += K2_GROUP_SMEM
             variant = 0
-            gsm = {}          # group item -> shared-memory element offset of its result
             for gid in gids:
                 (_, i, b), g = item_keys[gid]
                 tl = tls[i]
                 ib = in_base[i]
                 mem_begin, dep_begin = len(members), len(deps)
-                root = group_of.get(g)
-                if root is not None and root != g:
-                    gsm[g] = sum(1 << tls[i]["w"][keys[x][2]] for x in gsm if group_of[x] == root)
                 if b >= 0:
                     in_off, mk, mr = tl["in_off"], tl["mem_kind"], tl["mem_ref"]
                     mm, msm, mc = tl["mem_mask"], tl["mem_smask"], tl["mem_cls"]
                     j0, j1 = tl["mem_ptr"][b], tl["mem_ptr"][b + 1]
                     for j in range(j0, j1):
                         ref = mr[j]
-                        if mk[j] == 1 and order_gid[(i, ref)] in gsm and root is not None:
-                            members.append((gsm[order_gid[(i, ref)]], mm[j], msm[j], N.QTN_K2_SMEM))
-                            continue
                         off = ib + in_off[ref] if mk[j] == 0 else out_elem[order_gid[(i, ref)]]
                         members.append((off, mm[j], msm[j], mc[j]))
                     if not is_stage:
@@ -936,22 +835,15 @@ class Program:
                         members.append((off, 0, 0, 0))
                     w_, k_, L_, out_, slot_, nmem_ = N.QTN_FINALIZE, 0, 0, 0, i, len(tl["fin_kind"])
                     smem_, stm_ = 0, 0
-                # completion dependencies inside this stage (RAW + WAR); a
-                # group's own items are ordered by its block
+                # completion dependencies inside this stage (RAW + WAR)
                 for dg in deps_all[g]:
-                    if node_of[dg] == ni and not (root is not None and group_of.get(dg) == root):
+                    if node_of[dg] == ni:
                         pg = new_of[dg]
                         deps.append((pg, ntiles[pg]))
-                grp = 0
-                if root is not None and root != g:
-                    out_ = gsm[g]         # result in shared memory
-                elif root == g:
-                    grp = len(groups[g])
                 # BUCKET_DT field order
                 recs[gid] = (out_, w_, L_, k_, mem_begin, nmem_, dep_begin, len(deps) - dep_begin,
-                             tick if is_stage else 0, ntiles[gid], slot_, smem_, stm_, grp, 0)
-                # a group takes one ticket, on its root
-                tick += (0 if root != g else 1) if root is not None else ntiles[gid]
+                             tick if is_stage else 0, ntiles[gid], slot_, smem_, stm_, 0, 0)
+                tick += ntiles[gid]
             smem_max = max(smem_max, node_smem)
             dl = sorted(nd["deps"])
             node_list.append((nd["kind"], first, count, tick if is_stage else 0,

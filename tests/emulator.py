@@ -8,9 +8,7 @@ finaliser = product of rank-0 values.  Lets the planner be checked on CPU.
 Precision model of complex64 programs (qtn_program_t.inputs_hi): K2 stage
 items (small nodes) and finalisers compute in double, reading input members
 of rank <= 6 unrounded; large items compute in complex64 from the narrowed
-arena; every stored intermediate is complex64 — except inside K2 CTA groups
-(qtn_bucket_t.group): a group's non-root results stay in (double) shared
-memory, and its items read every input member unrounded."""
+arena; every stored intermediate is complex64."""
 import numpy as np
 
 from paper_2210_15874_b200 import _native as N
@@ -37,12 +35,6 @@ def run_program(prog, raw_parts):
         A = A.astype(np.complex64)
     res = np.zeros(len(prog.instances), np.complex128)
     B = prog.buckets
-    # K2 CTA groups: item -> root; a root's group starts group-1 items before it
-    group_root = {}
-    for r in range(len(B)):
-        for x in range(r - int(B[r]["group"]) + 1, r + 1) if int(B[r]["group"]) > 0 else ():
-            group_root[x] = r
-    gsm = {}   # root -> shared-memory results of its group (complex128)
     done = set()
     node_done = set()
     for ni, nd in enumerate(prog.nodes):
@@ -66,9 +58,6 @@ def run_program(prog, raw_parts):
             else:
                 w, k = int(b["w"]), int(b["k"])
                 r = np.arange(1 << w, dtype=np.int64)
-                root = group_root.get(int(g))
-                if root is not None and root not in gsm:
-                    gsm[root] = np.zeros(1 << 16, np.complex128)
                 acc = None
                 for s in range(1 << k):
                     p = None
@@ -76,12 +65,7 @@ def run_program(prog, raw_parts):
                         mask, smask = int(m["mask"]), int(m["smask"])
                         pc = bin(mask).count("1")
                         o = int(m["off"]) + (int(pext_vec(np.array([s]), smask)[0]) << pc) + pext_vec(r, mask)
-                        if root is not None and int(m["cls"]) & N.QTN_K2_SMEM:
-                            x = gsm[root][o]
-                        elif root is not None:
-                            x = np.where(o < n_hi, hi[np.minimum(o, max(n_hi - 1, 0))], A[o].astype(np.complex128)) \
-                                if n_hi else A[o].astype(np.complex128)
-                        elif small and n_hi:
+                        if small and n_hi:
                             staged = int(m["off"]) < n_hi and pc + bin(smask).count("1") <= 6
                             x = hi[o] if staged else A[o].astype(np.complex128)
                         else:
@@ -89,10 +73,7 @@ def run_program(prog, raw_parts):
                         p = x.copy() if p is None else p * x
                     acc = p if acc is None else acc + p
                 o = int(b["out_off"])
-                if root is not None and root != int(g):
-                    gsm[root][o: o + (1 << w)] = acc
-                else:
-                    A[o: o + (1 << w)] = acc.astype(A.dtype)
+                A[o: o + (1 << w)] = acc.astype(A.dtype)
             done.add(int(g))
         node_done.add(ni)
     return res
