@@ -82,6 +82,9 @@ struct Plan {
   int64_t btb[TBB];                     // B strides of the thread bits
   int32_t otb[TBB], ftb[TBB];           // out stride / F index bit of the thread bits
   int32_t oe[MAXE], fe[MAXE];           // out stride / F index bit of the expansion bits
+  int32_t rb;                           // replica bit present (RB = 2): a B bit no other member carries
+  int64_t rbs;                          // its B stride
+  int32_t rbo;                          // its output stride
   unsigned long long* timing;
   int32_t item;
 };
@@ -107,19 +110,22 @@ __device__ __forceinline__ void cfma(T& acc, T a, T b) {
 #define K4_C64_MINB 4
 #endif
 
-template <typename R, int K, int NE>
+template <typename R, int K, int NE, int RB>
 __device__ __forceinline__ void k4_body(const Plan& P);
 
-template <typename R, int K, int NE>
-__global__ void __launch_bounds__(NT, K4_C64_MINB) k4_kernel_c64(const __grid_constant__ Plan P) {
-  k4_body<R, K, NE>(P);
+template <typename R, int K, int NE, int RB>
+__global__ void __launch_bounds__(NT, RB == 2 ? 3 : K4_C64_MINB) k4_kernel_c64(const __grid_constant__ Plan P) {
+  k4_body<R, K, NE, RB>(P);
 }
-template <typename R, int K, int NE>
+template <typename R, int K, int NE, int RB>
 __global__ void __launch_bounds__(NT) k4_kernel_c128(const __grid_constant__ Plan P) {
-  k4_body<R, K, NE>(P);
+  k4_body<R, K, NE, RB>(P);
 }
 
-template <typename R, int K, int NE>
+// RB = 2: each thread also owns the B coordinate one "replica bit" over (a B
+// bit no other member carries): both share every product-table row, so each
+// row read from shared memory serves two results.
+template <typename R, int K, int NE, int RB>
 __device__ __forceinline__ void k4_body(const Plan& P) {
   using T = typename Cx<R>::T;
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -198,14 +204,16 @@ __device__ __forceinline__ void k4_body(const Plan& P) {
         obase += P.hs[nm][b];
       }
     // B for all s (registers), issued before a possible F rebuild
-    T bv[NS];
+    T bv[RB][NS];
     const T* bp = Bm + bb + boff;
 #pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      K4_CHECK(bb + boff + soffB[s] >= 0 && bb + boff + soffB[s] < P.span[P.iB], "B element %lld of %lld",
-               (long long)(bb + boff + soffB[s]), (long long)P.span[P.iB]);
-      bv[s] = __ldg(bp + soffB[s]);
-    }
+    for (int r = 0; r < RB; ++r)
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const int64_t o = bb + boff + soffB[s] + (r ? P.rbs : 0);
+        K4_CHECK(o >= 0 && o < P.span[P.iB], "B element %lld of %lld", (long long)o, (long long)P.span[P.iB]);
+        bv[r][s] = __ldg(bp + soffB[s] + (r ? P.rbs : 0));
+      }
     if ((h >> shf) != fkey) {
       fkey = h >> shf;
       __syncthreads();   // previous F no longer read
@@ -236,12 +244,19 @@ __device__ __forceinline__ void k4_body(const Plan& P) {
     for (int e = 0; e < NEV; ++e) {
       K4_CHECK(fe[e] + NS <= nfe, "F entry %d of %d", fe[e] + NS, nfe);
       const T* fp = F + fe[e];
-      T acc = cmul(bv[0], fp[0]);
+      T fr[NS];
 #pragma unroll
-      for (int s = 1; s < NS; ++s) cfma(acc, bv[s], fp[s]);
-      K4_CHECK(obase + ob + oe[e] >= 0 && obase + ob + oe[e] < P.out_elems, "result %lld of %lld",
-               (long long)(obase + ob + oe[e]), (long long)P.out_elems);
-      op[oe[e]] = acc;
+      for (int s = 0; s < NS; ++s) fr[s] = fp[s];
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        T acc = cmul(bv[r][0], fr[0]);
+#pragma unroll
+        for (int s = 1; s < NS; ++s) cfma(acc, bv[r][s], fr[s]);
+        const int64_t o = oe[e] + (r ? P.rbo : 0);
+        K4_CHECK(obase + ob + o >= 0 && obase + ob + o < P.out_elems, "result %lld of %lld",
+                 (long long)(obase + ob + o), (long long)P.out_elems);
+        op[o] = acc;
+      }
     }
   }
   if (P.timing && tid == 0) {
@@ -252,30 +267,35 @@ __device__ __forceinline__ void k4_body(const Plan& P) {
   }
 }
 
-template <typename R, int K, int NE>
+template <typename R, int K, int NE, int RB>
 const void* fn_k() {
   if constexpr (sizeof(R) == 4)
-    return (const void*)k4_kernel_c64<R, K, NE>;
+    return (const void*)k4_kernel_c64<R, K, NE, RB>;
   else
-    return (const void*)k4_kernel_c128<R, K, NE>;
+    return (const void*)k4_kernel_c128<R, K, NE, RB>;
 }
 
-template <typename R, int K>
+template <typename R, int K, int RB>
 const void* fn_ne(int ne) {
   switch (ne) {
-    case 0: return fn_k<R, K, 0>();
-    case 1: return fn_k<R, K, 1>();
-    case 2: return fn_k<R, K, 2>();
-    case 3: return fn_k<R, K, 3>();
-    default: return fn_k<R, K, 4>();
+    case 0: return fn_k<R, K, 0, RB>();
+    case 1: return fn_k<R, K, 1, RB>();
+    case 2: return fn_k<R, K, 2, RB>();
+    case 3: return fn_k<R, K, 3, RB>();
+    default: return fn_k<R, K, 4, RB>();
   }
 }
 
 template <typename R>
-const void* fn_of(int k, int ne) {
-  if (k == 1) return fn_ne<R, 1>(ne);
-  if (k == 2) return fn_ne<R, 2>(ne);
-  return fn_ne<R, 3>(ne);
+const void* fn_of(int k, int ne, int rb) {
+  if (rb) {
+    if (k == 1) return fn_ne<R, 1, 2>(ne);
+    if (k == 2) return fn_ne<R, 2, 2>(ne);
+    return fn_ne<R, 3, 2>(ne);
+  }
+  if (k == 1) return fn_ne<R, 1, 1>(ne);
+  if (k == 2) return fn_ne<R, 2, 1>(ne);
+  return fn_ne<R, 3, 1>(ne);
 }
 
 int fail(int code, const char* fmt, ...) {
@@ -327,8 +347,8 @@ int make_plan(const qtn_bucket_desc_t* d, int min_e, Plan* P, int* smem) {
   // B bits NO other member carries, so every lane of a warp reads the same
   // product-table row (shared-memory broadcast instead of bank conflicts);
   // then the remaining B bits, ascending.  Warps: the next 3.
+  bool used[64] = {};
   {
-    bool used[64] = {};
     const int sec = (int)(32 / esz);
     auto take = [&](int b) { tb[nt++] = b; used[b] = true; };
     for (int b = 0; b < w && nt < TBB; ++b)   // B's local axes 0 .. log2(sec)-1
@@ -340,10 +360,20 @@ int make_plan(const qtn_bucket_desc_t* d, int min_e, Plan* P, int* smem) {
       if (B.strides[b] != 0 && !used[b]) take(b);
   }
   if (ne < min_e) return fail(QTN_E_UNSUPPORTED, "K4: %d expansion bits", ne);
-  // tile bits T = tb u eb; F bits = T bits any other member carries
+  // replica bit: the first remaining B bit no other member carries (each
+  // thread then owns two B coordinates sharing every product-table row —
+  // half the shared-memory row reads).  Measured on cfg-2: complex128 all
+  // items and complex64 k = 3 gain (w21 k3: 21.3 -> 12.6 us c128, 44 -> 15 us
+  // c64); complex64 k <= 2 loses (w24 k2: 46 -> 54 us: 3 blocks/SM instead of 4)
+  int rbit = -1;
+  if (d->dtype == QTN_C128 || k == 3)
+    for (int b = 0; b < w && rbit < 0; ++b)
+      if (B.strides[b] != 0 && !used[b] && !carried[b]) rbit = b;
+  // tile bits T = tb u eb (u the replica bit); F bits = T bits any other member carries
   bool inT[64] = {};
   for (int i = 0; i < nt; ++i) inT[tb[i]] = true;
   for (int i = 0; i < ne; ++i) inT[eb[i]] = true;
+  if (rbit >= 0) inT[rbit] = true;
   int fbit[64], nf = 0;
   for (int b = 0; b < w; ++b) {
     fbit[b] = -1;
@@ -408,6 +438,9 @@ int make_plan(const qtn_bucket_desc_t* d, int min_e, Plan* P, int* smem) {
     P->oe[i] = 1 << eb[i];
     P->fe[i] = fbit[eb[i]] >= 0 ? 1 << fbit[eb[i]] : 0;
   }
+  P->rb = rbit >= 0 ? 1 : 0;
+  P->rbs = rbit >= 0 ? B.strides[rbit] : 0;
+  P->rbo = rbit >= 0 ? (int32_t)1 << rbit : 0;
   *smem = (int)(esz << (nf + k)) + nm * 128 * 4;
   (void)esz;
   return QTN_OK;
@@ -427,7 +460,7 @@ int qtn_k4_node(const qtn_bucket_desc_t* d, int min_e, unsigned long long* timin
   if (rc) return rc;
   P->timing = timing;
   P->item = item;
-  *fn = d->dtype == QTN_C64 ? fn_of<float>(P->k, P->nE) : fn_of<double>(P->k, P->nE);
+  *fn = d->dtype == QTN_C64 ? fn_of<float>(P->k, P->nE, P->rb) : fn_of<double>(P->k, P->nE, P->rb);
   cudaFuncAttributes fa;
   cudaError_t e = cudaFuncGetAttributes(&fa, *fn);
   if (e != cudaSuccess) return fail(QTN_E_CUDA, "cudaFuncGetAttributes: %s", cudaGetErrorString(e));
