@@ -193,6 +193,16 @@ typedef struct {
   const void* d2h_src;   /* device result slots                           */
   void* d2h_dst;         /* pinned host result buffer                     */
   int64_t d2h_bytes;     /* 0 = no download node                          */
+  /* Device-side input gather (instead of an upload node; n_gather > 0): a
+   * first kernel node reads the RAW input tensors (complex128, concatenated
+   * in pinned host memory, device-mapped) and writes input element t of the
+   * canonical image: arena[gather_dst[t]] = narrowed raw[gather_src[t]] (and
+   * inputs_hi[gather_dst[t]] = raw[gather_src[t]] for complex64 programs) —
+   * no host-side gather, no copy-engine round trip. */
+  const void* gather_raw;      /* pinned host, complex128                    */
+  const int64_t* gather_src;   /* device: raw element per image element      */
+  const int64_t* gather_dst;   /* device: arena element per image element     */
+  int64_t n_gather;
 } qtn_graph_io_t;
 int qtn_graph_create_io(const qtn_program_t* prog, const qtn_node_t* nodes, int32_t n_nodes,
                         const int32_t* node_deps, const qtn_graph_io_t* io, qtn_graph_t** out);

@@ -114,7 +114,9 @@ class BucketDescC(ctypes.Structure):
 class GraphIOC(ctypes.Structure):
     """qtn_graph_io_t: input upload / result download nodes of a program graph."""
     _fields_ = [("h2d_src", ctypes.c_void_p), ("h2d_dst", ctypes.c_void_p), ("h2d_bytes", ctypes.c_int64),
-                ("d2h_src", ctypes.c_void_p), ("d2h_dst", ctypes.c_void_p), ("d2h_bytes", ctypes.c_int64)]
+                ("d2h_src", ctypes.c_void_p), ("d2h_dst", ctypes.c_void_p), ("d2h_bytes", ctypes.c_int64),
+                ("gather_raw", ctypes.c_void_p), ("gather_src", ctypes.c_void_p), ("gather_dst", ctypes.c_void_p),
+                ("n_gather", ctypes.c_int64)]
 
 
 class PlanParamsC(ctypes.Structure):

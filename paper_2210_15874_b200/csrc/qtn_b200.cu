@@ -917,6 +917,20 @@ struct LargeK<double, NS, NV, ST, NB0> {
   static constexpr auto fn = large_kernel_c128<NS, NV, ST, NB0>;
 };
 
+// ---- input gather: raw tensors (pinned host, mapped) -> canonical image ----
+template <typename R>
+__global__ void __launch_bounds__(NT) gather_kernel(const double2* __restrict__ raw, const int64_t* __restrict__ src,
+                                                   const int64_t* __restrict__ dst, int64_t n,
+                                                   typename Cx<R>::T* __restrict__ arena, double2* __restrict__ hi) {
+  pdl_launch_dependents();
+  for (int64_t t = (int64_t)blockIdx.x * NT + threadIdx.x; t < n; t += (int64_t)gridDim.x * NT) {
+    const double2 v = raw[src[t]];
+    const int64_t o = dst[t];
+    narrow(v, arena[o]);
+    if (hi) hi[o] = v;
+  }
+}
+
 // ---- permutation (tensors entering a program in a non-canonical layout) ----
 struct PermStrides {
   int64_t s[QTN_MAX_WIDTH + 4];
@@ -1283,7 +1297,35 @@ int qtn_graph_create_host(const qtn_program_t* p, const qtn_bucket_t* items, con
   std::vector<LaunchSpec> specs(n_nodes);
   // optional input upload: every kernel node without a predecessor waits for it
   cudaGraphNode_t h2d = nullptr;
-  if (io && io->h2d_bytes > 0) {
+  if (io && io->n_gather > 0) {
+    // device-side gather of the raw inputs (mapped pinned host memory)
+    if (!io->gather_raw || !io->gather_src || !io->gather_dst || !p->arena) {
+      qtn_graph_destroy(g);
+      return set_err(QTN_E_INVALID, "gather: null pointer");
+    }
+    static thread_local struct {
+      const void* raw;
+      const int64_t* src;
+      const int64_t* dst;
+      int64_t n;
+      void* arena;
+      void* hi;
+    } ga;
+    ga = {io->gather_raw, io->gather_src, io->gather_dst, io->n_gather, p->arena, const_cast<void*>(p->inputs_hi)};
+    void* args[] = {&ga.raw, &ga.src, &ga.dst, &ga.n, &ga.arena, &ga.hi};
+    cudaKernelNodeParams kp = {};
+    kp.func = p->dtype == QTN_C64 ? (void*)gather_kernel<float> : (void*)gather_kernel<double>;
+    const int64_t blocks = std::min<int64_t>((io->n_gather + NT - 1) / NT, (int64_t)sm_count() * 4);
+    kp.gridDim = dim3((unsigned)std::max<int64_t>(1, blocks));
+    kp.blockDim = dim3(NT);
+    kp.sharedMemBytes = 0;
+    kp.kernelParams = args;
+    e = cudaGraphAddKernelNode(&h2d, g->graph, nullptr, 0, &kp);   // parameters copied at node creation
+    if (e != cudaSuccess) {
+      qtn_graph_destroy(g);
+      return cuda_err(e, "cudaGraphAddKernelNode(gather)");
+    }
+  } else if (io && io->h2d_bytes > 0) {
     e = cudaGraphAddMemcpyNode1D(&h2d, g->graph, nullptr, 0, io->h2d_dst, io->h2d_src, (size_t)io->h2d_bytes,
                                  cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {

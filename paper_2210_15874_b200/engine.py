@@ -1006,8 +1006,8 @@ class Executor:
             self.c = c
             self.done = torch.cuda.Event()
         self._graph = None
-        self.graph_io = None
-        self._staged = None   # raw parts the pinned image holds (submit)
+        self._io_graphs = {}  # raw-part pattern -> end-to-end graph + its pinned raw buffer
+        self._staged = None
         self._res_np = self.results_host.numpy()
 
     def _create_graph(self, io, prog_c=None):
@@ -1024,17 +1024,16 @@ class Executor:
                 deps.ctypes.data_as(ctypes.c_void_p), ctypes.byref(io) if io is not None else None, ctypes.byref(g)))
         return g
 
-    def kernel_mix(self, io=True):
-        """{'K1', 'K2', 'K3', 'K4', 'K5'}: graph nodes per kernel family (the
-        end-to-end graph when io, else the kernels-only graph)."""
-        g = self._io_graph() if io else self.graph
+    def kernel_mix(self, io=False):
+        """{'K1', 'K2', 'K3', 'K4', 'K5'}: graph nodes per kernel family."""
+        g = self.graph
         c = (ctypes.c_int32 * 5)()
         N.check(N.load().qtn_graph_kinds(g, c))
         return dict(zip(N.KERNEL_FAMILIES, (int(x) for x in c)))
 
-    def node_kernels(self, io=True):
-        """Per graph node, the kernel family that runs it ('K1'..'K4')."""
-        g = self._io_graph() if io else self.graph
+    def node_kernels(self, io=False):
+        """Per graph node, the kernel family that runs it ('K1'..'K5')."""
+        g = self.graph
         n = int(self.prog.n_nodes)
         c = (ctypes.c_int32 * max(n, 1))()
         N.check(N.load().qtn_graph_node_kinds(g, c, n))
@@ -1074,7 +1073,7 @@ class Executor:
         return self._graph
 
     def __del__(self):
-        for name in ("_graph", "graph_io"):
+        for name in ("_graph",):
             g = getattr(self, name, None)
             if g is not None and g.value:
                 try:
@@ -1133,47 +1132,82 @@ class Executor:
         t = self.timing.cpu().numpy()
         return t[0::2], t[1::2]
 
-    def _io_graph(self):
-        """The program graph with the input upload as its first node and the
-        result download as its last (built on first use): run() is then one
-        graph launch and one stream synchronisation."""
-        g = self.graph_io
-        if g is None:
+    def _io_graph(self, raw_parts):
+        """The end-to-end program graph for this pattern of raw input parts
+        (built on first use, cached per pattern): a first kernel node gathers
+        the raw input tensors — complex128, concatenated into a pinned,
+        device-mapped host buffer, one slot per distinct part — into the
+        canonical input image (narrowing for complex64, the unrounded copy
+        into inputs_hi); then the kernels; the finalisers write the result
+        slots straight into pinned host memory.  run() is then one host copy of
+        the raw parts, one graph launch and one stream synchronisation."""
+        torch = self.torch
+        slot_of, slots = {}, []
+        mapping = []
+        for i, part in enumerate(raw_parts):
+            k = id(part)
+            if k not in slot_of:
+                slot_of[k] = len(slots)
+                slots.append(int(part.size))
+            mapping.append(slot_of[k])
+        key = (tuple(mapping), tuple(slots))
+        hit = self._io_graphs.get(key)
+        if hit is None:
+            base = np.concatenate([[0], np.cumsum(slots)]).astype(np.int64)
+            src = np.concatenate([base[m] + p_ for m, p_ in zip(mapping, self.prog.img_src_parts)]) \
+                if len(mapping) else np.zeros(0, np.int64)
+            dst = np.ascontiguousarray(self.prog.img_dst, dtype=np.int64)
+            raw_host = torch.zeros(max(1, int(base[-1])), dtype=torch.complex128).pin_memory()
+            idx = torch.from_numpy(np.concatenate([src, dst])).to(self.device)
             # the finalisers write the result slots straight into the pinned
             # (device-mapped) host buffer: no download node after the last kernel
             c_io = N.ProgramC.from_buffer_copy(self.c)
             c_io.results = self.results_host.data_ptr()
-            self.c_io = c_io
-            io = N.GraphIOC(h2d_src=self.img_pinned.data_ptr(), h2d_dst=self.buf.data_ptr(),
-                            h2d_bytes=int(self.img_bytes), d2h_src=None, d2h_dst=None, d2h_bytes=0)
-            g = self.graph_io = self._create_graph(io, c_io)
-        return g
+            n = len(dst)
+            io = N.GraphIOC(h2d_src=None, h2d_dst=None, h2d_bytes=0, d2h_src=None, d2h_dst=None, d2h_bytes=0,
+                            gather_raw=raw_host.data_ptr(), gather_src=idx.data_ptr(),
+                            gather_dst=idx.data_ptr() + 8 * n, n_gather=n)
+            g = _OwnedGraph(self._create_graph(io, c_io))
+            hit = self._io_graphs[key] = (g, raw_host, raw_host.numpy(), base, idx, c_io, [None] * len(slots))
+        return hit
 
     def run(self, raw_parts, stream=None):
-        """Stage the inputs on the host, then one graph launch (upload,
-        kernels, download) and one synchronisation."""
+        """Copy the raw inputs into the pinned buffer, then one graph launch
+        (device gather, kernels, results into pinned host memory) and one
+        synchronisation."""
         self.submit(raw_parts, stream)
         return self.collect()
 
     def submit(self, raw_parts, stream=None):
-        """run() without the wait: stage the inputs into the pinned image,
+        """run() without the wait: copy the raw parts into the pinned buffer,
         launch the end-to-end graph and record `done`; collect() waits.  The
-        pinned image must not be restaged before collect()."""
+        buffer must not be restaged before collect()."""
         torch = self.torch
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        # the pinned image already holds these inputs when the parts are the
-        # very same read-only arrays as last time (immutable Tensors'
-        # concatenation, ordering._NetworkInputs): only the upload repeats
-        same = (self._staged is not None and len(self._staged) == len(raw_parts) and
-                all(a is b and not a.flags.writeable for a, b in zip(self._staged, raw_parts)))
-        if not same:
-            self._staged = None
-            self._gather(raw_parts)
-            self._staged = list(raw_parts)
+        g, raw_host, view, base, _, _, staged = self._io_graph(raw_parts)
+        done_slots = set()
+        for i, part in enumerate(raw_parts):
+            k = id(part)
+            if k in done_slots:
+                continue
+            done_slots.add(k)
+            sl = self._io_graphs_slot(raw_parts, i)
+            # the buffer already holds a read-only (immutable Tensors') part
+            if staged[sl] is part and not part.flags.writeable:
+                continue
+            np.copyto(view[base[sl]: base[sl] + part.size], part.reshape(-1), casting="no")
+            staged[sl] = part
         if self.timing is not None:
             self.timing.copy_(self.timing_init, non_blocking=True)
-        N.check(N.load().qtn_graph_launch(self._io_graph(), ctypes.c_void_p(s.cuda_stream)))
+        N.check(N.load().qtn_graph_launch(g.g, ctypes.c_void_p(s.cuda_stream)))
         self.done.record(s)
+
+    @staticmethod
+    def _io_graphs_slot(raw_parts, i):
+        seen = {}
+        for j, part in enumerate(raw_parts[: i + 1]):
+            seen.setdefault(id(part), len(seen))
+        return seen[id(raw_parts[i])]
 
     def collect(self):
         """Wait for the last submit() and return its per-instance values."""

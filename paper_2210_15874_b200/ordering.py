@@ -271,19 +271,19 @@ class _NetworkInputs:
 
     def __init__(self, cap=64):
         self.cap = cap
-        self.plans = OrderedDict()   # structure -> {(order, fixed, dtype, threshold): (key, Template)}
+        self.plans = OrderedDict()   # structure digest -> {(order, fixed, dtype, threshold): (key, Template)}
         self.lock = threading.Lock()
 
     def get(self, tn):
-        snap, struct, raw = tn.packed()
+        snap, struct, raw, digest = tn.packed()
         with self.lock:
-            plans = self.plans.get(struct)
+            plans = self.plans.get(digest)
             if plans is None:
-                plans = self.plans[struct] = {}
+                plans = self.plans[digest] = {}
                 while len(self.plans) > self.cap:
                     self.plans.popitem(last=False)
             else:
-                self.plans.move_to_end(struct)
+                self.plans.move_to_end(digest)
         return struct, raw, plans
 
 

@@ -14,6 +14,7 @@ Adds to the reference API:
 """
 from __future__ import annotations
 
+import hashlib
 from dataclasses import dataclass
 
 import numpy as np
@@ -37,9 +38,9 @@ class TensorNetwork:
     open_indices: tuple = ()
 
     def packed(self):
-        """(snapshot, structure, raw): the tensor list as it stands, its index
-        tuples and the raw concatenation of the (immutable) tensor data — the
-        host image the device gather reads.  Cached while `tensors` holds the
+        """(snapshot, structure, raw, digest): the tensor list as it stands, its
+        index tuples, the raw concatenation of the (immutable) tensor data —
+        the host image the device gather reads — and a digest of the structure.  Cached while `tensors` holds the
         very same Tensor objects; the network builders pack eagerly, so the
         contraction call only validates the snapshot (one identity compare)."""
         ts = self.tensors
@@ -53,7 +54,13 @@ class TensorNetwork:
         if raw.dtype != np.complex128:
             raw = raw.astype(np.complex128)
         raw.setflags(write=False)
-        pk = (snap, struct, raw)
+        # structure digest (index ids and ranks): the plan-cache key, so a new
+        # network of a known structure is recognised without hashing and
+        # comparing its index tuples
+        lens = np.fromiter((len(i) for i in struct), dtype=np.int64, count=len(struct))
+        ids = np.fromiter((x for i in struct for x in i), dtype=np.int64, count=int(lens.sum()))
+        digest = hashlib.blake2b(lens.tobytes() + b"|" + ids.tobytes(), digest_size=20).digest()
+        pk = (snap, struct, raw, digest)
         self.__dict__["_pk"] = pk
         return pk
 

@@ -39,9 +39,21 @@ def timeit(name, fn):
 
 
 timeit("contract_network (public call)", lambda: Q.contract_network(tn, order, be))
+nets = [bench.build_workload(seed=1 + k)[2].network for k in range(8)]
+cyc = [0]
+
+
+def new_angles():
+    cyc[0] += 1
+    return Q.contract_network(nets[cyc[0] % 8], order, be)
+
+
+timeit("contract_network, new angles every call", new_angles)
 timeit("Executor.run (stage + io graph + sync)", lambda: ex.run([raw]))
-gio = ex._io_graph()
-timeit("io graph launch + stream sync", lambda: (N.check(lib.qtn_graph_launch(gio, ctypes.c_void_p(s.cuda_stream))),
+raws = [n_.packed()[2] for n_ in nets]
+timeit("Executor.run, new inputs every call", lambda: ex.run([raws[(cyc.__setitem__(0, cyc[0] + 1) or cyc[0]) % 8]]))
+gio = ex._io_graph([raw])[0].g
+timeit("io graph (device gather) launch + stream sync", lambda: (N.check(lib.qtn_graph_launch(gio, ctypes.c_void_p(s.cuda_stream))),
                                                  s.synchronize()))
 gk = ex.graph
 timeit("kernel graph launch + stream sync", lambda: (N.check(lib.qtn_graph_launch(gk, ctypes.c_void_p(s.cuda_stream))),
