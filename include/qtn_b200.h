@@ -336,7 +336,7 @@ int qtn_bucket_plan(const qtn_bucket_desc_t* desc, int32_t* info);
 
 /* ---- K4: an expansion bucket (one dominant member) ----
  * Same contraction as qtn_bucket for a descriptor whose dominant member (the
- * one with the most result bits) lacks between min_e (>= 0) and 4 result bits
+ * one with the most result bits) lacks between min_e (>= 0) and 8 result bits
  * ("expansion bits"), k in 1..3, 8 <= w <= 31, the other members' bits inside
  * the K4 tile <= 12 (c64) / 11 (c128) with the summed bits.  The dominant
  * member is read once into registers, the others through a per-tile product

@@ -62,7 +62,8 @@ namespace qtn_k4 {
 
 constexpr int NT = 256;
 constexpr int TBB = 8;                  // thread bits (log2 NT)
-constexpr int MAXE = 4;                 // expansion bits
+constexpr int MAXE = 8;                 // expansion bits (the low 4 unrolled per thread, the rest rolled)
+constexpr int K4_WIDE_E_MIN_W = 20;     // more than 4 expansion bits: widths from here
 constexpr int MAXKS = 3;                // summed bits
 constexpr int MAXFB = 12;               // F table bits (|F| + k)
 constexpr int MAXM = QTN_MAX_MEMBERS;
@@ -130,7 +131,6 @@ __device__ __forceinline__ void k4_body(const Plan& P) {
   using T = typename Cx<R>::T;
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   constexpr int NS = 1 << K;
-  constexpr int NEV = 1 << NE;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* F = reinterpret_cast<T*>(smem_raw);
   const int nfe = 1 << (P.nF + K);                  // F entries
@@ -160,12 +160,17 @@ __device__ __forceinline__ void k4_body(const Plan& P) {
       ob += P.otb[b];
       fb += P.ftb[b];
     }
-  int32_t oe[NEV], fe[NEV];
+  // expansion bits: the low NEL unrolled (offset tables in registers), the
+  // high NEH walked by a rolled loop
+  constexpr int NEL = NE < 4 ? NE : 4;
+  constexpr int NEH = NE - NEL;
+  constexpr int NEVL = 1 << NEL;
+  int32_t oe[NEVL], fe[NEVL];
 #pragma unroll
-  for (int e = 0; e < NEV; ++e) {
+  for (int e = 0; e < NEVL; ++e) {
     int32_t o = 0, f = 0;
 #pragma unroll
-    for (int b = 0; b < NE; ++b)
+    for (int b = 0; b < NEL; ++b)
       if ((e >> b) & 1) {
         o += P.oe[b];
         f += P.fe[b];
@@ -239,23 +244,42 @@ __device__ __forceinline__ void k4_body(const Plan& P) {
       }
       __syncthreads();
     }
-    T* op = out + obase + ob;
+    // the results of this tile: 2^NE per thread, the low NEL expansion bits
+    // unrolled, the high NEH walked by a rolled loop (NE > 4 only)
+    auto emit = [&](int32_t oh, int32_t fh) {
+      T* op = out + obase + ob + oh;
 #pragma unroll
-    for (int e = 0; e < NEV; ++e) {
-      K4_CHECK(fe[e] + NS <= nfe, "F entry %d of %d", fe[e] + NS, nfe);
-      const T* fp = F + fe[e];
-      T fr[NS];
+      for (int e = 0; e < NEVL; ++e) {
+        K4_CHECK(fe[e] + fh + NS <= nfe, "F entry %d of %d", fe[e] + fh + NS, nfe);
+        const T* fp = F + fe[e] + fh;
+        T fr[NS];
 #pragma unroll
-      for (int s = 0; s < NS; ++s) fr[s] = fp[s];
+        for (int s = 0; s < NS; ++s) fr[s] = fp[s];
 #pragma unroll
-      for (int r = 0; r < RB; ++r) {
-        T acc = cmul(bv[r][0], fr[0]);
+        for (int r = 0; r < RB; ++r) {
+          T acc = cmul(bv[r][0], fr[0]);
 #pragma unroll
-        for (int s = 1; s < NS; ++s) cfma(acc, bv[r][s], fr[s]);
-        const int64_t o = oe[e] + (r ? P.rbo : 0);
-        K4_CHECK(obase + ob + o >= 0 && obase + ob + o < P.out_elems, "result %lld of %lld",
-                 (long long)(obase + ob + o), (long long)P.out_elems);
-        op[o] = acc;
+          for (int s = 1; s < NS; ++s) cfma(acc, bv[r][s], fr[s]);
+          const int64_t o = oe[e] + (r ? P.rbo : 0);
+          K4_CHECK(obase + ob + oh + o >= 0 && obase + ob + oh + o < P.out_elems, "result %lld of %lld",
+                   (long long)(obase + ob + oh + o), (long long)P.out_elems);
+          op[o] = acc;
+        }
+      }
+    };
+    if constexpr (NEH == 0) {
+      emit(0, 0);
+    } else {
+#pragma unroll 1
+      for (int eh = 0; eh < (1 << NEH); ++eh) {
+        int32_t oh = 0, fh = 0;
+#pragma unroll
+        for (int b = 0; b < NEH; ++b)
+          if ((eh >> b) & 1) {
+            oh += P.oe[NEL + b];
+            fh += P.fe[NEL + b] << K;
+          }
+        emit(oh, fh);
       }
     }
   }
@@ -282,7 +306,11 @@ const void* fn_ne(int ne) {
     case 1: return fn_k<R, K, 1, RB>();
     case 2: return fn_k<R, K, 2, RB>();
     case 3: return fn_k<R, K, 3, RB>();
-    default: return fn_k<R, K, 4, RB>();
+    case 4: return fn_k<R, K, 4, RB>();
+    case 5: return fn_k<R, K, 5, RB>();
+    case 6: return fn_k<R, K, 6, RB>();
+    case 7: return fn_k<R, K, 7, RB>();
+    default: return fn_k<R, K, 8, RB>();
   }
 }
 
@@ -342,6 +370,11 @@ int make_plan(const qtn_bucket_desc_t* d, int min_e, Plan* P, int* smem) {
       eb[ne++] = b;
     }
   if (w - ne < TBB) return fail(QTN_E_UNSUPPORTED, "K4: dominant member has %d result bits", best);
+  // more than 4 expansion bits (two mid-size members, an outer-product-like
+  // expansion): only for wide items — the 45-cone energy's w 22-26 items run
+  // 3-5x faster here than in K1, a w = 16 item ran slower (cfg-2: 4 -> 10 us)
+  if (ne > 4 && w < K4_WIDE_E_MIN_W)
+    return fail(QTN_E_UNSUPPORTED, "K4: %d expansion bits at width %d", ne, w);
   // Thread bits.  Lanes (the first 5): B's fastest axes first — one 32-byte
   // sector of B per lane group (2 complex128 / 4 complex64 elements) — then
   // B bits NO other member carries, so every lane of a warp reads the same

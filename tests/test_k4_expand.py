@@ -70,7 +70,8 @@ def _run(w, k, mems, dtype, seed):
 @pytest.mark.gpu
 @pytest.mark.parametrize("dtype", ["complex64", "complex128"])
 @pytest.mark.parametrize("w,k,ne,n_small", [(12, 1, 1, 1), (13, 2, 2, 2), (16, 2, 4, 3), (18, 3, 3, 2), (16, 1, 4, 4),
-                                            (20, 2, 1, 3), (14, 3, 2, 5), (22, 2, 4, 2)])
+                                            (20, 2, 1, 3), (14, 3, 2, 5), (22, 2, 4, 2), (20, 1, 5, 2), (20, 2, 6, 3),
+                                            (21, 1, 7, 2), (22, 1, 8, 2)])
 def test_k4_vs_einsum(dtype, w, k, ne, n_small):
     mems = _case(w, k, ne, n_small, seed=w * 100 + k * 10 + ne)
     out, ref = _run(w, k, mems, dtype, seed=w + k + ne)
@@ -97,12 +98,15 @@ def test_k4_rejects_non_expansions():
     x = torch.zeros(1 << 17, dtype=torch.complex64, device="cuda")
     out = torch.zeros(1 << 16, dtype=torch.complex64, device="cuda")
     s = torch.cuda.current_stream().cuda_stream
-    # dominant member lacks 5 result bits
-    big = {b: 1 << i for i, b in enumerate([0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10] + [16])}
-    small = {b: 1 << i for i, b in enumerate([11, 12, 13, 14, 15, 16])}
-    d = N.bucket_desc(N.QTN_C64, 16, out.data_ptr(), [(x.data_ptr(), big), (x.data_ptr(), small)], k=1)
+    # dominant member lacks 9 result bits (K4 takes at most 8)
+    x = torch.zeros(1 << 20, dtype=torch.complex64, device="cuda")
+    out = torch.zeros(1 << 18, dtype=torch.complex64, device="cuda")
+    big = {b: 1 << i for i, b in enumerate([0, 1, 2, 3, 4, 5, 6, 7, 8] + [18])}
+    small = {b: 1 << i for i, b in enumerate([9, 10, 11, 12, 13, 14, 15, 16, 17, 18])}
+    d = N.bucket_desc(N.QTN_C64, 18, out.data_ptr(), [(x.data_ptr(), big), (x.data_ptr(), small)], k=1)
     with pytest.raises(N.NativeError, match="expansion bits"):
         N.bucket_expand_launch(d, s)
+    out = torch.zeros(1 << 16, dtype=torch.complex64, device="cuda")
     # no expansion bit but min_e = 1
     full = {b: 1 << b for b in range(17)}
     d = N.bucket_desc(N.QTN_C64, 16, out.data_ptr(), [(x.data_ptr(), full)], k=1)
