@@ -61,6 +61,8 @@ def parse(argv=None):
     ap.add_argument("--cpu-sample", type=int, default=2, help="oracle contractions for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-strong", action="store_true", help="skip the full-graph strong-scaling figure")
+    ap.add_argument("--no-shares", action="store_true",
+                    help="skip the per-rank share timings (predicted strong scaling on one GPU)")
     ap.add_argument("--ref-budget-s", type=float, default=150.0)
     ap.add_argument("--sustain-s", type=float, default=1.0, help="clock-sampled sustained loop after the timed region")
     ap.add_argument("--simplify", action="store_true",
@@ -615,11 +617,50 @@ def graph_figure(args, rank, world, local, dtype, stream, flush):
     for u, unit in enumerate(plan.units):
         zz[unit.cone] += complex(v[2 * u], v[2 * u + 1])
     energy = sum(0.5 * (1 - z.real) for z in zz)
+    shares = None
+    if world == 1 and not args.no_shares:
+        shares = rank_shares(plan, be, local, stream, flush)
     return {"metric": "lightcones/s (N=30,p=4 full-graph energy, 45 tight lightcones)",
             "value": len(cones) * steps / t, "ms_per_energy": 1e3 * t / steps, "n_gpus": world, "dtype": dtype,
+            "rank_shares": shares,
             "scaling": "strong", "units": n_units, "energy": energy, "steps": steps,
             "lpt_makespan_share": round(_lpt_share([u.cost for u in plan.units], world), 4),
             "host_plan_s": round(t_plan, 3)}
+
+
+def rank_shares(plan, be, local, stream, flush, ns=(2, 4, 8), reps=5):
+    """Predicted strong scaling from this one GPU: for N ranks, each rank's
+    LPT share of the units is built as its own program and timed ALONE
+    (CUDA events, L2 flushed); the N-rank makespan is the slowest share (the
+    ranks never wait on one another until the final all-reduce of a few KB).
+    A prediction, not a multi-GPU measurement."""
+    import torch
+    from paper_2210_15874_b200 import distributed as D
+    costs = [u.cost for u in plan.units]
+    out = {}
+    for n in ns:
+        owner = D.lpt_assign(costs, n)
+        worst = 0.0
+        for r in range(n):
+            mine = [u for u in range(len(plan.units)) if owner[u] == r]
+            if not mine:
+                continue
+            prep = D.prepare_local(plan, mine, be, local)
+            for _ in range(2):
+                D.launch_prepared(prep, stream)
+            ts = []
+            for _ in range(reps):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                D.launch_prepared(prep, stream)
+                b.record(stream)
+                ts.append((a, b))
+            torch.cuda.synchronize()
+            worst = max(worst, sum(a.elapsed_time(b) for a, b in ts) / reps)
+            del prep
+        out[str(n)] = {"makespan_ms": round(worst, 4)}
+    return out
 
 
 def run_graph(args):

@@ -30,6 +30,17 @@ from .tensor_core import Backend, memory_estimate
 
 
 PLAN_THREADS = max(1, min(16, os.cpu_count() or 1))
+# LPT cost of a (cone, slice) unit: the bytes its device items must move
+# (members once + results once; merged chains write no intermediates) plus a
+# fixed charge for its latency-bound chains (~80 us at HBM rate).  Round 1
+# used SURVEY 8(d) algorithmic bytes, which overweight merged items.
+# Measured on the 45-cone N=30 p=4 energy (c64, bench rank_shares): 1 GPU
+# 6.94 -> 6.82 ms, predicted 8-rank makespan 1.32 -> 1.25 ms.
+UNIT_LATENCY_BYTES = 500_000_000
+
+
+def unit_cost(tmpl, dtype):
+    return E.executed_bytes(tmpl, dtype) + UNIT_LATENCY_BYTES
 
 
 @dataclass
@@ -91,7 +102,7 @@ def plan_units(cones, backend: Backend, heuristic="minfill", mem_cap=4 << 30, sl
     for ci, (tmpl, sliced, raw) in enumerate(res):
         templates.append(tmpl)
         raws.append(raw)
-        cost = E.algorithmic_bytes(tmpl, backend.dtype)
+        cost = unit_cost(tmpl, backend.dtype)
         for bits in np.ndindex(*(2,) * len(sliced)):
             units.append(Unit(ci, dict(zip(sliced, (int(b) for b in bits))), cost))
     return UnitPlan(list(cones), templates, raws, units)
@@ -107,7 +118,7 @@ def _balance(cones, res, backend, heuristic, mem_cap, n_ranks, factor, max_round
     stuck = set()
     sib = E.small_iter_bits_for(backend.threshold, backend.dtype)
     for _ in range(max_rounds):
-        per = [E.algorithmic_bytes(t, backend.dtype) for t, _, _ in res]
+        per = [unit_cost(t, backend.dtype) for t, _, _ in res]
         total = sum(c << len(s_) for c, (_, s_, _) in zip(per, res))
         target = total / (n_ranks * factor)
         cand = [i for i in range(len(res)) if i not in stuck and per[i] > target]
