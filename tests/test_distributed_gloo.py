@@ -98,8 +98,10 @@ def test_lpt_assignment_balanced_and_deterministic():
 
 def test_balance_slicing_spreads_the_heaviest_cone():
     """plan_units(balance_ranks=8) on N=30 p=4 tight cones: no unit above
-    total / 16 (the widest cone holds ~30 % of the work unsliced), LPT
-    makespan at 8 ranks within 15 % of ideal, total work inflated < 3 %."""
+    total / 16 (the widest cone holds ~16 % of the unit cost unsliced:
+    executed bytes + a per-unit latency charge, distributed.unit_cost), LPT
+    makespan at 8 ranks within 15 % of ideal, total cost inflated < 25 %
+    (the extra slices' latency charges)."""
     import paper_2210_15874_b200 as Q
     from paper_2210_15874_b200 import distributed as D
     g = Q.random_regular_graph(30, 3, seed=0)
@@ -110,9 +112,9 @@ def test_balance_slicing_spreads_the_heaviest_cone():
     p8 = D.plan_units(cones, be, mem_cap=1 << 40, balance_ranks=8)
     c0 = [u.cost for u in p0.units]
     c8 = [u.cost for u in p8.units]
-    assert max(c0) > 0.25 * sum(c0)
+    assert max(c0) > 0.12 * sum(c0)
     assert max(c8) <= sum(c8) / 16
-    assert sum(c8) < 1.03 * sum(c0)
+    assert sum(c8) < 1.25 * sum(c0)
     own = D.lpt_assign(c8, 8)
     load = [sum(c for c, o in zip(c8, own) if o == r) for r in range(8)]
     assert max(load) <= 1.15 * sum(c8) / 8
