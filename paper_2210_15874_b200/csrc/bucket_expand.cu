@@ -107,6 +107,9 @@ __device__ __forceinline__ void cfma(T& acc, T a, T b) {
 // complex64 variants are compiled for >= 4 resident blocks (<= 64 registers:
 // cfg-2 0.2395 -> 0.2346 ms, the default heuristic picked 32 registers with
 // spills); complex128 keeps the default (4 blocks measured 1.3 % slower)
+#ifndef K4_PF
+#define K4_PF 0
+#endif
 #ifndef K4_C64_MINB
 #define K4_C64_MINB 4
 #endif
@@ -200,16 +203,18 @@ __device__ __forceinline__ void k4_body(const Plan& P) {
   T* out = reinterpret_cast<T*>(P.out);
   const int shf = P.nH - P.nHF;
   int64_t fkey = -1;
-  for (; h < h_end; ++h) {
-    // B and output bases of this tile (every thread: no barrier)
-    int64_t bb = 0, obase = 0;
+  // B and output bases of tile h (every thread: no barrier)
+  auto bases = [&](int64_t hh, int64_t& bb, int64_t& obase) {
+    bb = 0;
+    obase = 0;
     for (int b = 0; b < P.nH; ++b)
-      if ((h >> b) & 1) {
+      if ((hh >> b) & 1) {
         bb += P.hs[P.iB][b];
         obase += P.hs[nm][b];
       }
-    // B for all s (registers), issued before a possible F rebuild
-    T bv[RB][NS];
+  };
+  // B for all s (registers)
+  auto loadB = [&](int64_t bb, T (&bv)[RB][NS]) {
     const T* bp = Bm + bb + boff;
 #pragma unroll
     for (int r = 0; r < RB; ++r)
@@ -219,6 +224,26 @@ __device__ __forceinline__ void k4_body(const Plan& P) {
         K4_CHECK(o >= 0 && o < P.span[P.iB], "B element %lld of %lld", (long long)o, (long long)P.span[P.iB]);
         bv[r][s] = __ldg(bp + soffB[s] + (r ? P.rbs : 0));
       }
+  };
+  int64_t bb, obase;
+  T bv[RB][NS];
+  bases(h, bb, obase);
+  loadB(bb, bv);
+  for (; h < h_end; ++h) {
+#if K4_PF
+    // the next tile's B is in flight while this tile's results are written
+    int64_t bbn = 0, obn = 0;
+    T bn[RB][NS];
+    if (h + 1 < h_end) {
+      bases(h + 1, bbn, obn);
+      loadB(bbn, bn);
+    }
+#else
+    if (h != blockIdx.x * per) {
+      bases(h, bb, obase);
+      loadB(bb, bv);
+    }
+#endif
     if ((h >> shf) != fkey) {
       fkey = h >> shf;
       __syncthreads();   // previous F no longer read
@@ -282,6 +307,13 @@ __device__ __forceinline__ void k4_body(const Plan& P) {
         emit(oh, fh);
       }
     }
+#if K4_PF
+    obase = obn;
+#pragma unroll
+    for (int r = 0; r < RB; ++r)
+#pragma unroll
+      for (int s = 0; s < NS; ++s) bv[r][s] = bn[r][s];
+#endif
   }
   if (P.timing && tid == 0) {
     unsigned long long t_end;
