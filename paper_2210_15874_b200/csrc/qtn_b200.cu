@@ -267,7 +267,12 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
   int pend_item = 0;
 
   pdl_launch_dependents();
-  pdl_wait();   // predecessor nodes' outputs (and this stage's ctrl reset) visible
+  // The stage's counters were zeroed by its previous run's last block (or by
+  // qtn_program_reset), both stream-ordered before this graph launch, and the
+  // program records are uploaded before it: the first ticket, its search and
+  // the item's records are fetched BEFORE waiting for the predecessor nodes
+  // (griddepcontrol.wait below, ahead of the first read of data a node writes)
+  bool waited = false;
   if (tid == 0) S.next = (int)atomicAdd(&ctl[0], 1u);
   for (;;) {
     __syncthreads();
@@ -327,6 +332,10 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
         for (int q = 0; q < (1 << k); ++q) S.sig[tid][q] = (int16_t)pext32((uint32_t)q, m.smask);
         const int lg = __popcll(m.mask) + __popc(m.smask);
         S.hmode[tid] = (HI && m.off < n_hi && lg <= 6) ? 1 : 0;
+      }
+      if (!waited) {
+        pdl_wait();   // predecessor nodes' outputs visible
+        waited = true;
       }
       if (HI && n_hi) {
         // stage the item's (small) input members unrounded
