@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define QTN_ABI_VERSION 9
+#define QTN_ABI_VERSION 10
 
 enum {
   QTN_OK = 0,
@@ -144,7 +144,13 @@ typedef struct {
  *    the batched small-bucket schedule (K2): dependencies inside the stage
  *    are per-item completion counters, tickets are stage-relative.
  *  QTN_NODE_LARGE: one item, one launch of the large-item kernel (K1)
- *    specialised by `variant`. */
+ *    specialised by `variant` (or K3 / K4 / K5 when the item has their
+ *    shape) — or, count == 2, a producer / consumer PAIR: item `first`'s
+ *    result is read by item first + 1 only, as a member carrying every
+ *    result and summed index of the consumer.  The pair runs as ONE K6
+ *    kernel (csrc/bucket_expand.cu: the producer's result never reaches
+ *    HBM) when it has K6's shape, else as two kernels in sequence;
+ *    n_tickets then holds the producer's K1 variant. */
 enum { QTN_NODE_SMALL = 0, QTN_NODE_LARGE = 1 };
 #define QTN_VARIANT_GENERIC (-1)
 /* variant = log2(2^k) | (varying staged members) << 4 | (one streamed member) << 8
@@ -217,11 +223,13 @@ int qtn_graph_create_host(const qtn_program_t* prog, const qtn_bucket_t* host_it
 /* Launch the instantiated graph (one call per program execution). */
 int qtn_graph_launch(qtn_graph_t* g, void* stream);
 int qtn_graph_destroy(qtn_graph_t* g);
-/* Kernel mix of a built graph: counts[5] = nodes run by K1 (fused large-item
+/* Kernel mix of a built graph: counts[6] = kernels of K1 (fused large-item
  * kernels), K2 (small-item stages), K3 (permutation-aware bucket kernel), K4
- * (expansion-item kernel) and K5 (streaming-item kernel). */
+ * (expansion-item kernel), K5 (streaming-item kernel) and K6 (expansion item
+ * fused with its consumer). */
 int qtn_graph_kinds(const qtn_graph_t* g, int32_t* counts);
-/* Per node (n = the graph's node count): 0 K1, 1 K2, 2 K3, 3 K4, 4 K5. */
+/* Per node (n = the graph's node count): 0 K1, 1 K2, 2 K3, 3 K4, 4 K5, 5 K6
+ * (a pair node that fell back to two kernels reports its consumer's). */
 int qtn_graph_node_kinds(const qtn_graph_t* g, int32_t* kinds, int32_t n);
 /* Host planning (no device needed): the greedy min-fill (heuristic 0) or
  * min-degree (1) elimination order of a network given as CSR index lists
@@ -351,6 +359,19 @@ int qtn_bucket_expand(const qtn_bucket_desc_t* desc, int32_t min_e, void* stream
  * directly through L1/L2 (csrc/bucket_stream.cu).  Program graphs route
  * their streaming items here (QTN_K5).  QTN_E_UNSUPPORTED otherwise. */
 int qtn_bucket_stream(const qtn_bucket_desc_t* desc, void* stream);
+
+/* ---- K6: an expansion bucket fused with its only consumer ----
+ * `producer` is a K4-shaped bucket (qtn_bucket_expand) whose result is member
+ * `member` of `consumer`, carrying every result and summed index of the
+ * consumer in order (consumer->mem[member].data == producer->out, strides
+ * 1, 2, 4, ... over the consumer's w + k iteration bits; producer->w ==
+ * consumer->w + consumer->k, consumer k in 1..3).  Computes the consumer's
+ * result without materialising the producer's: producer->out is NOT written
+ * (it may be any non-null pointer).  Same sum order as the two buckets run
+ * one after the other; the intermediate is not rounded to the element type.
+ * QTN_E_UNSUPPORTED when the pair does not have that shape. */
+int qtn_bucket_expand_fused(const qtn_bucket_desc_t* producer, const qtn_bucket_desc_t* consumer,
+                            int32_t member, void* stream);
 
 #ifdef __cplusplus
 }

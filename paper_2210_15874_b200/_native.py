@@ -26,12 +26,12 @@ QTN_FINALIZE = -1
 MAX_MEMBERS = 8
 MAX_WIDTH = 40
 MAX_SUMMED = 6
-ABI_VERSION = 9
+ABI_VERSION = 10
 QTN_NODE_SMALL = 0
 QTN_NODE_LARGE = 1
 QTN_VARIANT_GENERIC = -1
 # graph node kernel families (qtn_graph_node_kinds codes 0..4)
-KERNEL_FAMILIES = ("K1", "K2", "K3", "K4", "K5")
+KERNEL_FAMILIES = ("K1", "K2", "K3", "K4", "K5", "K6")
 
 # every symbol include/qtn_b200.h declares
 EXPORTS = (
@@ -46,6 +46,7 @@ EXPORTS = (
     "qtn_graph_kinds",
     "qtn_bucket_expand",
     "qtn_bucket_stream",
+    "qtn_bucket_expand_fused",
     "qtn_route_config",
     "qtn_graph_node_kinds",
     "qtn_graph_launch",
@@ -159,6 +160,8 @@ def load(path: str = LIB_PATH):
     lib.qtn_graph_node_kinds.argtypes = [vp, vp, i32]
     lib.qtn_bucket_expand.restype = ctypes.c_int
     lib.qtn_bucket_expand.argtypes = [ctypes.POINTER(BucketDescC), i32, vp]
+    lib.qtn_bucket_expand_fused.restype = ctypes.c_int
+    lib.qtn_bucket_expand_fused.argtypes = [ctypes.POINTER(BucketDescC), ctypes.POINTER(BucketDescC), i32, vp]
     lib.qtn_bucket_stream.restype = ctypes.c_int
     lib.qtn_bucket_stream.argtypes = [ctypes.POINTER(BucketDescC), vp]
     lib.qtn_route_config.restype = ctypes.c_char_p
@@ -317,6 +320,15 @@ def bucket_expand_launch(desc, stream, min_e=0):
     descriptor is not an expansion of one dominant member)."""
     lib = require_device()
     check(lib.qtn_bucket_expand(ctypes.byref(desc), int(min_e), ctypes.c_void_p(stream)))
+
+
+def bucket_expand_fused_launch(producer, consumer, member, stream):
+    """K6 on a producer bucket fused with the consumer that reads its whole
+    result as member `member` (QTN_E_UNSUPPORTED -> NativeError when the pair
+    does not have K6's shape); the producer's output is not written."""
+    lib = require_device()
+    check(lib.qtn_bucket_expand_fused(ctypes.byref(producer), ctypes.byref(consumer), int(member),
+                                      ctypes.c_void_p(stream)))
 
 
 def bucket_stream_launch(desc, stream):

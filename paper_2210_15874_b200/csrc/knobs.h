@@ -22,6 +22,7 @@ struct QtnKnobs {
   int k3_v1;        // QTN_K3_V1     1: K3 first-generation kernel
   int k3_ulim;      // QTN_K3_ULIM   K3 folded-table bits limit
   int k3_inv2;      // QTN_K3_INV2   0: no second invariant operand in K3
+  int k6_min_w;     // QTN_K6        narrowest producer fused with its consumer by K6 (0 = K6 off)
 };
 
 const QtnKnobs& qtn_knobs();

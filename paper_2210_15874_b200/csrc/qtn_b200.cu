@@ -1106,6 +1106,9 @@ int qtn_k4_node(const qtn_bucket_desc_t* d, int min_e, unsigned long long* timin
                 const void** fn, int* grid, int* smem);
 int qtn_k3_node(const qtn_bucket_desc_t* d, unsigned long long* timing, int32_t item, void* plan, const void** fn,
                 int* grid, int* smem);
+size_t qtn_k6_plan_bytes();
+int qtn_k6_node(const qtn_bucket_desc_t* dp, const qtn_bucket_desc_t* dc, int ipc, unsigned long long* timing,
+                int32_t item_p, int32_t item_c, void* plan, const void** fn, int* grid, int* smem);
 
 namespace {
 
@@ -1136,6 +1139,7 @@ QtnKnobs read_knobs() {
   k.k3_v1 = knob("QTN_K3_V1", 0, 0, 1);
   k.k3_ulim = knob("QTN_K3_ULIM", 5, 0, 8);
   k.k3_inv2 = knob("QTN_K3_INV2", 1, 0, 1);
+  k.k6_min_w = knob("QTN_K6", 18, 0, 40);
   return k;
 }
 
@@ -1189,8 +1193,8 @@ const QtnKnobs& qtn_knobs() {
 struct qtn_graph {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
-  int32_t kinds[5] = {0, 0, 0, 0, 0};   // nodes run by K1, K2, K3, K4, K5
-  std::vector<int32_t> node_kind;       // per node: 0 K1, 1 K2, 2 K3, 3 K4, 4 K5
+  int32_t kinds[6] = {0, 0, 0, 0, 0, 0};   // kernels K1, K2, K3, K4, K5, K6 in the graph
+  std::vector<int32_t> node_kind;          // per node: 0 K1, 1 K2, 2 K3, 3 K4, 4 K5, 5 K6
 };
 
 extern "C" {
@@ -1203,9 +1207,9 @@ const char* qtn_route_config(void) {
     char buf[512];
     snprintf(buf, sizeof(buf),
              "k3_route=%d k4_min_e=%d k4_all=%d k5=%d pdl=%d k3_tcap=%d k3_stage_kb=%d k3_run=%d k3_v1=%d k3_ulim=%d "
-             "k3_inv2=%d",
+             "k3_inv2=%d k6_min_w=%d",
              k.k3_route, k.k4_min_e, k.k4_all, k.k5, k.pdl, k.k3_tcap, k.k3_stage_kb, k.k3_run, k.k3_v1, k.k3_ulim,
-             k.k3_inv2);
+             k.k3_inv2, k.k6_min_w);
     return std::string(buf);
   }();
   return txt.c_str();
@@ -1237,8 +1241,27 @@ int qtn_node_launch(const qtn_program_t* p, const qtn_node_t* nd, int32_t ni, vo
   int rc = check_program(p);
   if (rc) return rc;
   if (!nd) return set_err(QTN_E_INVALID, "null node");
+  if (nd->kind == QTN_NODE_LARGE && nd->count == 2) {
+    // producer / consumer pair: the two items in order (K1 each)
+    qtn_node_t sub[2] = {*nd, *nd};
+    sub[0].count = sub[1].count = 1;
+    sub[1].first = nd->first + 1;
+    sub[0].variant = nd->n_tickets;
+    sub[0].n_tickets = sub[1].n_tickets = 0;
+    qtn_bucket_t bp;
+    if (nd->first < 0 || nd->first + 1 >= p->n_buckets) return set_err(QTN_E_INVALID, "item %d out of range", nd->first);
+    const cudaError_t e = cudaMemcpy(&bp, p->buckets + nd->first, sizeof(bp), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_err(e, "cudaMemcpy(item)");
+    sub[0].smem_bytes = (int32_t)((bp.smem_elems * (p->dtype == QTN_C64 ? 8 : 16) + 15) / 16 * 16);
+    for (int j = 0; j < 2; ++j) {
+      rc = qtn_node_launch(p, &sub[j], ni, stream);
+      if (rc) return rc;
+    }
+    return QTN_OK;
+  }
   K1Item itm{};
   if (nd->kind == QTN_NODE_LARGE) {
+    if (nd->count != 1) return set_err(QTN_E_INVALID, "large node with %d items", nd->count);
     if (nd->first < 0 || nd->first >= p->n_buckets) return set_err(QTN_E_INVALID, "item %d out of range", nd->first);
     cudaError_t e = cudaMemcpy(&itm.b, p->buckets + nd->first, sizeof(itm.b), cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cuda_err(e, "cudaMemcpy(item)");
@@ -1344,91 +1367,92 @@ int qtn_graph_create_host(const qtn_program_t* p, const qtn_bucket_t* items, con
   }
   const QtnKnobs& route = qtn_knobs();
   const bool use_pdl = route.pdl != 0;
-  for (int i = 0; i < n_nodes; ++i) {
-    const qtn_node_t& nd = nodes[i];
-    if (nd.kind == QTN_NODE_LARGE && (nd.first < 0 || nd.first >= p->n_buckets)) {
-      qtn_graph_destroy(g);
-      return set_err(QTN_E_INVALID, "node %d: item %d out of range", i, nd.first);
-    }
+  const size_t esz = p->dtype == QTN_C64 ? 8 : 16;
+  // Launch of one item-level node `sub` (a SMALL stage, or ONE large item):
+  // K2 / K1 from make_launch, then the K5 / K4 / K3 routes for large items.
+  // fam: 0 K1, 1 K2, 2 K3, 3 K4, 4 K5.
+  auto route_node = [&](const qtn_node_t& sub, int ni, LaunchSpec& spec, int& fam) -> int {
     K1Item itm{};
-    if (nd.kind == QTN_NODE_LARGE) {
-      itm.b = items[nd.first];
-      if (itm.b.n_mem < 0 || itm.b.n_mem > MAXM) {
-        qtn_graph_destroy(g);
-        return set_err(QTN_E_INVALID, "node %d: item with %d members", i, itm.b.n_mem);
-      }
+    if (sub.kind == QTN_NODE_LARGE) {
+      itm.b = items[sub.first];
+      if (itm.b.n_mem < 0 || itm.b.n_mem > MAXM) return set_err(QTN_E_INVALID, "node %d: item with %d members", ni, itm.b.n_mem);
       for (int j = 0; j < itm.b.n_mem; ++j) itm.mem[j] = mems_ptr[itm.b.mem_begin + j];
     }
-    rc = make_launch(p, &nd, i, nd.kind == QTN_NODE_LARGE ? &itm : nullptr, &specs[i]);
-    if (rc) {
-      qtn_graph_destroy(g);
-      return rc;
-    }
-    ++g->kinds[nd.kind == QTN_NODE_LARGE ? 0 : 1];
-    g->node_kind.push_back(nd.kind == QTN_NODE_LARGE ? 0 : 1);
+    int rc2 = make_launch(p, &sub, ni, sub.kind == QTN_NODE_LARGE ? &itm : nullptr, &spec);
+    if (rc2) return rc2;
+    fam = sub.kind == QTN_NODE_LARGE ? 0 : 1;
+    if (sub.kind != QTN_NODE_LARGE || !p->arena || !have_mems) return QTN_OK;
+    const qtn_bucket_t& it = items[sub.first];
+    auto take = [&](std::vector<unsigned char>&& plan, const void* fn, int grid, int smem, int f) {
+      spec.k3plan = std::move(plan);
+      spec.fn = fn;
+      spec.grid = grid;
+      spec.smem = smem;
+      spec.args[0] = spec.k3plan.data();
+      fam = f;
+    };
+    qtn_bucket_desc_t d;
+    k3_desc(p, it, mems_ptr, &d);
+    const void* fn = nullptr;
+    int grid = 0, smem = 0;
     // K5: streaming items (one member carries every result bit)
-    bool k5 = false;
-    if (nd.kind == QTN_NODE_LARGE && p->arena && have_mems && route.k5 && items[nd.first].k >= 1) {
-      qtn_bucket_desc_t d;
-      k3_desc(p, items[nd.first], mems_ptr, &d);
+    if (route.k5 && it.k >= 1) {
       std::vector<unsigned char> plan(qtn_k5_plan_bytes());
-      const void* fn = nullptr;
-      int grid = 0, smem = 0;
-      if (qtn_k5_node(&d, route.k5 >= 2 ? 4 : 0, p->timing, nd.first, plan.data(), &fn, &grid, &smem) == QTN_OK) {
-        specs[i].k3plan = std::move(plan);
-        specs[i].fn = fn;
-        specs[i].grid = grid;
-        specs[i].smem = smem;
-        specs[i].args[0] = specs[i].k3plan.data();
-        k5 = true;
-        ++g->kinds[4];
-        --g->kinds[0];
-        g->node_kind.back() = 4;
+      if (qtn_k5_node(&d, route.k5 >= 2 ? 4 : 0, p->timing, sub.first, plan.data(), &fn, &grid, &smem) == QTN_OK) {
+        take(std::move(plan), fn, grid, smem, 4);
+        return QTN_OK;
       }
     }
     // K4: expansion items of one dominant member (QTN_K4 = fewest expansion
-    // bits routed, 0 = never)
-    const int k4_min_e = route.k4_min_e;
-    bool k4 = false;
-    if (!k5 && nd.kind == QTN_NODE_LARGE && p->arena && have_mems && k4_min_e > 0 && items[nd.first].k >= 1 &&
-        items[nd.first].w >= 12) {
-      qtn_bucket_desc_t d;
-      k3_desc(p, items[nd.first], mems_ptr, &d);
+    // bits routed, 0 = never); non-expansion items too: complex128 by default
+    // (cfg-2 0.3575 -> 0.3519 ms), not complex64 (its streaming items stay
+    // faster in K1); QTN_K4_ALL overrides
+    if (route.k4_min_e > 0 && it.k >= 1 && it.w >= 12) {
       std::vector<unsigned char> plan(qtn_k4_plan_bytes());
-      const void* fn = nullptr;
-      int grid = 0, smem = 0;
-      // non-expansion items too: complex128 by default (cfg-2 0.3575 -> 0.3519 ms),
-      // not complex64 (its streaming items stay faster in K1); QTN_K4_ALL overrides
-      const int k4_all_env = route.k4_all;
-      const bool k4_all = k4_all_env >= 0 ? k4_all_env != 0 : p->dtype == QTN_C128;
-      if (qtn_k4_node(&d, k4_all ? 0 : k4_min_e, p->timing, nd.first, plan.data(), &fn, &grid, &smem) == QTN_OK) {
-        specs[i].k3plan = std::move(plan);
-        specs[i].fn = fn;
-        specs[i].grid = grid;
-        specs[i].smem = smem;
-        specs[i].args[0] = specs[i].k3plan.data();
-        k4 = true;
-        ++g->kinds[3];
-        --g->kinds[0];
-        g->node_kind.back() = 3;
-      }   // else: not an expansion item (K3 / K1 below)
+      const bool k4_all = route.k4_all >= 0 ? route.k4_all != 0 : p->dtype == QTN_C128;
+      if (qtn_k4_node(&d, k4_all ? 0 : route.k4_min_e, p->timing, sub.first, plan.data(), &fn, &grid, &smem) ==
+          QTN_OK) {
+        take(std::move(plan), fn, grid, smem, 3);
+        return QTN_OK;
+      }
     }
-    if (!k5 && !k4 && nd.kind == QTN_NODE_LARGE && p->arena && have_mems &&
-        k3_route(items[nd.first], mems_ptr, p->dtype)) {
-      qtn_bucket_desc_t d;
-      k3_desc(p, items[nd.first], mems_ptr, &d);
-      specs[i].k3plan.resize(qtn_k3_plan_bytes());
-      const void* fn = nullptr;
-      int grid = 0, smem = 0;
-      if (qtn_k3_node(&d, p->timing, nd.first, specs[i].k3plan.data(), &fn, &grid, &smem) == QTN_OK) {
-        specs[i].fn = fn;
-        specs[i].grid = grid;
-        specs[i].smem = smem;
-        specs[i].args[0] = specs[i].k3plan.data();
-        ++g->kinds[2];
-        --g->kinds[0];
-        g->node_kind.back() = 2;
-      }   // else: K1 stays (the K3 planner declined this item)
+    if (k3_route(it, mems_ptr, p->dtype)) {
+      std::vector<unsigned char> plan(qtn_k3_plan_bytes());
+      if (qtn_k3_node(&d, p->timing, sub.first, plan.data(), &fn, &grid, &smem) == QTN_OK)
+        take(std::move(plan), fn, grid, smem, 2);
+      // else: K1 stays (the K3 planner declined this item)
+    }
+    return QTN_OK;
+  };
+  auto add_kernel = [&](const LaunchSpec& spec, const std::vector<cudaGraphNode_t>& deps, bool first_node,
+                        cudaGraphNode_t* node) -> int {
+    cudaKernelNodeParams kp = {};
+    kp.func = const_cast<void*>(spec.fn);
+    kp.gridDim = dim3(spec.grid);
+    kp.blockDim = dim3(NT);
+    kp.sharedMemBytes = spec.smem;
+    kp.kernelParams = const_cast<void**>(spec.args);
+    cudaError_t e2 = cudaGraphAddKernelNode(node, g->graph, (h2d && first_node) ? &h2d : nullptr,
+                                            (h2d && first_node) ? 1 : 0, &kp);
+    if (e2 != cudaSuccess) return cuda_err(e2, "cudaGraphAddKernelNode");
+    // programmatic edges (PDL): the kernels call griddepcontrol.wait before
+    // reading predecessor outputs
+    for (cudaGraphNode_t from : deps) {
+      cudaGraphEdgeData ed = {};
+      ed.from_port = use_pdl ? cudaGraphKernelNodePortProgrammatic : cudaGraphKernelNodePortDefault;
+      ed.type = use_pdl ? cudaGraphDependencyTypeProgrammatic : cudaGraphDependencyTypeDefault;
+      e2 = cudaGraphAddDependencies_v2(g->graph, &from, node, &ed, 1);
+      if (e2 != cudaSuccess) return cuda_err(e2, "cudaGraphAddDependencies_v2");
+    }
+    return QTN_OK;
+  };
+  for (int i = 0; i < n_nodes; ++i) {
+    const qtn_node_t& nd = nodes[i];
+    const bool pair = nd.kind == QTN_NODE_LARGE && nd.count == 2;
+    if (nd.kind == QTN_NODE_LARGE &&
+        (nd.first < 0 || nd.first + (pair ? 1 : 0) >= p->n_buckets || (nd.count != 1 && nd.count != 2))) {
+      qtn_graph_destroy(g);
+      return set_err(QTN_E_INVALID, "node %d: items [%d, +%d) out of range", i, nd.first, nd.count);
     }
     std::vector<cudaGraphNode_t> deps;
     for (int d = 0; d < nd.n_dep; ++d) {
@@ -1439,30 +1463,65 @@ int qtn_graph_create_host(const qtn_program_t* p, const qtn_bucket_t* items, con
       }
       deps.push_back(gn[j]);
     }
-    cudaKernelNodeParams kp = {};
-    kp.func = const_cast<void*>(specs[i].fn);
-    kp.gridDim = dim3(specs[i].grid);
-    kp.blockDim = dim3(NT);
-    kp.sharedMemBytes = specs[i].smem;
-    kp.kernelParams = specs[i].args;
-    e = cudaGraphAddKernelNode(&gn[i], g->graph, (h2d && nd.n_dep == 0) ? &h2d : nullptr,
-                               (h2d && nd.n_dep == 0) ? 1 : 0, &kp);
-    if (e != cudaSuccess) {
-      qtn_graph_destroy(g);
-      return cuda_err(e, "cudaGraphAddKernelNode");
-    }
-    // programmatic edges (PDL): the kernels call griddepcontrol.wait before
-    // reading predecessor outputs
-    for (cudaGraphNode_t from : deps) {
-      cudaGraphEdgeData ed = {};
-      ed.from_port = use_pdl ? cudaGraphKernelNodePortProgrammatic : cudaGraphKernelNodePortDefault;
-      ed.type = use_pdl ? cudaGraphDependencyTypeProgrammatic : cudaGraphDependencyTypeDefault;
-      e = cudaGraphAddDependencies_v2(g->graph, &from, &gn[i], &ed, 1);
-      if (e != cudaSuccess) {
-        qtn_graph_destroy(g);
-        return cuda_err(e, "cudaGraphAddDependencies_v2");
+    int fam = 0;
+    if (pair) {
+      // producer / consumer pair (the producer's result is read by the
+      // consumer only): K6 keeps the producer's result out of HBM; otherwise
+      // the two items run as two kernels in sequence
+      const qtn_bucket_t& bp = items[nd.first];
+      const qtn_bucket_t& bc = items[nd.first + 1];
+      bool fused = false;
+      if (route.k6_min_w > 0 && bp.w >= route.k6_min_w && p->arena && have_mems) {
+        int ipc = -1;
+        for (int j = 0; j < bc.n_mem; ++j)
+          if (mems_ptr[bc.mem_begin + j].off == bp.out_off) ipc = j;
+        qtn_bucket_desc_t dp, dc;
+        k3_desc(p, bp, mems_ptr, &dp);
+        k3_desc(p, bc, mems_ptr, &dc);
+        std::vector<unsigned char> plan(qtn_k6_plan_bytes());
+        const void* fn = nullptr;
+        int grid = 0, smem = 0;
+        if (ipc >= 0 && qtn_k6_node(&dp, &dc, ipc, p->timing, nd.first, nd.first + 1, plan.data(), &fn, &grid,
+                                    &smem) == QTN_OK) {
+          specs[i].prog = *p;
+          specs[i].k3plan = std::move(plan);
+          specs[i].fn = fn;
+          specs[i].grid = grid;
+          specs[i].smem = smem;
+          specs[i].args[0] = specs[i].k3plan.data();
+          fam = 5;
+          fused = true;
+          rc = add_kernel(specs[i], deps, nd.n_dep == 0, &gn[i]);
+        }
       }
+      if (!fused) {
+        qtn_node_t sp = nd, sc = nd;
+        sp.count = sc.count = 1;
+        sc.first = nd.first + 1;
+        sp.variant = nd.n_tickets;   // LARGE pairs carry the producer's K1 variant here
+        sp.n_tickets = sc.n_tickets = 0;
+        sp.smem_bytes = (int32_t)((bp.smem_elems * esz + 15) / 16 * 16);
+        LaunchSpec lp;
+        int fp = 0;
+        cudaGraphNode_t np_ = nullptr;
+        rc = route_node(sp, i, lp, fp);
+        if (!rc) rc = add_kernel(lp, deps, nd.n_dep == 0, &np_);
+        if (!rc) {
+          ++g->kinds[fp];
+          rc = route_node(sc, i, specs[i], fam);
+        }
+        if (!rc) rc = add_kernel(specs[i], std::vector<cudaGraphNode_t>{np_}, false, &gn[i]);
+      }
+    } else {
+      rc = route_node(nd, i, specs[i], fam);
+      if (!rc) rc = add_kernel(specs[i], deps, nd.n_dep == 0, &gn[i]);
     }
+    if (rc) {
+      qtn_graph_destroy(g);
+      return rc;
+    }
+    ++g->kinds[fam];
+    g->node_kind.push_back(fam);
   }
   // optional result download after every kernel node
   if (io && io->d2h_bytes > 0) {
@@ -1492,7 +1551,7 @@ int qtn_graph_launch(qtn_graph_t* g, void* stream) {
 
 int qtn_graph_kinds(const qtn_graph_t* g, int32_t* counts) {
   if (!g || !counts) return set_err(QTN_E_INVALID, "null argument");
-  for (int i = 0; i < 5; ++i) counts[i] = g->kinds[i];
+  for (int i = 0; i < 6; ++i) counts[i] = g->kinds[i];
   return QTN_OK;
 }
 

@@ -116,6 +116,9 @@ SMALL_ITER_BITS_SINGLE = {"complex64": int(_SIB) if _SIB else 11, "complex128": 
 SMALL_TILE_BITS = {"complex64": 8, "complex128": 7}  # K2 tiles: below one vector step
 # QTN_MERGE=0 disables chain merging (A/B measurements)
 MERGE_DEFAULT = os.environ.get("QTN_MERGE", "1") != "0"
+# producer / consumer pair nodes (K6 in the graph builder; the library knob
+# QTN_K6 sets the narrowest producer it fuses, 0 = two kernels per pair)
+FUSE_PAIRS = True
 
 
 @dataclass
@@ -753,10 +756,21 @@ class Program:
             _, i, b = q
             return b < 0 or tls[i]["variant"][b] == VARIANT_SMALL
 
+        # producer / consumer pairs (one node, K6 in the graph builder)
+        self.fused = self._pairs(keys, tls, order_gid, prods, deps_all, is_small) if FUSE_PAIRS else {}
+        fused_c = {c: p_ for p_, c in self.fused.items()}
         node_of = [-1] * len(keys)
         nodes = []           # dict(kind, items, deps:set)
         open_stage = -1
         for g, q in enumerate(keys):
+            if g in self.fused:
+                continue          # placed with its consumer
+            if g in fused_c:
+                p_ = fused_c[g]
+                ext = {node_of[x] for x in set(deps_all[p_]) | set(deps_all[g]) if x not in (p_, g)}
+                nodes.append({"kind": N.QTN_NODE_LARGE, "items": [p_, g], "deps": ext})
+                node_of[p_] = node_of[g] = len(nodes) - 1
+                continue
             ext = {node_of[p] for p in deps_all[g]}
             if is_small(q):
                 # join the open stage unless a producer is a node created after it
@@ -810,6 +824,7 @@ class Program:
             # K2 stage: double-precision products + staged unrounded input members
             node_smem = SMALL_PROD_ELEMS * 16 + N.MAX_MEMBERS * K2_HI_SLOT * 16 if is_stage else 0
             variant = 0
+            pair_variant = 0   # LARGE pair: the producer's K1 variant (qtn_node_t.n_tickets)
             for gid in gids:
                 (_, i, b), g = item_keys[gid]
                 tl = tls[i]
@@ -824,6 +839,9 @@ class Program:
                         off = ib + in_off[ref] if mk[j] == 0 else out_elem[order_gid[(i, ref)]]
                         members.append((off, mm[j], msm[j], mc[j]))
                     if not is_stage:
+                        if gid == first and count == 2:
+                            pair_variant = tl["variant"][b]
+                            smem_max = max(smem_max, _align(tl["smem_elems"][b] * esz, 16))
                         variant = tl["variant"][b]
                         node_smem = _align(tl["smem_elems"][b] * esz, 16)
                     w_, k_, L_, out_, slot_, nmem_ = tl["w"][b], tl["k"][b], tl["L"][b], out_elem[g], -1, j1 - j0
@@ -846,7 +864,7 @@ class Program:
                 tick += ntiles[gid]
             smem_max = max(smem_max, node_smem)
             dl = sorted(nd["deps"])
-            node_list.append((nd["kind"], first, count, tick if is_stage else 0,
+            node_list.append((nd["kind"], first, count, tick if is_stage else pair_variant,
                               variant, len(node_deps), len(dl), node_smem))
             node_deps.extend(dl)
         B = np.array(recs, dtype=N.BUCKET_DT) if nb else np.zeros(0, N.BUCKET_DT)
@@ -873,6 +891,48 @@ class Program:
             src.append(s_)
         self.img_dst = np.concatenate(dst) if dst else np.zeros(0, np.int64)
         self.img_src_parts = src
+
+    @staticmethod
+    def _pairs(keys, tls, order_gid, prods, deps_all, is_small):
+        """Producer -> consumer pairs for K6 (csrc/bucket_expand.cu): the
+        consumer C is a large item reading the producer P's whole result as a
+        member that carries every result and summed index of C (P.w = C.w +
+        C.k, C.k <= 3), P is a large item with k <= 3 read by C alone, and no
+        other item waits for P (no write-after-read edge on P's inputs).  The
+        pair becomes one node; the graph builder runs it as one K6 kernel when
+        P is a K4 expansion with C's summed bits set aside (else as two
+        kernels).  A producer is never itself a consumer of another pair."""
+        dependents = {}
+        for g, ds in enumerate(deps_all):
+            for d in ds:
+                dependents.setdefault(d, set()).add(g)
+        readers = {}
+        for g, ps in enumerate(prods):
+            for p_ in ps:
+                readers[p_] = readers.get(p_, 0) + 1
+        pairs, used = {}, set()
+        for g, (_, i, b) in enumerate(keys):
+            if b < 0 or is_small(keys[g]) or g in used:
+                continue
+            tl = tls[i]
+            w, k = tl["w"][b], tl["k"][b]
+            if not 1 <= k <= 3:
+                continue
+            for j in range(tl["mem_ptr"][b], tl["mem_ptr"][b + 1]):
+                if tl["mem_kind"][j] != 1:
+                    continue
+                if tl["mem_mask"][j] != (1 << w) - 1 or tl["mem_smask"][j] != (1 << k) - 1:
+                    continue
+                pb = tl["mem_ref"][j]
+                p_ = order_gid[(i, pb)]
+                if p_ in used or is_small(keys[p_]) or not 1 <= tl["k"][pb] <= 3 or tl["w"][pb] != w + k:
+                    continue
+                if readers.get(p_, 0) != 1 or dependents.get(p_, set()) != {g}:
+                    continue
+                pairs[p_] = g
+                used |= {p_, g}
+                break
+        return pairs
 
     def algorithmic_bytes(self) -> int:
         return sum(algorithmic_bytes(inst.template, self.dtype) for inst in self.instances)
@@ -1025,14 +1085,14 @@ class Executor:
         return g
 
     def kernel_mix(self, io=False):
-        """{'K1', 'K2', 'K3', 'K4', 'K5'}: graph nodes per kernel family."""
+        """{'K1', ..., 'K6'}: kernels per family in the program graph."""
         g = self.graph
-        c = (ctypes.c_int32 * 5)()
+        c = (ctypes.c_int32 * 6)()
         N.check(N.load().qtn_graph_kinds(g, c))
         return dict(zip(N.KERNEL_FAMILIES, (int(x) for x in c)))
 
     def node_kernels(self, io=False):
-        """Per graph node, the kernel family that runs it ('K1'..'K5')."""
+        """Per graph node, the kernel family that runs it ('K1'..'K6')."""
         g = self.graph
         n = int(self.prog.n_nodes)
         c = (ctypes.c_int32 * max(n, 1))()

@@ -467,3 +467,36 @@ def test_native_dry_run_and_slicing_match_python():
         Q.dry_run(nets[0][0], nets[0][1][:-1])
     with pytest.raises(ValueError, match="target_width"):
         Q.suggest_slicing(nets[0][0], nets[0][1], 0)
+
+
+@pytest.mark.parametrize("dtype", ["complex64", "complex128"])
+def test_producer_consumer_pairs_cfg2(dtype):
+    """K6 pairs (engine.Program._pairs): the cfg-2 lightcone's widest
+    intermediate (w = 24, read whole by the w = 22 k = 2 item) becomes one pair
+    node; every pair's producer is read by its consumer only, as a member that
+    carries every consumer index in canonical order; the program still
+    evaluates to the oracle's value (emulator runs the pair's items in order)."""
+    g, graph, params = _cfg("cfg2")
+    c = Q.qaoa_maxcut_circuit(graph, params)
+    lc = Q.extract_lightcone(c, (0, 15), cone="tight")
+    order = Q.greedy_order(lc.network)
+    t = E.plan_template([x.indices for x in lc.network.tensors], order, dtype, wave_aware=True)
+    prog = E.Program([E.Instance(t)], dtype)
+    B, M = prog.buckets, prog.members
+    pairs = [nd for nd in prog.nodes if nd["kind"] == 1 and nd["count"] == 2]
+    assert len(pairs) == len(prog.fused) >= 1
+    widths = sorted((int(B[nd["first"]]["w"]), int(B[nd["first"] + 1]["w"])) for nd in pairs)
+    assert (24, 22) in widths
+    for nd in pairs:
+        p_, c_ = B[nd["first"]], B[nd["first"] + 1]
+        assert p_["w"] == c_["w"] + c_["k"]
+        readers = [g for g in range(prog.n_buckets) for m in M[B[g]["mem_begin"]: B[g]["mem_begin"] + B[g]["n_mem"]]
+                   if m["off"] == p_["out_off"]]
+        assert readers == [nd["first"] + 1]
+        m = [m for m in M[c_["mem_begin"]: c_["mem_begin"] + c_["n_mem"]] if m["off"] == p_["out_off"]][0]
+        assert m["mask"] == (1 << int(c_["w"])) - 1 and m["smask"] == (1 << int(c_["k"])) - 1
+    if dtype == "complex128":   # (the emulator takes ~30 s on this program)
+        ts = [(x.indices, x.data) for x in lc.network.tensors]
+        ref, _ = O.contract_network(ts, order)
+        val = run_program(prog, [np.concatenate([np.asarray(x.data).ravel() for x in lc.network.tensors])])[0]
+        assert abs(val - ref) <= 1e-12 * abs(ref)
