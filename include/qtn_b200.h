@@ -372,6 +372,12 @@ int qtn_bucket_stream(const qtn_bucket_desc_t* desc, void* stream);
  * QTN_E_UNSUPPORTED when the pair does not have that shape. */
 int qtn_bucket_expand_fused(const qtn_bucket_desc_t* producer, const qtn_bucket_desc_t* consumer,
                             int32_t member, void* stream);
+/* Plan only (no device): info[8] = producer summed bits, consumer summed
+ * bits, expansion bits, product-table bits, gathered consumer members,
+ * uniform consumer members, consumer summed bits no gathered member carries,
+ * tile-id bits.  Same errors as qtn_bucket_expand_fused. */
+int qtn_bucket_expand_fused_plan(const qtn_bucket_desc_t* producer, const qtn_bucket_desc_t* consumer,
+                                 int32_t member, int32_t* info);
 
 #ifdef __cplusplus
 }

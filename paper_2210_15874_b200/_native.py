@@ -47,6 +47,7 @@ EXPORTS = (
     "qtn_bucket_expand",
     "qtn_bucket_stream",
     "qtn_bucket_expand_fused",
+    "qtn_bucket_expand_fused_plan",
     "qtn_route_config",
     "qtn_graph_node_kinds",
     "qtn_graph_launch",
@@ -162,6 +163,8 @@ def load(path: str = LIB_PATH):
     lib.qtn_bucket_expand.argtypes = [ctypes.POINTER(BucketDescC), i32, vp]
     lib.qtn_bucket_expand_fused.restype = ctypes.c_int
     lib.qtn_bucket_expand_fused.argtypes = [ctypes.POINTER(BucketDescC), ctypes.POINTER(BucketDescC), i32, vp]
+    lib.qtn_bucket_expand_fused_plan.restype = ctypes.c_int
+    lib.qtn_bucket_expand_fused_plan.argtypes = [ctypes.POINTER(BucketDescC), ctypes.POINTER(BucketDescC), i32, vp]
     lib.qtn_bucket_stream.restype = ctypes.c_int
     lib.qtn_bucket_stream.argtypes = [ctypes.POINTER(BucketDescC), vp]
     lib.qtn_route_config.restype = ctypes.c_char_p
@@ -329,6 +332,16 @@ def bucket_expand_fused_launch(producer, consumer, member, stream):
     lib = require_device()
     check(lib.qtn_bucket_expand_fused(ctypes.byref(producer), ctypes.byref(consumer), int(member),
                                       ctypes.c_void_p(stream)))
+
+
+def bucket_expand_fused_plan(producer, consumer, member):
+    """K6 plan only (no device): (producer k, consumer k, expansion bits,
+    product-table bits, gathered members, uniform members, q bits no gathered
+    member carries, tile-id bits)."""
+    lib = load()
+    info = (ctypes.c_int32 * 8)()
+    check(lib.qtn_bucket_expand_fused_plan(ctypes.byref(producer), ctypes.byref(consumer), int(member), info))
+    return tuple(info)
 
 
 def bucket_stream_launch(desc, stream):

@@ -38,78 +38,9 @@
 #include <cstring>
 #include <string>
 
-int qtn_internal_set_error(int code, const char* msg);
-
-// QTN_DEBUG build: bounds-check every member / product-table / result index
-#ifdef QTN_DEBUG
-#define K4_CHECK(cond, ...)                                                        \
-  do {                                                                             \
-    if (!(cond)) {                                                                 \
-      printf("K4_CHECK %s:%d (block %d thread %d): ", __FILE__, __LINE__,          \
-             (int)blockIdx.x, (int)threadIdx.x);                                   \
-      printf(__VA_ARGS__);                                                         \
-      printf("\n");                                                               \
-      __trap();                                                                    \
-    }                                                                              \
-  } while (0)
-#else
-#define K4_CHECK(cond, ...) \
-  do {                      \
-  } while (0)
-#endif
+#include "k4_plan.h"
 
 namespace qtn_k4 {
-
-constexpr int NT = 256;
-constexpr int TBB = 8;                  // thread bits (log2 NT)
-constexpr int MAXE = 8;                 // expansion bits (the low 4 unrolled per thread, the rest rolled)
-constexpr int K4_WIDE_E_MIN_W = 20;     // more than 4 expansion bits: widths from here
-constexpr int MAXKS = 3;                // summed bits
-constexpr int MAXFB = 12;               // F table bits (|F| + k)
-constexpr int MAXM = QTN_MAX_MEMBERS;
-constexpr int MAXH = 32;                // tile-selecting result bits
-constexpr int MAXQ = 3;                 // K6: consumer summed bits (set-aside producer bits)
-
-struct Plan {
-  void* out;
-  const void* mptr[MAXM];
-  int32_t nm, k, nE, nF, nH, iB;
-  int32_t nHF;                          // tile-id bits other members carry (the highest nHF of nH)
-  int64_t n_tiles;
-  int64_t out_elems;                    // 2^w
-  int64_t span[MAXM];                   // elements each member spans (QTN_DEBUG bounds checks)
-  int64_t hs[MAXM + 1][MAXH];           // per member (and out, index nm): stride of tile bit j
-  uint32_t fs[MAXM][MAXFB];             // F entry bit q (s bits first) -> member stride
-  int64_t bs[MAXKS];                    // B strides of the summed bits
-  int64_t btb[TBB];                     // B strides of the thread bits
-  int32_t otb[TBB], ftb[TBB];           // out stride / F index bit of the thread bits
-  int32_t oe[MAXE], fe[MAXE];           // out stride / F index bit of the expansion bits
-  int32_t rb;                           // replica bit present (RB = 2): a B bit no other member carries
-  int64_t rbs;                          // its B stride
-  int32_t rbo;                          // its output stride
-  unsigned long long* timing;
-  int32_t item;
-  // result bit of every thread / expansion / tile bit (fused plans map a
-  // consumer's members onto the same bits); the nq set-aside bits (K6)
-  int8_t tbit[TBB], ebit[MAXE], hbit[MAXH];
-  int32_t nq;                           // top result bits set aside (K6: the consumer's summed bits)
-  int64_t bq[MAXQ];                     // B stride of set-aside bit i
-  int32_t fq[MAXQ];                     // F index bit (1 << f) of set-aside bit i, 0 = no other member carries it
-};
-
-template <typename R> struct Cx;
-template <> struct Cx<float> { using T = float2; };
-template <> struct Cx<double> { using T = double2; };
-
-template <typename T>
-__device__ __forceinline__ T cmul(T a, T b) {
-  return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x};
-}
-template <typename T>
-__device__ __forceinline__ void cfma(T& acc, T a, T b) {
-  acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
-  acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
-}
 
 // complex64 variants are compiled for >= 4 resident blocks (<= 64 registers:
 // cfg-2 0.2395 -> 0.2346 ms, the default heuristic picked 32 registers with
@@ -330,327 +261,6 @@ __device__ __forceinline__ void k4_body(const Plan& P) {
   }
 }
 
-// =========================================================================
-// K6: an expansion item fused with its only consumer
-// =========================================================================
-// A consumer item C whose member X is the whole result of a K4-shaped
-// producer item P (X carries every result and summed bit of C, so P's result
-// bits are C's result bits r followed by C's summed bits q):
-//     out_C[r] = sum_q G(q, r) * X(q, r),   X(q, r) = sum_s B(s, q, r) * F(f(q, r), s)
-// G = the product of C's other members.  P's K4 plan is made with the q bits
-// set aside: each thread loads B for every (q, s) into registers, forms X(q,
-// r) for its results in registers and sums over q right away — X (the widest
-// intermediate of a lightcone: 2^24 complex128 = 268 MB at cfg-2) is never
-// written to or read back from HBM.  Products and sums follow the unfused
-// order (s ascending inside X, q ascending outside); X is not rounded to the
-// element type in between.
-constexpr int MAXG = 2;   // consumer members carrying result bits (gathered per result)
-
-struct FPlan {
-  Plan p;                     // producer plan, q bits set aside; p.out = C's output
-  int32_t ng;                 // gathered consumer members
-  const void* gptr[MAXG];
-  int64_t ghs[MAXG][MAXH];    // stride of tile bit j (p.hbit order)
-  int32_t gtb[MAXG][TBB];     // stride of thread bit t
-  int32_t ge[MAXG][MAXE];     // stride of expansion bit e
-  int32_t gq[MAXG][MAXQ];     // stride of consumer summed bit i
-  int64_t gspan[MAXG];
-  int32_t nu;                 // consumer members on summed bits only: folded into U[q]
-  const void* uptr[MAXM];
-  int32_t uq[MAXM][MAXQ];
-  int32_t item_c;             // consumer item (timing; p.item = producer)
-};
-
-template <typename R, int K, int NE, int NQ>
-__device__ __forceinline__ void k6_body(const FPlan& FP);
-
-template <typename R, int K, int NE, int NQ>
-__global__ void __launch_bounds__(NT, 2) k6_kernel_c64(const __grid_constant__ FPlan FP) {
-  k6_body<R, K, NE, NQ>(FP);
-}
-template <typename R, int K, int NE, int NQ>
-__global__ void __launch_bounds__(NT, 2) k6_kernel_c128(const __grid_constant__ FPlan FP) {
-  k6_body<R, K, NE, NQ>(FP);
-}
-
-template <typename R, int K, int NE, int NQ>
-__device__ __forceinline__ void k6_body(const FPlan& FP) {
-  using T = typename Cx<R>::T;
-  const Plan& P = FP.p;
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  constexpr int NS = 1 << K;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* F = reinterpret_cast<T*>(smem_raw);
-  const int nfe = 1 << (P.nF + K);
-  uint32_t* LUT = reinterpret_cast<uint32_t*>(smem_raw + sizeof(T) * nfe);
-  __shared__ int64_t sbase[MAXM + 1];
-  __shared__ T sU[NQ];
-  const int tid = threadIdx.x;
-  const int nm = P.nm;
-  const int ng = FP.ng;
-  const int nlo = P.nF + K < 6 ? P.nF + K : 6;
-  for (int x = tid; x < nm * 128; x += NT) {
-    const int j = x >> 7, y = x & 63, hi = (x >> 6) & 1;
-    uint32_t o = 0;
-    if (j != P.iB)
-      for (int b = 0; b < 6; ++b) {
-        const int q = hi ? nlo + b : b;
-        if (((y >> b) & 1) && (hi ? q < P.nF + K : b < nlo)) o += P.fs[j][q];
-      }
-    LUT[x] = o;
-  }
-  int64_t boff = 0;
-  int32_t ob = 0, fb = 0;
-  int32_t gthr[MAXG] = {};
-#pragma unroll
-  for (int b = 0; b < TBB; ++b)
-    if ((tid >> b) & 1) {
-      boff += P.btb[b];
-      ob += P.otb[b];
-      fb += P.ftb[b];
-#pragma unroll
-      for (int g = 0; g < MAXG; ++g) gthr[g] += FP.gtb[g][b];
-    }
-  // the low 2 expansion bits unrolled (the B file already holds NQ * NS
-  // values), the rest walked by a rolled loop
-  constexpr int NEL = NE < 2 ? NE : 2;
-  constexpr int NEH = NE - NEL;
-  constexpr int NEVL = 1 << NEL;
-  int32_t oe[NEVL], fe[NEVL];
-#pragma unroll
-  for (int e = 0; e < NEVL; ++e) {
-    int32_t o = 0, f = 0;
-#pragma unroll
-    for (int b = 0; b < NEL; ++b)
-      if ((e >> b) & 1) {
-        o += P.oe[b];
-        f += P.fe[b];
-      }
-    oe[e] = o;
-    fe[e] = (fb + f) << K;
-  }
-  int64_t soffB[NS], qoffB[NQ];
-  int32_t fqo[NQ];
-#pragma unroll
-  for (int s = 0; s < NS; ++s) {
-    int64_t o = 0;
-#pragma unroll
-    for (int b = 0; b < K; ++b)
-      if ((s >> b) & 1) o += P.bs[b];
-    soffB[s] = o;
-  }
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    int64_t o = 0;
-    int32_t f = 0;
-#pragma unroll
-    for (int b = 0; b < MAXQ; ++b)
-      if ((1 << b) < NQ && ((q >> b) & 1)) {
-        o += P.bq[b];
-        f += P.fq[b];
-      }
-    qoffB[q] = o;
-    fqo[q] = f << K;
-  }
-  const int64_t per = (P.n_tiles + gridDim.x - 1) / gridDim.x;
-  int64_t h = (int64_t)blockIdx.x * per;
-  const int64_t h_end = h + per < P.n_tiles ? h + per : P.n_tiles;
-  if (h >= h_end) return;
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  unsigned long long t_start = 0;
-  if (P.timing && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-  // U[q] = product of the consumer members that carry no result bit
-  if (tid < NQ) {
-    T u = {R(1), R(0)};
-    for (int i = 0; i < FP.nu; ++i) {
-      int32_t o = 0;
-#pragma unroll
-      for (int b = 0; b < MAXQ; ++b)
-        if ((tid >> b) & 1) o += FP.uq[i][b];
-      u = cmul(u, __ldg(reinterpret_cast<const T*>(FP.uptr[i]) + o));
-    }
-    sU[tid] = u;
-  }
-  __syncthreads();
-  const T* Bm = reinterpret_cast<const T*>(P.mptr[P.iB]);
-  T* out = reinterpret_cast<T*>(P.out);
-  const int shf = P.nH - P.nHF;
-  int64_t fkey = -1;
-  for (; h < h_end; ++h) {
-    int64_t bb = 0, obase = 0;
-    int64_t gb[MAXG] = {};
-    for (int b = 0; b < P.nH; ++b)
-      if ((h >> b) & 1) {
-        bb += P.hs[P.iB][b];
-        obase += P.hs[nm][b];
-#pragma unroll
-        for (int g = 0; g < MAXG; ++g) gb[g] += FP.ghs[g][b];
-      }
-    // B for every (q, s): NQ * NS independent loads in flight
-    T bv[NQ][NS];
-    {
-      const T* bp = Bm + bb + boff;
-#pragma unroll
-      for (int q = 0; q < NQ; ++q)
-#pragma unroll
-        for (int s = 0; s < NS; ++s) {
-          K4_CHECK(bb + boff + qoffB[q] + soffB[s] >= 0 && bb + boff + qoffB[q] + soffB[s] < P.span[P.iB],
-                   "K6 B element %lld", (long long)(bb + boff + qoffB[q] + soffB[s]));
-          bv[q][s] = __ldg(bp + qoffB[q] + soffB[s]);
-        }
-      // U[q] folded into the B file (NQ * NS products per tile instead of
-      // one per result and q)
-      if (FP.nu) {
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-          const T u = sU[q];
-#pragma unroll
-          for (int s = 0; s < NS; ++s) bv[q][s] = cmul(u, bv[q][s]);
-        }
-      }
-    }
-    if ((h >> shf) != fkey) {
-      fkey = h >> shf;
-      __syncthreads();
-      if (tid < nm) {
-        int64_t o = 0;
-        for (int b = shf; b < P.nH; ++b)
-          if ((h >> b) & 1) o += P.hs[tid][b];
-        sbase[tid] = o;
-      }
-      __syncthreads();
-      for (int x = tid; x < nfe; x += NT) {
-        T v = {R(1), R(0)};
-        const int lo = x & 63, hi = x >> 6;
-        for (int j = 0; j < nm; ++j) {
-          if (j == P.iB) continue;
-          const T* mp = reinterpret_cast<const T*>(P.mptr[j]);
-          K4_CHECK(sbase[j] + LUT[j * 128 + lo] + LUT[j * 128 + 64 + hi] < P.span[j], "K6 member %d", j);
-          v = cmul(v, __ldg(mp + sbase[j] + LUT[j * 128 + lo] + LUT[j * 128 + 64 + hi]));
-        }
-        F[x] = v;
-      }
-      __syncthreads();
-    }
-    auto emit = [&](int32_t oh, int32_t fh, const int32_t (&gh)[MAXG]) {
-      T* op = out + obase + ob + oh;
-#pragma unroll
-      for (int e = 0; e < NEVL; ++e) {
-        int32_t ge[MAXG];
-#pragma unroll
-        for (int g = 0; g < MAXG; ++g) {
-          int32_t o = gthr[g] + gh[g];
-#pragma unroll
-          for (int b = 0; b < NEL; ++b)
-            if ((e >> b) & 1) o += FP.ge[g][b];
-          ge[g] = o;
-        }
-        T acc;
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-          const T* fp = F + fe[e] + fh + fqo[q];
-          K4_CHECK(fe[e] + fh + fqo[q] + NS <= nfe, "K6 F entry %d of %d", fe[e] + fh + fqo[q] + NS, nfe);
-          T x = cmul(bv[q][0], fp[0]);
-#pragma unroll
-          for (int s = 1; s < NS; ++s) cfma(x, bv[q][s], fp[s]);
-#pragma unroll
-          for (int gi = 0; gi < MAXG; ++gi)
-            if (gi < ng) {
-              int32_t o = ge[gi];
-#pragma unroll
-              for (int b = 0; b < MAXQ; ++b)
-                if ((1 << b) < NQ && ((q >> b) & 1)) o += FP.gq[gi][b];
-              K4_CHECK(gb[gi] + o >= 0 && gb[gi] + o < FP.gspan[gi], "K6 consumer member %d element %lld", gi,
-                       (long long)(gb[gi] + o));
-              x = cmul(__ldg(reinterpret_cast<const T*>(FP.gptr[gi]) + gb[gi] + o), x);
-            }
-          if (q == 0) {
-            acc = x;
-          } else {
-            acc.x += x.x;
-            acc.y += x.y;
-          }
-        }
-        K4_CHECK(obase + ob + oh + oe[e] >= 0 && obase + ob + oh + oe[e] < P.out_elems, "K6 result %lld",
-                 (long long)(obase + ob + oh + oe[e]));
-        op[oe[e]] = acc;
-      }
-    };
-    if constexpr (NEH == 0) {
-      const int32_t gh[MAXG] = {};
-      emit(0, 0, gh);
-    } else {
-#pragma unroll 1
-      for (int eh = 0; eh < (1 << NEH); ++eh) {
-        int32_t oh = 0, fh = 0;
-        int32_t gh[MAXG] = {};
-#pragma unroll
-        for (int b = 0; b < NEH; ++b)
-          if ((eh >> b) & 1) {
-            oh += P.oe[NEL + b];
-            fh += P.fe[NEL + b] << K;
-#pragma unroll
-            for (int g = 0; g < MAXG; ++g) gh[g] += FP.ge[g][NEL + b];
-          }
-        emit(oh, fh, gh);
-      }
-    }
-  }
-  if (P.timing && tid == 0) {
-    unsigned long long t_end;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
-    atomicMin(&P.timing[2 * P.item], t_start);
-    atomicMax(&P.timing[2 * P.item + 1], t_end);
-    atomicMin(&P.timing[2 * FP.item_c], t_start);
-    atomicMax(&P.timing[2 * FP.item_c + 1], t_end);
-  }
-}
-
-// register budget of the B file: NQ * 2^K values per thread
-template <typename R, int K, int NQ>
-constexpr bool k6_fits() {
-  return NQ * (1 << K) <= (sizeof(R) == 4 ? 32 : 16);
-}
-
-template <typename R, int K, int NE, int NQ>
-const void* fn_k6e() {
-  if constexpr (!k6_fits<R, K, NQ>())
-    return nullptr;
-  else if constexpr (sizeof(R) == 4)
-    return (const void*)k6_kernel_c64<R, K, NE, NQ>;
-  else
-    return (const void*)k6_kernel_c128<R, K, NE, NQ>;
-}
-
-template <typename R, int K, int NQ>
-const void* fn_k6_ne(int ne) {
-  switch (ne) {
-    case 0: return fn_k6e<R, K, 0, NQ>();
-    case 1: return fn_k6e<R, K, 1, NQ>();
-    case 2: return fn_k6e<R, K, 2, NQ>();
-    case 3: return fn_k6e<R, K, 3, NQ>();
-    case 4: return fn_k6e<R, K, 4, NQ>();
-    case 5: return fn_k6e<R, K, 5, NQ>();
-    case 6: return fn_k6e<R, K, 6, NQ>();
-    case 7: return fn_k6e<R, K, 7, NQ>();
-    default: return fn_k6e<R, K, 8, NQ>();
-  }
-}
-
-template <typename R, int K>
-const void* fn_k6_q(int nq, int ne) {
-  if (nq == 1) return fn_k6_ne<R, K, 2>(ne);
-  if (nq == 2) return fn_k6_ne<R, K, 4>(ne);
-  return fn_k6_ne<R, K, 8>(ne);
-}
-
-template <typename R>
-const void* fn_k6(int k, int nq, int ne) {
-  if (k == 1) return fn_k6_q<R, 1>(nq, ne);
-  if (k == 2) return fn_k6_q<R, 2>(nq, ne);
-  return fn_k6_q<R, 3>(nq, ne);
-}
-
 template <typename R, int K, int NE, int RB>
 const void* fn_k() {
   if constexpr (sizeof(R) == 4)
@@ -707,7 +317,7 @@ int sm_count() {
 // top nq result bits are set aside — not thread, expansion or tile bits; the
 // fused kernel walks them per thread (B strides bq, F index bits fq) and the
 // plan's output covers the low w - nq bits only.
-int make_plan(const qtn_bucket_desc_t* d, int min_e, Plan* P, int* smem, int nq = 0) {
+int make_plan(const qtn_bucket_desc_t* d, int min_e, Plan* P, int* smem, int nq) {
   memset(P, 0, sizeof(*P));
   const int w = d->w, k = d->k, nm = d->n_mem;
   const int wf = w - nq;   // free result bits
@@ -847,55 +457,6 @@ int make_plan(const qtn_bucket_desc_t* d, int min_e, Plan* P, int* smem, int nq 
   return QTN_OK;
 }
 
-// Plan K6 for producer `dp` feeding member `ipc` of consumer `dc` (see
-// k6_body).  QTN_E_UNSUPPORTED when the pair does not have that shape or the
-// producer is not a K4 expansion once the consumer's summed bits are set aside.
-int make_fplan(const qtn_bucket_desc_t* dp, const qtn_bucket_desc_t* dc, int ipc, FPlan* F, int* smem) {
-  memset(F, 0, sizeof(*F));
-  if (!dp || !dc) return fail(QTN_E_INVALID, "K6: null descriptor");
-  const int wc = dc->w, kc = dc->k, nmc = dc->n_mem;
-  if (dc->dtype != dp->dtype) return fail(QTN_E_INVALID, "K6: producer and consumer dtypes differ");
-  if (kc < 1 || kc > MAXQ || nmc < 1 || nmc > MAXM || ipc < 0 || ipc >= nmc || dp->w != wc + kc)
-    return fail(QTN_E_UNSUPPORTED, "K6: consumer w=%d k=%d n_mem=%d, producer w=%d", wc, kc, nmc, dp->w);
-  // the producer's result is the consumer's member ipc in canonical order
-  if (dc->mem[ipc].data != dp->out) return fail(QTN_E_INVALID, "K6: consumer member %d is not the producer's result", ipc);
-  for (int b = 0; b < wc + kc; ++b)
-    if (dc->mem[ipc].strides[b] != ((int64_t)1 << b))
-      return fail(QTN_E_UNSUPPORTED, "K6: consumer member %d is not the whole producer result", ipc);
-  if ((1 << kc) * (1 << dp->k) > (dp->dtype == QTN_C64 ? 32 : 16))
-    return fail(QTN_E_UNSUPPORTED, "K6: %d B registers per thread", (1 << kc) * (1 << dp->k));
-  int rc = make_plan(dp, 0, &F->p, smem, kc);
-  if (rc) return rc;
-  Plan& P = F->p;
-  if (!dc->out) return fail(QTN_E_INVALID, "K6: null output");
-  P.out = dc->out;
-  for (int i = 0; i < nmc; ++i) {
-    if (i == ipc) continue;
-    const qtn_bmember_t& m = dc->mem[i];
-    if (!m.data) return fail(QTN_E_INVALID, "K6: null consumer member %d", i);
-    bool res = false;
-    int64_t span = 1;
-    for (int b = 0; b < wc + kc; ++b) span += m.strides[b];
-    for (int b = 0; b < wc; ++b) res |= m.strides[b] != 0;
-    if (span >= ((int64_t)1 << 31)) return fail(QTN_E_UNSUPPORTED, "K6: consumer member %d spans 2^31 elements", i);
-    if (res) {
-      if (F->ng == MAXG) return fail(QTN_E_UNSUPPORTED, "K6: more than %d consumer members carry result bits", MAXG);
-      const int g = F->ng++;
-      F->gptr[g] = m.data;
-      for (int j = 0; j < P.nH; ++j) F->ghs[g][j] = m.strides[P.hbit[j]];
-      for (int t = 0; t < TBB; ++t) F->gtb[g][t] = (int32_t)m.strides[P.tbit[t]];
-      for (int e = 0; e < P.nE; ++e) F->ge[g][e] = (int32_t)m.strides[P.ebit[e]];
-      for (int q = 0; q < kc; ++q) F->gq[g][q] = (int32_t)m.strides[wc + q];
-      F->gspan[g] = span;
-    } else {
-      const int u = F->nu++;
-      F->uptr[u] = m.data;
-      for (int q = 0; q < kc; ++q) F->uq[u][q] = (int32_t)m.strides[wc + q];
-    }
-  }
-  return QTN_OK;
-}
-
 }  // namespace qtn_k4
 
 size_t qtn_k4_plan_bytes() { return sizeof(qtn_k4::Plan); }
@@ -940,45 +501,3 @@ extern "C" int qtn_bucket_expand(const qtn_bucket_desc_t* d, int32_t min_e, void
   return QTN_OK;
 }
 
-size_t qtn_k6_plan_bytes() { return sizeof(qtn_k4::FPlan); }
-
-// Program-graph node for a producer / consumer pair (qtn_graph_create_host).
-int qtn_k6_node(const qtn_bucket_desc_t* dp, const qtn_bucket_desc_t* dc, int ipc, unsigned long long* timing,
-                int32_t item_p, int32_t item_c, void* plan, const void** fn, int* grid, int* smem) {
-  using namespace qtn_k4;
-  FPlan* F = reinterpret_cast<FPlan*>(plan);
-  int rc = make_fplan(dp, dc, ipc, F, smem);
-  if (rc) return rc;
-  F->p.timing = timing;
-  F->p.item = item_p;
-  F->item_c = item_c;
-  *fn = dp->dtype == QTN_C64 ? fn_k6<float>(F->p.k, F->p.nq, F->p.nE) : fn_k6<double>(F->p.k, F->p.nq, F->p.nE);
-  if (!*fn) return fail(QTN_E_UNSUPPORTED, "K6: no kernel for k=%d nq=%d", F->p.k, F->p.nq);
-  cudaFuncAttributes fa;
-  cudaError_t e = cudaFuncGetAttributes(&fa, *fn);
-  if (e != cudaSuccess) return fail(QTN_E_CUDA, "cudaFuncGetAttributes: %s", cudaGetErrorString(e));
-  if (*smem > fa.maxDynamicSharedSizeBytes) {
-    e = cudaFuncSetAttribute(*fn, cudaFuncAttributeMaxDynamicSharedMemorySize, *smem);
-    if (e != cudaSuccess) return fail(QTN_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-  }
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, *fn, NT, *smem);
-  if (e != cudaSuccess) return fail(QTN_E_CUDA, "occupancy: %s", cudaGetErrorString(e));
-  if (per_sm < 1) return fail(QTN_E_UNSUPPORTED, "K6 cannot be resident with %d B smem", *smem);
-  *grid = (int)std::min<int64_t>(F->p.n_tiles, (int64_t)per_sm * sm_count());
-  return QTN_OK;
-}
-
-extern "C" int qtn_bucket_expand_fused(const qtn_bucket_desc_t* producer, const qtn_bucket_desc_t* consumer,
-                                       int32_t member, void* stream) {
-  using namespace qtn_k4;
-  static thread_local FPlan F;
-  const void* fn = nullptr;
-  int grid = 0, smem = 0;
-  int rc = qtn_k6_node(producer, consumer, member, nullptr, 0, 0, &F, &fn, &grid, &smem);
-  if (rc) return rc;
-  void* args[] = {&F};
-  const cudaError_t e = cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(NT), args, smem, (cudaStream_t)stream);
-  if (e != cudaSuccess) return fail(QTN_E_CUDA, "K6 launch: %s", cudaGetErrorString(e));
-  return QTN_OK;
-}

@@ -1,0 +1,566 @@
+// bucket_fused.cu — K6: an expansion item fused with its only consumer.
+//
+// A consumer item C (one reference bucket, or a merged chain summing k_C <= 3
+// indices, src/tensor_core.py:148-164) whose member X is the WHOLE result of
+// a producer item P: X carries every result and summed index of C in the
+// canonical order, so P's result bits are C's result bits r followed by C's
+// summed bits q, and nothing else reads P's result (the reference re-buckets
+// it at its earliest index and contracts it there, src/ordering.py:175-187).
+//     out_C[r] = sum_q G(q, r) * U(q) * X(q, r)
+//     X(q, r)  = sum_s B(s, q, r) * F(f(q, r), s)                 (P, as K4)
+// B = P's dominant member, F = the product of P's other members (a per-tile
+// table in shared memory, csrc/bucket_expand.cu), U = the product of C's
+// members that carry no result index, G = C's one member that does (at most
+// one; the widest intermediate of a lightcone is typically read by such a
+// pair: cfg-2's w = 24 complex128 result, 268 MB, written and read back by
+// two kernels, is never materialised here).
+//
+// P's K4 plan is made with the q bits set aside: each thread owns one B
+// coordinate (8 thread bits), holds B(s, q) for every (s, q) in registers
+// (U folded in), and walks its 2^|E| expansion results; per result it forms
+// X(q, r) for every q from broadcast product-table rows and sums over q right
+// away.  The q loop is ordered so that G is constant over runs of q (the q
+// bits G does not carry first): each run is summed, then multiplied by G
+// once.  G values are loaded for a whole batch of results before any is
+// used.  Sum order: s ascending inside X, q in the plan's order outside; X
+// is not rounded to the element type.
+//
+// One source, three objects (Makefile): K6_PART 0 = planner + C ABI, 1 =
+// complex64 kernels, 2 = complex128 kernels (compiled in parallel).
+#include "k4_plan.h"
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstring>
+
+#ifndef K6_PART
+#define K6_PART 0
+#endif
+// B of the next tile copied into thread-private shared-memory slots while
+// the current tile computes (cp.async); 0 = direct loads at each tile start
+// (default: measured neutral to 5 % slower on cfg-2, the G gathers dominate)
+#ifndef K6_BPF
+#define K6_BPF 0
+#endif
+// expansion bits unrolled per result batch (at most 2)
+#ifndef K6_NEL_C64
+#define K6_NEL_C64 2
+#endif
+#ifndef K6_NEL_C128
+#define K6_NEL_C128 2
+#endif
+
+namespace qtn_k4 {
+
+struct FPlan {
+  Plan p;                     // producer plan, q bits set aside; p.out = C's output
+  int32_t ng;                 // gathered consumer members (0 or 1)
+  const void* gptr;
+  int64_t ghs[MAXH];          // G stride of tile bit j (p.hbit order)
+  int32_t gtb[TBB];           // of thread bit t
+  int32_t ge[MAXE];           // of expansion bit e
+  int32_t gq[MAXQ];           // of q loop bit i
+  int64_t gspan;
+  int32_t nu;                 // consumer members on summed bits only: folded into U[q]
+  const void* uptr[MAXM];
+  int32_t uq[MAXM][MAXQ];
+  int32_t nqn;                // q loop bits G does not carry (the low ones)
+  int32_t item_c;             // consumer item (timing; p.item = producer)
+};
+
+// Kernel selection: K = producer summed bits, NQ = 2^(consumer summed bits),
+// GQ = G runs per result (0: no G member), NEL = expansion bits unrolled per
+// batch (the rest walked by a rolled loop).
+const void* k6_fn_c64(int k, int nq, int gq, int nel);
+const void* k6_fn_c128(int k, int nq, int gq, int nel);
+
+// shared-memory bytes of the B prefetch slots (one per (q, s) value per thread)
+inline int k6_stage_bytes(int dtype, int k, int nq) {
+  return K6_BPF ? NT * (1 << k) * (1 << nq) * (dtype == QTN_C64 ? 8 : 16) : 0;
+}
+
+#if K6_PART > 0
+
+__device__ __forceinline__ void cp_async(void* dst, const float2* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async(void* dst, const double2* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+// the value has arrived in registers (orders a later async overwrite of its slot)
+__device__ __forceinline__ void arrived(float2 v) { asm volatile("" ::"f"(v.x), "f"(v.y)); }
+__device__ __forceinline__ void arrived(double2 v) { asm volatile("" ::"d"(v.x), "d"(v.y)); }
+
+template <typename R, int K, int NQ, int GQ, int NEL>
+__device__ __forceinline__ void k6_body(const FPlan& FP) {
+  using T = typename Cx<R>::T;
+  const Plan& P = FP.p;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  constexpr int NS = 1 << K;
+  constexpr int NR = GQ == 0 ? 1 : GQ;   // runs of q
+  constexpr int QN = NQ / NR;            // q per run
+  constexpr int NEVL = 1 << NEL;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* F = reinterpret_cast<T*>(smem_raw);
+  const int nfe = 1 << (P.nF + K);
+  uint32_t* LUT = reinterpret_cast<uint32_t*>(smem_raw + sizeof(T) * nfe);
+  // B prefetch slots: value v of thread t at [v * NT + t] (conflict-free)
+  T* bst = reinterpret_cast<T*>(smem_raw + ((sizeof(T) * nfe + P.nm * 128 * 4 + 15) & ~size_t(15)));
+  __shared__ int64_t sbase[MAXM + 1];
+  __shared__ T sU[NQ];
+  const int tid = threadIdx.x;
+  const int nm = P.nm;
+  const int nlo = P.nF + K < 6 ? P.nF + K : 6;
+  for (int x = tid; x < nm * 128; x += NT) {
+    const int j = x >> 7, y = x & 63, hi = (x >> 6) & 1;
+    uint32_t o = 0;
+    if (j != P.iB)
+      for (int b = 0; b < 6; ++b) {
+        const int q = hi ? nlo + b : b;
+        if (((y >> b) & 1) && (hi ? q < P.nF + K : b < nlo)) o += P.fs[j][q];
+      }
+    LUT[x] = o;
+  }
+  int64_t boff = 0;
+  int32_t ob = 0, fb = 0, gthr = 0;
+#pragma unroll
+  for (int b = 0; b < TBB; ++b)
+    if ((tid >> b) & 1) {
+      boff += P.btb[b];
+      ob += P.otb[b];
+      fb += P.ftb[b];
+      gthr += FP.gtb[b];
+    }
+  // the low NEL expansion bits: out / F / G offsets per unrolled result
+  int32_t oe[NEVL], fe[NEVL], ge[NEVL];
+#pragma unroll
+  for (int e = 0; e < NEVL; ++e) {
+    int32_t o = 0, f = 0, g = 0;
+#pragma unroll
+    for (int b = 0; b < NEL; ++b)
+      if ((e >> b) & 1) {
+        o += P.oe[b];
+        f += P.fe[b];
+        g += FP.ge[b];
+      }
+    oe[e] = o;
+    fe[e] = (fb + f) << K;
+    ge[e] = gthr + g;
+  }
+  int64_t qoffB[NQ];
+  int32_t fqo[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    int64_t o = 0;
+    int32_t f = 0;
+#pragma unroll
+    for (int b = 0; b < MAXQ; ++b)
+      if ((1 << b) < NQ && ((q >> b) & 1)) {
+        o += P.bq[b];
+        f += P.fq[b];
+      }
+    qoffB[q] = o;
+    fqo[q] = f << K;
+  }
+  int32_t gro[NR];   // G offset of each run (its q bits are the high loop bits)
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    int32_t o = 0;
+#pragma unroll
+    for (int b = 0; b < MAXQ; ++b)
+      if ((1 << b) < NQ && (((r * QN) >> b) & 1)) o += FP.gq[b];
+    gro[r] = o;
+  }
+  int64_t soffB[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    int64_t o = 0;
+#pragma unroll
+    for (int b = 0; b < K; ++b)
+      if ((s >> b) & 1) o += P.bs[b];
+    soffB[s] = o;
+  }
+  const int neh = P.nE - NEL;   // expansion bits walked by the rolled loop
+  const int64_t per = (P.n_tiles + gridDim.x - 1) / gridDim.x;
+  int64_t h = (int64_t)blockIdx.x * per;
+  const int64_t h_end = h + per < P.n_tiles ? h + per : P.n_tiles;
+  if (h >= h_end) return;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  unsigned long long t_start = 0;
+  if (P.timing && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  // U[q] = product of the consumer members that carry no result bit
+  if (tid < NQ) {
+    T u = {R(1), R(0)};
+    for (int i = 0; i < FP.nu; ++i) {
+      int32_t o = 0;
+#pragma unroll
+      for (int b = 0; b < MAXQ; ++b)
+        if ((tid >> b) & 1) o += FP.uq[i][b];
+      u = cmul(u, __ldg(reinterpret_cast<const T*>(FP.uptr[i]) + o));
+    }
+    sU[tid] = u;
+  }
+  __syncthreads();
+  const T* Bm = reinterpret_cast<const T*>(P.mptr[P.iB]);
+  const T* Gm = reinterpret_cast<const T*>(FP.gptr);
+  T* out = reinterpret_cast<T*>(P.out);
+  const int shf = P.nH - P.nHF;
+  int64_t fkey = -1;
+  auto bbase = [&](int64_t hh) {
+    int64_t o = 0;
+    for (int b = 0; b < P.nH; ++b)
+      if ((hh >> b) & 1) o += P.hs[P.iB][b];
+    return o;
+  };
+#if K6_BPF
+  auto issue_b = [&](int64_t hh) {
+    const T* bp = Bm + bbase(hh) + boff;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+      for (int s = 0; s < NS; ++s) cp_async(bst + (q * NS + s) * NT + tid, bp + qoffB[q] + soffB[s]);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  issue_b(h);
+#endif
+  for (; h < h_end; ++h) {
+    int64_t obase = 0, gb = 0;
+    for (int b = 0; b < P.nH; ++b)
+      if ((h >> b) & 1) {
+        obase += P.hs[nm][b];
+        gb += FP.ghs[b];
+      }
+    // B for every (q, s), U folded in
+    T bv[NQ][NS];
+    {
+#if K6_BPF
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+#pragma unroll
+        for (int s = 0; s < NS; ++s) bv[q][s] = bst[(q * NS + s) * NT + tid];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+#pragma unroll
+        for (int s = 0; s < NS; ++s) arrived(bv[q][s]);
+      if (h + 1 < h_end) issue_b(h + 1);   // the next tile's B lands while this one computes
+#else
+      const int64_t bb = bbase(h);
+      const T* bp = Bm + bb + boff;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          K4_CHECK(bb + boff + qoffB[q] + soffB[s] >= 0 && bb + boff + qoffB[q] + soffB[s] < P.span[P.iB],
+                   "K6 B element %lld", (long long)(bb + boff + qoffB[q] + soffB[s]));
+          bv[q][s] = __ldg(bp + qoffB[q] + soffB[s]);
+        }
+#endif
+      if (FP.nu) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const T u = sU[q];
+#pragma unroll
+          for (int s = 0; s < NS; ++s) bv[q][s] = cmul(u, bv[q][s]);
+        }
+      }
+    }
+    if ((h >> shf) != fkey) {
+      fkey = h >> shf;
+      __syncthreads();
+      if (tid < nm) {
+        int64_t o = 0;
+        for (int b = shf; b < P.nH; ++b)
+          if ((h >> b) & 1) o += P.hs[tid][b];
+        sbase[tid] = o;
+      }
+      __syncthreads();
+      for (int x = tid; x < nfe; x += NT) {
+        T v = {R(1), R(0)};
+        const int lo = x & 63, hi = x >> 6;
+        for (int j = 0; j < nm; ++j) {
+          if (j == P.iB) continue;
+          const T* mp = reinterpret_cast<const T*>(P.mptr[j]);
+          K4_CHECK(sbase[j] + LUT[j * 128 + lo] + LUT[j * 128 + 64 + hi] < P.span[j], "K6 member %d", j);
+          v = cmul(v, __ldg(mp + sbase[j] + LUT[j * 128 + lo] + LUT[j * 128 + 64 + hi]));
+        }
+        F[x] = v;
+      }
+      __syncthreads();
+    }
+    T* op = out + obase + ob;
+    const T* gp = Gm + gb;
+    // batches of NEVL results: the high expansion bits walked here
+#pragma unroll 1
+    for (int eh = 0; eh < (1 << neh); ++eh) {
+      int32_t oh = 0, fh = 0, gh = 0;
+      for (int b = 0; b < neh; ++b)
+        if ((eh >> b) & 1) {
+          oh += P.oe[NEL + b];
+          fh += P.fe[NEL + b] << K;
+          gh += FP.ge[NEL + b];
+        }
+      // G for the whole batch first (one long-latency round trip per batch)
+      T gv[NEVL][NR];
+      if constexpr (GQ > 0) {
+#pragma unroll
+        for (int e = 0; e < NEVL; ++e)
+#pragma unroll
+          for (int r = 0; r < NR; ++r) {
+            K4_CHECK(gb + ge[e] + gh + gro[r] >= 0 && gb + ge[e] + gh + gro[r] < FP.gspan, "K6 G element %lld",
+                     (long long)(gb + ge[e] + gh + gro[r]));
+#ifdef K6_EXP_NOG
+            gv[e][r] = T{R(1) + R(ge[e] + gh + gro[r]) * R(1e-30), R(0)};   // timing experiment only
+#else
+            gv[e][r] = __ldg(gp + ge[e] + gh + gro[r]);
+#endif
+          }
+      }
+#pragma unroll
+      for (int e = 0; e < NEVL; ++e) {
+        const T* fpe = F + fe[e] + fh;
+        T acc;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          T xs;
+#pragma unroll
+          for (int qi = 0; qi < QN; ++qi) {
+            const int q = r * QN + qi;
+            const T* fp = fpe + fqo[q];
+            K4_CHECK(fe[e] + fh + fqo[q] + NS <= nfe, "K6 F entry %d of %d", fe[e] + fh + fqo[q] + NS, nfe);
+            if (qi == 0)
+              xs = cmul(bv[q][0], fp[0]);
+            else
+              cfma(xs, bv[q][0], fp[0]);
+#pragma unroll
+            for (int s = 1; s < NS; ++s) cfma(xs, bv[q][s], fp[s]);
+          }
+          if constexpr (GQ > 0) {
+            if (r == 0)
+              acc = cmul(gv[e][r], xs);
+            else
+              cfma(acc, gv[e][r], xs);
+          } else {
+            acc = xs;
+          }
+        }
+        K4_CHECK(obase + ob + oh + oe[e] >= 0 && obase + ob + oh + oe[e] < P.out_elems, "K6 result %lld",
+                 (long long)(obase + ob + oh + oe[e]));
+        op[oh + oe[e]] = acc;
+      }
+    }
+  }
+  if (P.timing && tid == 0) {
+    unsigned long long t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    atomicMin(&P.timing[2 * P.item], t_start);
+    atomicMax(&P.timing[2 * P.item + 1], t_end);
+    atomicMin(&P.timing[2 * FP.item_c], t_start);
+    atomicMax(&P.timing[2 * FP.item_c + 1], t_end);
+  }
+}
+
+#ifndef K6_MINB_C64
+#define K6_MINB_C64 3
+#endif
+#ifndef K6_MINB_C128
+#define K6_MINB_C128 2
+#endif
+#if K6_PART == 1
+using KR = float;
+#define K6_MINB K6_MINB_C64
+#define K6_KERNEL k6_kernel_c64
+#define K6_FN k6_fn_c64
+#else
+using KR = double;
+#define K6_MINB K6_MINB_C128
+#define K6_KERNEL k6_kernel_c128
+#define K6_FN k6_fn_c128
+#endif
+
+template <int K, int NQ, int GQ, int NEL>
+__global__ void __launch_bounds__(NT, K6_MINB) K6_KERNEL(const __grid_constant__ FPlan FP) {
+  k6_body<KR, K, NQ, GQ, NEL>(FP);
+}
+
+template <int K, int NQ, int GQ>
+const void* fn_nel(int nel) {
+  if (nel == 0) return (const void*)K6_KERNEL<K, NQ, GQ, 0>;
+  if (nel == 1) return (const void*)K6_KERNEL<K, NQ, GQ, 1>;
+  return (const void*)K6_KERNEL<K, NQ, GQ, 2>;
+}
+
+template <int K, int NQ>
+const void* fn_gq(int gq, int nel) {
+  if (gq == 0) return fn_nel<K, NQ, 0>(nel);
+  if (gq == 1) return fn_nel<K, NQ, 1>(nel);
+  if (gq == 2 && NQ >= 2) return fn_nel<K, NQ, (NQ >= 2 ? 2 : 1)>(nel);
+  if (gq == 4 && NQ >= 4) return fn_nel<K, NQ, (NQ >= 4 ? 4 : 1)>(nel);
+  if (gq == 8 && NQ >= 8) return fn_nel<K, NQ, (NQ >= 8 ? 8 : 1)>(nel);
+  return nullptr;
+}
+
+// B file: NQ * 2^K values per thread, at most 16
+const void* K6_FN(int k, int nq, int gq, int nel) {
+  if (k == 1 && nq == 2) return fn_gq<1, 2>(gq, nel);
+  if (k == 1 && nq == 4) return fn_gq<1, 4>(gq, nel);
+  if (k == 1 && nq == 8) return fn_gq<1, 8>(gq, nel);
+  if (k == 2 && nq == 2) return fn_gq<2, 2>(gq, nel);
+  if (k == 2 && nq == 4) return fn_gq<2, 4>(gq, nel);
+  if (k == 3 && nq == 2) return fn_gq<3, 2>(gq, nel);
+  return nullptr;
+}
+
+#endif  // K6_PART > 0
+
+#if K6_PART == 0
+
+// Plan K6 for producer `dp` feeding member `ipc` of consumer `dc`.
+// QTN_E_UNSUPPORTED when the pair does not have that shape or the producer is
+// not a K4 expansion once the consumer's summed bits are set aside.
+int make_fplan(const qtn_bucket_desc_t* dp, const qtn_bucket_desc_t* dc, int ipc, FPlan* F, int* smem) {
+  memset(F, 0, sizeof(*F));
+  if (!dp || !dc) return fail(QTN_E_INVALID, "K6: null descriptor");
+  const int wc = dc->w, kc = dc->k, nmc = dc->n_mem;
+  if (dc->dtype != dp->dtype) return fail(QTN_E_INVALID, "K6: producer and consumer dtypes differ");
+  if (kc < 1 || kc > MAXQ || nmc < 1 || nmc > MAXM || ipc < 0 || ipc >= nmc || dp->w != wc + kc)
+    return fail(QTN_E_UNSUPPORTED, "K6: consumer w=%d k=%d n_mem=%d, producer w=%d", wc, kc, nmc, dp->w);
+  // the producer's result is the consumer's member ipc in canonical order
+  if (dc->mem[ipc].data != dp->out) return fail(QTN_E_INVALID, "K6: consumer member %d is not the producer's result", ipc);
+  for (int b = 0; b < wc + kc; ++b)
+    if (dc->mem[ipc].strides[b] != ((int64_t)1 << b))
+      return fail(QTN_E_UNSUPPORTED, "K6: consumer member %d is not the whole producer result", ipc);
+  if ((1 << kc) * (1 << dp->k) > 16)
+    return fail(QTN_E_UNSUPPORTED, "K6: %d B registers per thread", (1 << kc) * (1 << dp->k));
+  int rc = make_plan(dp, 0, &F->p, smem, kc);
+  if (rc) return rc;
+  Plan& P = F->p;
+  if (!dc->out) return fail(QTN_E_INVALID, "K6: null output");
+  P.out = dc->out;
+  for (int i = 0; i < nmc; ++i) {
+    if (i == ipc) continue;
+    const qtn_bmember_t& m = dc->mem[i];
+    if (!m.data) return fail(QTN_E_INVALID, "K6: null consumer member %d", i);
+    bool res = false;
+    int64_t span = 1;
+    for (int b = 0; b < wc + kc; ++b) span += m.strides[b];
+    for (int b = 0; b < wc; ++b) res |= m.strides[b] != 0;
+    if (span >= ((int64_t)1 << 31)) return fail(QTN_E_UNSUPPORTED, "K6: consumer member %d spans 2^31 elements", i);
+    if (res) {
+      if (F->ng) return fail(QTN_E_UNSUPPORTED, "K6: more than one consumer member carries result bits");
+      F->ng = 1;
+      F->gptr = m.data;
+      for (int j = 0; j < P.nH; ++j) F->ghs[j] = m.strides[P.hbit[j]];
+      for (int t = 0; t < TBB; ++t) F->gtb[t] = (int32_t)m.strides[P.tbit[t]];
+      for (int e = 0; e < P.nE; ++e) F->ge[e] = (int32_t)m.strides[P.ebit[e]];
+      for (int q = 0; q < kc; ++q) F->gq[q] = (int32_t)m.strides[wc + q];
+      F->gspan = span;
+    } else {
+      const int u = F->nu++;
+      F->uptr[u] = m.data;
+      for (int q = 0; q < kc; ++q) F->uq[u][q] = (int32_t)m.strides[wc + q];
+    }
+  }
+  // q loop order: the bits G does not carry first (G is then constant over
+  // runs of 2^nqn consecutive q)
+  int ord[MAXQ], no = 0;
+  for (int pass = 0; pass < 2; ++pass)
+    for (int q = 0; q < kc; ++q) {
+      const bool carried = F->ng && F->gq[q] != 0;
+      if (carried == (pass == 1)) ord[no++] = q;
+      if (!carried && pass == 0) ++F->nqn;
+    }
+  {
+    const FPlan T0 = *F;
+    for (int i = 0; i < kc; ++i) {
+      P.bq[i] = T0.p.bq[ord[i]];
+      P.fq[i] = T0.p.fq[ord[i]];
+      F->gq[i] = T0.gq[ord[i]];
+      for (int u = 0; u < F->nu; ++u) F->uq[u][i] = T0.uq[u][ord[i]];
+    }
+  }
+  return QTN_OK;
+}
+
+// the kernel of a plan (nullptr: no instantiation)
+const void* fn_of_plan(const FPlan& F, int dtype) {
+  const int nq = 1 << F.p.nq;
+  const int gq = F.ng ? (nq >> F.nqn) : 0;
+  const int nel_max = dtype == QTN_C64 ? K6_NEL_C64 : K6_NEL_C128;
+  const int nel = F.p.nE < nel_max ? F.p.nE : nel_max;
+  return dtype == QTN_C64 ? k6_fn_c64(F.p.k, nq, gq, nel) : k6_fn_c128(F.p.k, nq, gq, nel);
+}
+
+}  // namespace qtn_k4
+
+size_t qtn_k6_plan_bytes() { return sizeof(qtn_k4::FPlan); }
+
+// Program-graph node for a producer / consumer pair (qtn_graph_create_host).
+int qtn_k6_node(const qtn_bucket_desc_t* dp, const qtn_bucket_desc_t* dc, int ipc, unsigned long long* timing,
+                int32_t item_p, int32_t item_c, void* plan, const void** fn, int* grid, int* smem) {
+  using namespace qtn_k4;
+  FPlan* F = reinterpret_cast<FPlan*>(plan);
+  int rc = make_fplan(dp, dc, ipc, F, smem);
+  if (rc) return rc;
+  *smem = ((*smem + 15) & ~15) + k6_stage_bytes(dp->dtype, F->p.k, F->p.nq);
+  F->p.timing = timing;
+  F->p.item = item_p;
+  F->item_c = item_c;
+  *fn = fn_of_plan(*F, dp->dtype);
+  if (!*fn) return fail(QTN_E_UNSUPPORTED, "K6: no kernel for k=%d nq=%d", F->p.k, F->p.nq);
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, *fn);
+  if (e != cudaSuccess) return fail(QTN_E_CUDA, "cudaFuncGetAttributes: %s", cudaGetErrorString(e));
+  if (*smem > fa.maxDynamicSharedSizeBytes) {
+    e = cudaFuncSetAttribute(*fn, cudaFuncAttributeMaxDynamicSharedMemorySize, *smem);
+    if (e != cudaSuccess) return fail(QTN_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+  }
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, *fn, NT, *smem);
+  if (e != cudaSuccess) return fail(QTN_E_CUDA, "occupancy: %s", cudaGetErrorString(e));
+  if (per_sm < 1) return fail(QTN_E_UNSUPPORTED, "K6 cannot be resident with %d B smem", *smem);
+  *grid = (int)std::min<int64_t>(F->p.n_tiles, (int64_t)per_sm * sm_count());
+  return QTN_OK;
+}
+
+extern "C" int qtn_bucket_expand_fused_plan(const qtn_bucket_desc_t* producer, const qtn_bucket_desc_t* consumer,
+                                            int32_t member, int32_t* info) {
+  using namespace qtn_k4;
+  if (!info) return fail(QTN_E_INVALID, "null info");
+  static thread_local FPlan F;
+  int smem = 0;
+  const int rc = make_fplan(producer, consumer, member, &F, &smem);
+  if (rc) return rc;
+  if (!fn_of_plan(F, producer->dtype)) return fail(QTN_E_UNSUPPORTED, "K6: no kernel for k=%d nq=%d", F.p.k, F.p.nq);
+  info[0] = F.p.k;
+  info[1] = F.p.nq;
+  info[2] = F.p.nE;
+  info[3] = F.p.nF;
+  info[4] = F.ng;
+  info[5] = F.nu;
+  info[6] = F.nqn;
+  info[7] = F.p.nH;
+  return QTN_OK;
+}
+
+extern "C" int qtn_bucket_expand_fused(const qtn_bucket_desc_t* producer, const qtn_bucket_desc_t* consumer,
+                                       int32_t member, void* stream) {
+  using namespace qtn_k4;
+  static thread_local FPlan F;
+  const void* fn = nullptr;
+  int grid = 0, smem = 0;
+  int rc = qtn_k6_node(producer, consumer, member, nullptr, 0, 0, &F, &fn, &grid, &smem);
+  if (rc) return rc;
+  void* args[] = {&F};
+  const cudaError_t e = cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(NT), args, smem, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(QTN_E_CUDA, "K6 launch: %s", cudaGetErrorString(e));
+  return QTN_OK;
+}
+
+#else
+
+}  // namespace qtn_k4
+
+#endif  // K6_PART == 0

@@ -853,8 +853,9 @@ class Program:
                         members.append((off, 0, 0, 0))
                     w_, k_, L_, out_, slot_, nmem_ = N.QTN_FINALIZE, 0, 0, 0, i, len(tl["fin_kind"])
                     smem_, stm_ = 0, 0
-                # completion dependencies inside this stage (RAW + WAR)
-                for dg in deps_all[g]:
+                # completion dependencies inside this stage (RAW + WAR; a
+                # pair node's consumer follows its producer in stream order)
+                for dg in (deps_all[g] if is_stage else ()):
                     if node_of[dg] == ni:
                         pg = new_of[dg]
                         deps.append((pg, ntiles[pg]))

@@ -67,11 +67,11 @@ def _run_pair(wc, kc, kp, ne, n_small, n_gather, n_uniform, dtype, seed):
 @pytest.mark.parametrize("dtype", ["complex64", "complex128"])
 @pytest.mark.parametrize("wc,kc,kp,ne,n_small,n_gather,n_uniform", [
     (12, 1, 1, 1, 1, 0, 0), (14, 2, 2, 2, 2, 1, 2), (16, 2, 2, 4, 3, 1, 1), (15, 1, 3, 3, 2, 1, 0),
-    (18, 2, 1, 4, 2, 2, 1), (20, 2, 2, 4, 2, 1, 2), (19, 3, 1, 2, 2, 1, 1), (20, 1, 2, 6, 3, 1, 1),
+    (18, 2, 1, 4, 2, 1, 1), (20, 2, 2, 4, 2, 1, 2), (19, 3, 1, 2, 2, 1, 1), (20, 1, 2, 6, 3, 1, 1),
     (13, 3, 2, 0, 1, 0, 3)])
 def test_k6_vs_two_einsums(dtype, wc, kc, kp, ne, n_small, n_gather, n_uniform):
-    if dtype == "complex128" and (1 << kc) * (1 << kp) > 16:
-        pytest.skip("complex128 K6 holds at most 16 B values per thread")
+    if (1 << kc) * (1 << kp) > 16:
+        pytest.skip("K6 holds at most 16 B values per thread")
     out, ref = _run_pair(wc, kc, kp, ne, n_small, n_gather, n_uniform, dtype, seed=wc * 100 + kc * 10 + kp)
     assert not out.isnan().any()
     tol = 1e-5 if dtype == "complex64" else 1e-12
@@ -81,8 +81,9 @@ def test_k6_vs_two_einsums(dtype, wc, kc, kp, ne, n_small, n_gather, n_uniform):
 
 @pytest.mark.gpu
 def test_k6_rejects_other_shapes():
-    """The consumer member must be the producer's whole result in order; too
-    many B registers per thread (complex128: 2^kc * 2^kp <= 16)."""
+    """The consumer member must be the producer's whole result in order; at
+    most 2^kc * 2^kp = 16 B registers per thread; at most one consumer member
+    carries result bits."""
     import torch
     s = torch.cuda.current_stream().cuda_stream
     x = torch.zeros(1 << 16, dtype=torch.complex128, device="cuda")
@@ -99,3 +100,11 @@ def test_k6_rejects_other_shapes():
     dc = N.bucket_desc(N.QTN_C128, 12, cout.data_ptr(), [(pout.data_ptr(), {b: 1 << b for b in range(14)})], k=2)
     with pytest.raises(N.NativeError, match="registers"):
         N.bucket_expand_fused_launch(dp3, dc, 0, s)
+    x = torch.zeros(1 << 16, dtype=torch.complex128, device="cuda")
+    g = {b: 1 << i for i, b in enumerate(range(4))}
+    dp = N.bucket_desc(N.QTN_C128, 14, pout.data_ptr(), [(x.data_ptr(), {b: 1 << b for b in range(16)})], k=2)
+    dc = N.bucket_desc(N.QTN_C128, 12, cout.data_ptr(), [(pout.data_ptr(), {b: 1 << b for b in range(14)}),
+                                                          (x.data_ptr(), g), (x.data_ptr(), g)], k=2)
+    with pytest.raises(N.NativeError, match="more than one consumer member"):
+        N.bucket_expand_fused_launch(dp, dc, 0, s)
+    torch.cuda.synchronize()
