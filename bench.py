@@ -403,7 +403,7 @@ def dominant_kernel(lcp, stream, flush, reps=50):
     fam = ext.node_kernels(io=False)
     items = [{"item": int(g), "w": int(prog.buckets[g]["w"]), "k": int(prog.buckets[g]["k"]),
               "kernel": fam[node_of[g]], "live_us": round(float(acc[g]) / 1e3, 1),
-              "bytes_MB": round(prog.item_bytes(g) / 1e6, 1)} for g in top]
+              "node_bytes_MB": round(lcp.ex.node_bytes(node_of[g]) / 1e6, 1)} for g in top]
     del ext
     g = top[0]
     gr, fam0 = lcp.ex.node_graph(node_of[g])
@@ -421,9 +421,11 @@ def dominant_kernel(lcp, stream, flush, reps=50):
     torch.cuda.synchronize()
     dur = sum(a.elapsed_time(b) for a, b in ts) / reps / 1e3
     b = prog.buckets[g]
+    nd = prog.nodes[node_of[g]]
     key = f"{lcp.dtype}:{fam0}:w{int(b['w'])}k{int(b['k'])}"
     return {"item": int(g), "kernel": fam0, "key": key, "w": int(b["w"]), "k": int(b["k"]),
-            "bytes": prog.item_bytes(g), "us": dur * 1e6, "top_items_live": items}
+            "items": list(range(int(nd["first"]), int(nd["first"]) + int(nd["count"]))),
+            "bytes": lcp.ex.node_bytes(node_of[g]), "us": dur * 1e6, "top_items_live": items}
 
 
 def sustained_clocks(lcp, stream, flush, seconds, local):
@@ -495,7 +497,7 @@ def run_ours(args):
     peak, peak_src = peak_hbm()
     prog = progs[hd].prog
     ms = 1e3 * t_dev / args.steps
-    alg, exe = prog.algorithmic_bytes(), prog.executed_bytes()
+    alg, exe = prog.algorithmic_bytes(), progs[hd].ex.executed_bytes()
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         dt, v_cpu = cpu_oracle_time(lc, order, args.cpu_sample)
@@ -531,9 +533,10 @@ def run_ours(args):
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": (traffic or {}).get("dram_bytes"), "peak_source": peak_src,
-            "kernel": f"{dom['kernel']} on item {dom['item']} (w={dom['w']}, k={dom['k']}), timed alone with CUDA "
-                      f"events ({dom['us']:.1f} us per launch); achieved = compulsory bytes (members once + result "
-                      f"once = {dom['bytes']}) / launch duration",
+            "kernel": f"{dom['kernel']} on item(s) {dom['items']} (w={dom['w']}, k={dom['k']}), node timed alone with "
+                      f"CUDA events ({dom['us']:.1f} us per launch); achieved = compulsory bytes (members once + "
+                      f"result once{'; a K6 pair neither writes nor reads its producer result' if dom['kernel'] == 'K6' else ''}"
+                      f" = {dom['bytes']}) / launch duration",
             "dominant_share_of_step": dom["us"] / 1e3 / ms,
             "traffic_source": (traffic or {}).get("source"),
             "step": {"executed_GBps": exe / (ms / 1e3) / 1e9, "frac_executed": exe / (ms / 1e3) / 1e9 / peak,
@@ -549,8 +552,9 @@ def run_ours(args):
                 "call": "paper_2210_15874_b200.contract_network(tn_k, order, Backend.b200(...)) from host Tensors, "
                         "tn_k = the lightcone at QaoaParams.seeded(4, 1 + k % 8): new gate tensors every step",
                 "h2d_note": f"input image per step ({'complex128 + complex64 copies' if hd == 'complex64' else 'complex128'})"},
-        "gpu_launches": args.steps * prog.n_nodes,
-        "gpu_launches_note": f"{prog.n_nodes} kernels per step, issued as one CUDA graph launch",
+        "gpu_launches": args.steps * sum(progs[hd].ex.kernel_mix(io=False).values()),
+        "gpu_launches_note": f"{sum(progs[hd].ex.kernel_mix(io=False).values())} kernels per step "
+                             f"({prog.n_nodes} graph nodes), issued as one CUDA graph launch",
         "clocks": clocks,
         "clocks_sustained": sustained,
         "strong": strong,

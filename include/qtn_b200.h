@@ -130,11 +130,13 @@ typedef struct {
   unsigned long long* timing;   /* optional: 2 per bucket (first start, last end, ns) */
   int64_t arena_elems;          /* arena size in elements (bounds checks of the
                                    QTN_DEBUG build; 0 = unchecked)             */
-  /* complex64 programs: the input region [0, n_in_elems) of the arena also
-   * as complex128 (the gate tensors before narrowing).  K2 stages compute in
-   * double precision and read input members from here, so the gates enter
-   * the contraction unrounded; only intermediates are stored as complex64.
-   * NULL / 0 = inputs as stored in the arena (complex128 programs). */
+  /* n_in_elems: the arena's input region [0, n_in_elems) (gate tensors).
+   * complex64 programs: inputs_hi holds the
+   * same region as complex128 (the gates before narrowing) — K2 stages
+   * compute in double precision and stage small input members from here in
+   * shared memory before an item waits for its producers, so the
+   * gates enter the contraction unrounded; only intermediates are stored as
+   * complex64.  inputs_hi NULL (complex128 programs): no staging. */
   const void* inputs_hi;
   int64_t n_in_elems;
 } qtn_program_t;

@@ -317,7 +317,7 @@ int sm_count() {
 // top nq result bits are set aside — not thread, expansion or tile bits; the
 // fused kernel walks them per thread (B strides bq, F index bits fq) and the
 // plan's output covers the low w - nq bits only.
-int make_plan(const qtn_bucket_desc_t* d, int min_e, Plan* P, int* smem, int nq) {
+int make_plan(const qtn_bucket_desc_t* d, int min_e, Plan* P, int* smem, int nq, int ne_max) {
   memset(P, 0, sizeof(*P));
   const int w = d->w, k = d->k, nm = d->n_mem;
   const int wf = w - nq;   // free result bits
@@ -338,16 +338,18 @@ int make_plan(const qtn_bucket_desc_t* d, int min_e, Plan* P, int* smem, int nq)
   for (int b = 0; b < w; ++b)
     for (int i = 0; i < nm; ++i)
       if (i != iB && d->mem[i].strides[b] != 0) carried[b] = true;
+  int ne_all = 0;   // B-lacking result bits; the lowest ne_max are expansion bits, the rest tile bits
   for (int b = 0; b < wf; ++b)
     if (B.strides[b] == 0) {
-      if (ne == MAXE) return fail(QTN_E_UNSUPPORTED, "K4: more than %d expansion bits", MAXE);
-      eb[ne++] = b;
+      if (ne_all == MAXE) return fail(QTN_E_UNSUPPORTED, "K4: more than %d expansion bits", MAXE);
+      ++ne_all;
+      if (ne < ne_max) eb[ne++] = b;
     }
   if (wf - ne < TBB) return fail(QTN_E_UNSUPPORTED, "K4: dominant member has %d result bits", best);
   // more than 4 expansion bits (two mid-size members, an outer-product-like
   // expansion): only for wide items — the 45-cone energy's w 22-26 items run
   // 3-5x faster here than in K1, a w = 16 item ran slower (cfg-2: 4 -> 10 us)
-  if (ne > 4 && w < K4_WIDE_E_MIN_W)
+  if (ne_all > 4 && w < K4_WIDE_E_MIN_W)
     return fail(QTN_E_UNSUPPORTED, "K4: %d expansion bits at width %d", ne, w);
   // Thread bits.  Lanes (the first 5): B's fastest axes first — one 32-byte
   // sector of B per lane group (2 complex128 / 4 complex64 elements) — then
@@ -366,7 +368,7 @@ int make_plan(const qtn_bucket_desc_t* d, int min_e, Plan* P, int* smem, int nq)
     for (int b = 0; b < wf && nt < TBB; ++b)
       if (B.strides[b] != 0 && !used[b]) take(b);
   }
-  if (ne < min_e) return fail(QTN_E_UNSUPPORTED, "K4: %d expansion bits", ne);
+  if (ne_all < min_e) return fail(QTN_E_UNSUPPORTED, "K4: %d expansion bits", ne_all);
   // replica bit: the first remaining B bit no other member carries (each
   // thread then owns two B coordinates sharing every product-table row —
   // half the shared-memory row reads).  Measured on cfg-2: complex128 all

@@ -42,6 +42,21 @@
 #ifndef K6_BPF
 #define K6_BPF 0
 #endif
+// L1 prefetch of the next result batch's G lines (K6_GPF: cfg-2 w24 pair
+// c128 79.9 -> 75.8 us, c64 57.4 -> 55.3 us) / L2 prefetch of the next
+// tile's B lines (K6_BPF2: neutral, off)
+#ifndef K6_GPF
+#define K6_GPF 1
+#endif
+#ifndef K6_BPF2
+#define K6_BPF2 0
+#endif
+// expansion bits walked per thread (the producer's other B-lacking bits
+// become tile bits: more, smaller tiles balance the persistent grid; 3 and
+// 8 measured within 5 % on cfg-2, 2 slower)
+#ifndef K6_NE_MAX
+#define K6_NE_MAX 8
+#endif
 // expansion bits unrolled per result batch (at most 2)
 #ifndef K6_NEL_C64
 #define K6_NEL_C64 2
@@ -89,6 +104,8 @@ __device__ __forceinline__ void cp_async(void* dst, const double2* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
                : "memory");
 }
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 // the value has arrived in registers (orders a later async overwrite of its slot)
 __device__ __forceinline__ void arrived(float2 v) { asm volatile("" ::"f"(v.x), "f"(v.y)); }
 __device__ __forceinline__ void arrived(double2 v) { asm volatile("" ::"d"(v.x), "d"(v.y)); }
@@ -107,9 +124,11 @@ __device__ __forceinline__ void k6_body(const FPlan& FP) {
   const int nfe = 1 << (P.nF + K);
   uint32_t* LUT = reinterpret_cast<uint32_t*>(smem_raw + sizeof(T) * nfe);
   // B prefetch slots: value v of thread t at [v * NT + t] (conflict-free)
-  T* bst = reinterpret_cast<T*>(smem_raw + ((sizeof(T) * nfe + P.nm * 128 * 4 + 15) & ~size_t(15)));
+  [[maybe_unused]] T* bst = reinterpret_cast<T*>(smem_raw + ((sizeof(T) * nfe + P.nm * 128 * 4 + 15) & ~size_t(15)));
   __shared__ int64_t sbase[MAXM + 1];
   __shared__ T sU[NQ];
+  // out / F / G offsets of every batch of the rolled expansion bits
+  __shared__ int4 sEH[1 << (MAXE - 1)];
   const int tid = threadIdx.x;
   const int nm = P.nm;
   const int nlo = P.nF + K < 6 ? P.nF + K : 6;
@@ -183,9 +202,19 @@ __device__ __forceinline__ void k6_body(const FPlan& FP) {
     soffB[s] = o;
   }
   const int neh = P.nE - NEL;   // expansion bits walked by the rolled loop
-  const int64_t per = (P.n_tiles + gridDim.x - 1) / gridDim.x;
-  int64_t h = (int64_t)blockIdx.x * per;
-  const int64_t h_end = h + per < P.n_tiles ? h + per : P.n_tiles;
+  for (int eh = tid; eh < (1 << neh); eh += NT) {
+    int32_t oh = 0, fh = 0, gh = 0;
+    for (int b = 0; b < neh; ++b)
+      if ((eh >> b) & 1) {
+        oh += P.oe[NEL + b];
+        fh += P.fe[NEL + b] << K;
+        gh += FP.ge[NEL + b];
+      }
+    sEH[eh] = make_int4(oh, fh, gh, 0);
+  }
+  // balanced contiguous runs of tile ids (every block gets floor or ceil)
+  int64_t h = (int64_t)blockIdx.x * P.n_tiles / gridDim.x;
+  const int64_t h_end = ((int64_t)blockIdx.x + 1) * P.n_tiles / gridDim.x;
   if (h >= h_end) return;
   asm volatile("griddepcontrol.wait;" ::: "memory");
   unsigned long long t_start = 0;
@@ -234,6 +263,15 @@ __device__ __forceinline__ void k6_body(const FPlan& FP) {
       }
     // B for every (q, s), U folded in
     T bv[NQ][NS];
+#if K6_BPF2
+    if (h + 1 < h_end) {   // the next tile's B lines into L2 while this tile computes
+      const T* bpn = Bm + bbase(h + 1) + boff;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+#pragma unroll
+        for (int s = 0; s < NS; ++s) prefetch_l2(bpn + qoffB[q] + soffB[s]);
+    }
+#endif
     {
 #if K6_BPF
       asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -295,15 +333,22 @@ __device__ __forceinline__ void k6_body(const FPlan& FP) {
     // batches of NEVL results: the high expansion bits walked here
 #pragma unroll 1
     for (int eh = 0; eh < (1 << neh); ++eh) {
-      int32_t oh = 0, fh = 0, gh = 0;
-      for (int b = 0; b < neh; ++b)
-        if ((eh >> b) & 1) {
-          oh += P.oe[NEL + b];
-          fh += P.fe[NEL + b] << K;
-          gh += FP.ge[NEL + b];
-        }
-      // G for the whole batch first (one long-latency round trip per batch)
+      const int4 ehv = sEH[eh];
+      const int32_t oh = ehv.x, fh = ehv.y, gh = ehv.z;
+      // G for the whole batch first (one long-latency round trip per batch);
+      // the next batch's lines are prefetched into L1 meanwhile
       T gv[NEVL][NR];
+#if K6_GPF
+      if constexpr (GQ > 0) {
+        if (eh + 1 < (1 << neh)) {
+          const int32_t ghn = sEH[eh + 1].z;
+#pragma unroll
+          for (int e = 0; e < NEVL; ++e)
+#pragma unroll
+            for (int r = 0; r < NR; ++r) prefetch_l1(gp + ge[e] + ghn + gro[r]);
+        }
+      }
+#endif
       if constexpr (GQ > 0) {
 #pragma unroll
         for (int e = 0; e < NEVL; ++e)
@@ -434,7 +479,7 @@ int make_fplan(const qtn_bucket_desc_t* dp, const qtn_bucket_desc_t* dc, int ipc
       return fail(QTN_E_UNSUPPORTED, "K6: consumer member %d is not the whole producer result", ipc);
   if ((1 << kc) * (1 << dp->k) > 16)
     return fail(QTN_E_UNSUPPORTED, "K6: %d B registers per thread", (1 << kc) * (1 << dp->k));
-  int rc = make_plan(dp, 0, &F->p, smem, kc);
+  int rc = make_plan(dp, 0, &F->p, smem, kc, K6_NE_MAX);
   if (rc) return rc;
   Plan& P = F->p;
   if (!dc->out) return fail(QTN_E_INVALID, "K6: null output");

@@ -242,7 +242,10 @@ template <typename R>
 __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_t first, int32_t count,
                                                    int32_t n_tickets, uint32_t* ctl) {
   using T = typename Cx<R>::T;
-  // complex64 programs may carry unrounded inputs (P.inputs_hi)
+  // complex64 programs may carry unrounded inputs (P.inputs_hi), staged in
+  // shared memory as complex128 before the item waits for its producers
+  // (complex128 programs read their inputs in the compute loop: staging them
+  // too measured 12 % slower on cfg-2)
   constexpr bool HI = Cx<R>::VEC == 2;
   // K2 computes in double at both element types: products and the in-order
   // sum over assignments are rounded once, when the result is stored; input
@@ -409,6 +412,7 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
           // of complex64 programs: the narrowed copy, replaced at multiply
           // time by the unrounded value staged in shi / read from inputs_hi)
           T x[MAXM][UJ];
+          int xe[MAXM][UJ];   // staged input member: element index into shi
 #pragma unroll
           for (int i = 0; i < MAXM; ++i) {
             if (i < nm) {
@@ -418,9 +422,7 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
                                    (S.pclo[i] == L ? (uint64_t)ue[j] : (uint64_t)pext32((uint32_t)ue[j], S.mlo[i]));
                 QTN_CHECK(QTN_ARENA_OK(P, o), "small item %d member %d off %lld", cur, i, (long long)o);
                 if (HI && ((hbits >> i) & 1u)) {
-                  // staged input member: its element index rides in the x
-                  // slot; the unrounded value replaces it at multiply time
-                  x[i][j].x = __int_as_float((int)(o - S.off[i]));
+                  xe[i][j] = (int)(o - S.off[i]);
                 } else {
                   x[i][j] = __ldcg(A + o);
                 }
@@ -435,7 +437,7 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
               if (i < nm) {
                 D xi;
                 if (HI && ((hbits >> i) & 1u)) {
-                  const int e = __float_as_int(x[i][j].x);
+                  const int e = xe[i][j];
                   QTN_CHECK(e >= 0 && e < K2_HI_SLOT, "hi member %d index %d", i, e);
                   xi = shi[i * K2_HI_SLOT + e];
                 } else {

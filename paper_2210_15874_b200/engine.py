@@ -1063,7 +1063,7 @@ class Executor:
             c.timing = self.timing.data_ptr() if timing else None
             c.arena_elems = prog.arena_elems
             c.inputs_hi = self.buf.data_ptr() if prog.hi_elems else None
-            c.n_in_elems = n_in if prog.hi_elems else 0
+            c.n_in_elems = n_in   # input region (K2 stages stage small input members from it)
             self.c = c
             self.done = torch.cuda.Event()
         self._graph = None
@@ -1099,6 +1099,28 @@ class Executor:
         c = (ctypes.c_int32 * max(n, 1))()
         N.check(N.load().qtn_graph_node_kinds(g, c, n))
         return [N.KERNEL_FAMILIES[c[i]] for i in range(n)]
+
+    def node_bytes(self, ni) -> int:
+        """Compulsory bytes of graph node `ni` as it runs: each member read
+        once, each result written once — a K6 pair moves neither its
+        producer's result nor the consumer's read of it."""
+        prog = self.prog
+        nd = prog.nodes[ni]
+        first, count = int(nd["first"]), int(nd["count"])
+        tot = sum(prog.item_bytes(g) for g in range(first, first + count))
+        if count == 2 and int(nd["kind"]) == N.QTN_NODE_LARGE and self.node_kernels()[ni] == "K6":
+            tot -= 2 * (1 << int(prog.buckets[first]["w"])) * ELEM_BYTES[prog.dtype]
+        return tot
+
+    def executed_bytes(self) -> int:
+        """Bytes the program's kernels must move (engine.executed_bytes of the
+        templates, less the producer results K6 pairs keep on chip)."""
+        tot = self.prog.executed_bytes()
+        fam = self.node_kernels()
+        for ni, nd in enumerate(self.prog.nodes):
+            if int(nd["count"]) == 2 and int(nd["kind"]) == N.QTN_NODE_LARGE and fam[ni] == "K6":
+                tot -= 2 * (1 << int(self.prog.buckets[int(nd["first"])]["w"])) * ELEM_BYTES[self.prog.dtype]
+        return tot
 
     def node_graph(self, ni):
         """A graph of node `ni` alone (no dependencies; the same kernel and
