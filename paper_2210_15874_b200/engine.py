@@ -757,7 +757,7 @@ class Program:
             return b < 0 or tls[i]["variant"][b] == VARIANT_SMALL
 
         # producer / consumer pairs (one node, K6 in the graph builder)
-        self.fused = self._pairs(keys, tls, order_gid, prods, deps_all, is_small) if FUSE_PAIRS else {}
+        self.fused = self._pairs(keys, tls, order_gid, prods, deps_all, war, is_small) if FUSE_PAIRS else {}
         fused_c = {c: p_ for p_, c in self.fused.items()}
         node_of = [-1] * len(keys)
         nodes = []           # dict(kind, items, deps:set)
@@ -894,12 +894,14 @@ class Program:
         self.img_src_parts = src
 
     @staticmethod
-    def _pairs(keys, tls, order_gid, prods, deps_all, is_small):
+    def _pairs(keys, tls, order_gid, prods, deps_all, war, is_small):
         """Producer -> consumer pairs for K6 (csrc/bucket_expand.cu): the
         consumer C is a large item reading the producer P's whole result as a
         member that carries every result and summed index of C (P.w = C.w +
         C.k, C.k <= 3), P is a large item with k <= 3 read by C alone, and no
-        other item waits for P (no write-after-read edge on P's inputs).  The
+        other item waits for P (no write-after-read edge on P's inputs), and
+        C's result does not reuse memory P reads (K6 reads P's members while
+        it writes C's result: a reused block would be overwritten in flight).  The
         pair becomes one node; the graph builder runs it as one K6 kernel when
         P is a K4 expansion with C's summed bits set aside (else as two
         kernels).  A producer is never itself a consumer of another pair."""
@@ -928,7 +930,7 @@ class Program:
                 p_ = order_gid[(i, pb)]
                 if p_ in used or is_small(keys[p_]) or not 1 <= tl["k"][pb] <= 3 or tl["w"][pb] != w + k:
                     continue
-                if readers.get(p_, 0) != 1 or dependents.get(p_, set()) != {g}:
+                if readers.get(p_, 0) != 1 or dependents.get(p_, set()) != {g} or p_ in war[g]:
                     continue
                 pairs[p_] = g
                 used |= {p_, g}

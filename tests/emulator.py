@@ -24,6 +24,20 @@ def pext_vec(r, mask):
     return out
 
 
+def pair_overlaps(prog, nd):
+    """A K6 pair node reads both items' members while it writes the
+    consumer's result: True when that result overlaps any of them."""
+    B = prog.buckets
+    bc = B[int(nd["first"]) + 1]
+    lo, hi = int(bc["out_off"]), int(bc["out_off"]) + (1 << int(bc["w"]))
+    for g in (int(nd["first"]), int(nd["first"]) + 1):
+        for m in prog.members[B[g]["mem_begin"]: B[g]["mem_begin"] + B[g]["n_mem"]]:
+            n = 1 << (bin(int(m["mask"])).count("1") + bin(int(m["smask"])).count("1"))
+            if not (int(m["off"]) + n <= lo or int(m["off"]) >= hi):
+                return True
+    return False
+
+
 def run_program(prog, raw_parts):
     A = np.zeros(prog.arena_elems, np.complex128)
     srcs = [raw[s] for raw, s in zip(raw_parts, prog.img_src_parts)]
@@ -42,6 +56,8 @@ def run_program(prog, raw_parts):
             assert int(d) in node_done and int(d) < ni, "graph dependency not earlier"
         items = range(int(nd["first"]), int(nd["first"]) + int(nd["count"]))
         small = nd["kind"] == N.QTN_NODE_SMALL
+        if not small and int(nd["count"]) == 2:
+            assert not pair_overlaps(prog, nd), "pair result overlaps a member"
         if small:
             items = sorted(items, key=lambda g: int(B[g]["tick_begin"]))
         for g in items:

@@ -500,3 +500,45 @@ def test_producer_consumer_pairs_cfg2(dtype):
         ref, _ = O.contract_network(ts, order)
         val = run_program(prog, [np.concatenate([np.asarray(x.data).ravel() for x in lc.network.tensors])])[0]
         assert abs(val - ref) <= 1e-12 * abs(ref)
+
+
+def test_pairs_with_memory_reuse(monkeypatch):
+    """With liveness reuse a consumer's result may take a block its producer
+    read; such a pair cannot run as one K6 kernel (the emulator asserts no
+    pair result overlaps a member), and the values stay exact."""
+    monkeypatch.setattr(E, "REUSE_MIN_ELEMS", 1)
+    g, graph, params = _cfg("cfg2")
+    c = Q.qaoa_maxcut_circuit(graph, params)
+    lc = Q.extract_lightcone(c, (0, 11), cone="tight")
+    order = Q.greedy_order(lc.network)
+    t = E.plan_template([x.indices for x in lc.network.tensors], order, "complex128", wave_aware=True)
+    prog = E.Program([E.Instance(t), E.Instance(t)], "complex128", reuse_above=0)
+    assert prog.reuse
+    raw = np.concatenate([np.asarray(x.data).ravel() for x in lc.network.tensors])
+    ref, _ = O.contract_network([(x.indices, x.data) for x in lc.network.tensors], order)
+    for v in run_program(prog, [raw, raw]):
+        assert abs(v - ref) <= 1e-12 * abs(ref)
+
+
+def test_cfg4_pairs_never_overwrite_their_inputs():
+    """cfg-4 (N=200 p=5 tight cones sliced to 32) batched under a 125 GB
+    budget: liveness reuse is on and thousands of producer/consumer pairs
+    form; no pair's consumer result may take a block its producer reads
+    (K6 writes one while reading the other — the race that made cfg-4
+    energies run-dependent before the planner excluded such pairs)."""
+    from emulator import pair_overlaps
+    from paper_2210_15874_b200 import distributed as D
+    g = Q.random_regular_graph(200, 3, seed=0)
+    c = Q.qaoa_maxcut_circuit(g, Q.QaoaParams.seeded(5, 0))
+    be = Q.Backend.b200(dtype="complex64")
+    cones = [Q.extract_lightcone(c, e, cone="tight") for e in g.edges]
+    plan = D.plan_units(cones, be, slice_target=32, mem_cap=1 << 40, n_workers=8)
+    n_pairs = 0
+    for batch in D._batches(list(range(len(plan.units))), plan, be, 125 << 30):
+        prog = E.Program([E.Instance(plan.templates[plan.units[u].cone], plan.units[u].assignment) for u in batch],
+                         "complex64")
+        for nd in prog.nodes:
+            if nd["kind"] == 1 and nd["count"] == 2:
+                n_pairs += 1
+                assert not pair_overlaps(prog, nd)
+    assert n_pairs > 1000
