@@ -7,7 +7,7 @@
 
 Every kernel of this library is matched (K2 small_kernel, K1
 large_kernel_c64/_c128, K3 k3_kernel/k3v2_kernel, K4 k4_kernel_c64/_c128, K5
-k5_kernel_c64/_c128);
+k5_kernel_c64/_c128, K6 k6_kernel_c64/_c128);
 the first <n_nodes> of them are the step (scripts/one_step.py prints the
 program's node count).  Times are ncu's: cold L2, serialised node by node —
 the SHARE of each kernel is what compares with the live bench."""
@@ -15,10 +15,10 @@ import csv
 import re
 import sys
 
-FAMILIES = r"(small_kernel|large_kernel_c64|large_kernel_c128|k3v2_kernel|k3_kernel|k4_kernel_c64|k4_kernel_c128|k5_kernel_c64|k5_kernel_c128)"
+FAMILIES = r"(small_kernel|large_kernel_c64|large_kernel_c128|k3v2_kernel|k3_kernel|k4_kernel_c64|k4_kernel_c128|k5_kernel_c64|k5_kernel_c128|k6_kernel_c64|k6_kernel_c128)"
 FAMILY_OF = {"small_kernel": "K2", "large_kernel_c64": "K1", "large_kernel_c128": "K1", "k3v2_kernel": "K3",
              "k3_kernel": "K3", "k4_kernel_c64": "K4", "k4_kernel_c128": "K4", "k5_kernel_c64": "K5",
-             "k5_kernel_c128": "K5"}
+             "k5_kernel_c128": "K5", "k6_kernel_c64": "K6", "k6_kernel_c128": "K6"}
 
 
 def rows(path):

@@ -40,4 +40,4 @@ if "--dominant" in sys.argv or "--item" in sys.argv:
 else:
     lcp.ex.launch(s)
     torch.cuda.synchronize()
-    print(f"nodes={lcp.prog.n_nodes} zz={complex(*lcp.ex.results[:2].cpu().numpy()).real:.15e}")
+    print(f"nodes={lcp.prog.n_nodes} kernels={sum(lcp.ex.kernel_mix(io=False).values())} zz={complex(*lcp.ex.results[:2].cpu().numpy()).real:.15e}")
