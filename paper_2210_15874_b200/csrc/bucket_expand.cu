@@ -317,13 +317,14 @@ int sm_count() {
 // top nq result bits are set aside — not thread, expansion or tile bits; the
 // fused kernel walks them per thread (B strides bq, F index bits fq) and the
 // plan's output covers the low w - nq bits only.
-int make_plan(const qtn_bucket_desc_t* d, int min_e, Plan* P, int* smem, int nq, int ne_max) {
+int make_plan(const qtn_bucket_desc_t* d, int min_e, Plan* P, int* smem, int nq, int ne_max, int ntb) {
   memset(P, 0, sizeof(*P));
   const int w = d->w, k = d->k, nm = d->n_mem;
   const int wf = w - nq;   // free result bits
   const size_t esz = d->dtype == QTN_C64 ? 8 : 16;
   if (d->dtype != QTN_C64 && d->dtype != QTN_C128) return fail(QTN_E_INVALID, "K4: bad dtype");
-  if (k < 1 || k > MAXKS || nm < 1 || nm > MAXM || wf < TBB || w > 31 || nq < 0 || nq > MAXQ)
+  if (k < 1 || k > MAXKS || nm < 1 || nm > MAXM || wf < ntb || w > 31 || nq < 0 || nq > MAXQ || ntb < 5 ||
+      ntb > TBB)
     return fail(QTN_E_UNSUPPORTED, "K4: w=%d k=%d n_mem=%d nq=%d", w, k, nm, nq);
   // dominant member: most result bits
   int iB = 0, best = -1;
@@ -345,7 +346,7 @@ int make_plan(const qtn_bucket_desc_t* d, int min_e, Plan* P, int* smem, int nq,
       ++ne_all;
       if (ne < ne_max) eb[ne++] = b;
     }
-  if (wf - ne < TBB) return fail(QTN_E_UNSUPPORTED, "K4: dominant member has %d result bits", best);
+  if (wf - ne < ntb) return fail(QTN_E_UNSUPPORTED, "K4: dominant member has %d result bits", best);
   // more than 4 expansion bits (two mid-size members, an outer-product-like
   // expansion): only for wide items — the 45-cone energy's w 22-26 items run
   // 3-5x faster here than in K1, a w = 16 item ran slower (cfg-2: 4 -> 10 us)
@@ -360,12 +361,12 @@ int make_plan(const qtn_bucket_desc_t* d, int min_e, Plan* P, int* smem, int nq,
   {
     const int sec = (int)(32 / esz);
     auto take = [&](int b) { tb[nt++] = b; used[b] = true; };
-    for (int b = 0; b < wf && nt < TBB; ++b)   // B's local axes 0 .. log2(sec)-1
+    for (int b = 0; b < wf && nt < ntb; ++b)   // B's local axes 0 .. log2(sec)-1
       if (B.strides[b] != 0 && B.strides[b] < sec) take(b);
     for (int pass = 0; pass < 2; ++pass)
       for (int b = 0; b < wf && nt < 5; ++b)
         if (B.strides[b] != 0 && !used[b] && (pass == 1 || !carried[b])) take(b);
-    for (int b = 0; b < wf && nt < TBB; ++b)
+    for (int b = 0; b < wf && nt < ntb; ++b)
       if (B.strides[b] != 0 && !used[b]) take(b);
   }
   if (ne_all < min_e) return fail(QTN_E_UNSUPPORTED, "K4: %d expansion bits", ne_all);
@@ -435,7 +436,7 @@ int make_plan(const qtn_bucket_desc_t* d, int min_e, Plan* P, int* smem, int nq,
       if (fbit[b] >= 0) P->fs[i][k + fbit[b]] = (uint32_t)d->mem[i].strides[b];
   }
   for (int q = 0; q < k; ++q) P->bs[q] = B.strides[w + q];
-  for (int i = 0; i < TBB; ++i) {
+  for (int i = 0; i < ntb; ++i) {
     P->btb[i] = B.strides[tb[i]];
     P->otb[i] = 1 << tb[i];
     P->ftb[i] = fbit[tb[i]] >= 0 ? 1 << fbit[tb[i]] : 0;

@@ -36,20 +36,11 @@
 #ifndef K6_PART
 #define K6_PART 0
 #endif
-// B of the next tile copied into thread-private shared-memory slots while
-// the current tile computes (cp.async); 0 = direct loads at each tile start
-// (default: measured neutral to 5 % slower on cfg-2, the G gathers dominate)
-#ifndef K6_BPF
-#define K6_BPF 0
-#endif
-// L1 prefetch of the next result batch's G lines (K6_GPF: cfg-2 w24 pair
-// c128 79.9 -> 75.8 us, c64 57.4 -> 55.3 us) / L2 prefetch of the next
-// tile's B lines (K6_BPF2: neutral, off)
+// L1 prefetch of the next result batch's G lines (cfg-2 w24 pair c128 79.9
+// -> 75.8 us, c64 57.4 -> 55.3 us).  Measured and dropped: cp.async staging
+// of the next tile's B in shared memory, L2 prefetch of it (neutral).
 #ifndef K6_GPF
 #define K6_GPF 1
-#endif
-#ifndef K6_BPF2
-#define K6_BPF2 0
 #endif
 // expansion bits walked per thread (the producer's other B-lacking bits
 // become tile bits: more, smaller tiles balance the persistent grid; 3 and
@@ -63,6 +54,14 @@
 #endif
 #ifndef K6_NEL_C128
 #define K6_NEL_C128 2
+#endif
+// lane-split kernels (two lanes per B coordinate, each with half the q runs)
+// for plans with at least two G runs, per element type: bit 0 complex64,
+// bit 1 complex128.  cfg-2 w24 pair: complex64 55.3 -> 49.8 us (64 registers,
+// 4 blocks/SM), complex128 73.7 -> 77.8 us (80 registers with spills): on
+// for complex64 only
+#ifndef K6_SPLIT
+#define K6_SPLIT 1
 #endif
 
 namespace qtn_k4 {
@@ -80,37 +79,30 @@ struct FPlan {
   const void* uptr[MAXM];
   int32_t uq[MAXM][MAXQ];
   int32_t nqn;                // q loop bits G does not carry (the low ones)
+  int32_t split;              // lanes per B coordinate (1 or 2)
   int32_t item_c;             // consumer item (timing; p.item = producer)
 };
 
 // Kernel selection: K = producer summed bits, NQ = 2^(consumer summed bits),
 // GQ = G runs per result (0: no G member), NEL = expansion bits unrolled per
-// batch (the rest walked by a rolled loop).
-const void* k6_fn_c64(int k, int nq, int gq, int nel);
-const void* k6_fn_c128(int k, int nq, int gq, int nel);
-
-// shared-memory bytes of the B prefetch slots (one per (q, s) value per thread)
-inline int k6_stage_bytes(int dtype, int k, int nq) {
-  return K6_BPF ? NT * (1 << k) * (1 << nq) * (dtype == QTN_C64 ? 8 : 16) : 0;
-}
+// batch (the rest walked by a rolled loop), SPLIT = lanes per B coordinate.
+const void* k6_fn_c64(int k, int nq, int gq, int nel, int split);
+const void* k6_fn_c128(int k, int nq, int gq, int nel, int split);
 
 #if K6_PART > 0
 
-__device__ __forceinline__ void cp_async(void* dst, const float2* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async(void* dst, const double2* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
-               : "memory");
-}
 __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
-__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
-// the value has arrived in registers (orders a later async overwrite of its slot)
-__device__ __forceinline__ void arrived(float2 v) { asm volatile("" ::"f"(v.x), "f"(v.y)); }
-__device__ __forceinline__ void arrived(double2 v) { asm volatile("" ::"d"(v.x), "d"(v.y)); }
 
-template <typename R, int K, int NQ, int GQ, int NEL>
+template <typename T>
+__device__ __forceinline__ T shfl_xor(T v, int m) {
+  return {__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m)};
+}
+
+// SPLIT = 2: lane bit 4 splits the q runs between the two lanes of a pair
+// (each holds half the B file: fewer registers, more resident warps); per
+// result batch the pair exchanges half of its per-lane partial results with
+// one shuffle step, and each lane stores half of the batch.
+template <typename R, int K, int NQ, int GQ, int NEL, int SPLIT>
 __device__ __forceinline__ void k6_body(const FPlan& FP) {
   using T = typename Cx<R>::T;
   const Plan& P = FP.p;
@@ -118,13 +110,14 @@ __device__ __forceinline__ void k6_body(const FPlan& FP) {
   constexpr int NS = 1 << K;
   constexpr int NR = GQ == 0 ? 1 : GQ;   // runs of q
   constexpr int QN = NQ / NR;            // q per run
+  constexpr int NRL = NR / SPLIT;        // runs per lane
+  constexpr int NQL = NRL * QN;          // q per lane
   constexpr int NEVL = 1 << NEL;
+  static_assert(SPLIT == 1 || (SPLIT == 2 && NR >= 2), "a lane split needs two G runs");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* F = reinterpret_cast<T*>(smem_raw);
   const int nfe = 1 << (P.nF + K);
   uint32_t* LUT = reinterpret_cast<uint32_t*>(smem_raw + sizeof(T) * nfe);
-  // B prefetch slots: value v of thread t at [v * NT + t] (conflict-free)
-  [[maybe_unused]] T* bst = reinterpret_cast<T*>(smem_raw + ((sizeof(T) * nfe + P.nm * 128 * 4 + 15) & ~size_t(15)));
   __shared__ int64_t sbase[MAXM + 1];
   __shared__ T sU[NQ];
   // out / F / G offsets of every batch of the rolled expansion bits
@@ -142,11 +135,16 @@ __device__ __forceinline__ void k6_body(const FPlan& FP) {
       }
     LUT[x] = o;
   }
+  // thread bits (SPLIT 2: lane bit 4 is the run half lr, the others index
+  // the plan's 7 thread bits)
+  const int lr = SPLIT == 2 ? (tid >> 4) & 1 : 0;
+  const int tix = SPLIT == 2 ? ((tid & 15) | ((tid >> 5) << 4)) : tid;
+  constexpr int NTB = SPLIT == 2 ? TBB - 1 : TBB;
   int64_t boff = 0;
   int32_t ob = 0, fb = 0, gthr = 0;
 #pragma unroll
-  for (int b = 0; b < TBB; ++b)
-    if ((tid >> b) & 1) {
+  for (int b = 0; b < NTB; ++b)
+    if ((tix >> b) & 1) {
       boff += P.btb[b];
       ob += P.otb[b];
       fb += P.ftb[b];
@@ -168,10 +166,12 @@ __device__ __forceinline__ void k6_body(const FPlan& FP) {
     fe[e] = (fb + f) << K;
     ge[e] = gthr + g;
   }
-  int64_t qoffB[NQ];
-  int32_t fqo[NQ];
+  // this lane's q values: runs r = rl * SPLIT + lr, q = r * QN + qi
+  int64_t qoffB[NQL];
+  int32_t fqo[NQL];
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) {
+  for (int ql = 0; ql < NQL; ++ql) {
+    const int q = ((ql / QN) * SPLIT + lr) * QN + ql % QN;
     int64_t o = 0;
     int32_t f = 0;
 #pragma unroll
@@ -180,17 +180,18 @@ __device__ __forceinline__ void k6_body(const FPlan& FP) {
         o += P.bq[b];
         f += P.fq[b];
       }
-    qoffB[q] = o;
-    fqo[q] = f << K;
+    qoffB[ql] = o;
+    fqo[ql] = f << K;
   }
-  int32_t gro[NR];   // G offset of each run (its q bits are the high loop bits)
+  int32_t gro[NRL];   // G offset of each of this lane's runs (a run's q bits are the high loop bits)
 #pragma unroll
-  for (int r = 0; r < NR; ++r) {
+  for (int rl = 0; rl < NRL; ++rl) {
+    const int r = rl * SPLIT + lr;
     int32_t o = 0;
 #pragma unroll
     for (int b = 0; b < MAXQ; ++b)
       if ((1 << b) < NQ && (((r * QN) >> b) & 1)) o += FP.gq[b];
-    gro[r] = o;
+    gro[rl] = o;
   }
   int64_t soffB[NS];
 #pragma unroll
@@ -237,71 +238,32 @@ __device__ __forceinline__ void k6_body(const FPlan& FP) {
   T* out = reinterpret_cast<T*>(P.out);
   const int shf = P.nH - P.nHF;
   int64_t fkey = -1;
-  auto bbase = [&](int64_t hh) {
-    int64_t o = 0;
-    for (int b = 0; b < P.nH; ++b)
-      if ((hh >> b) & 1) o += P.hs[P.iB][b];
-    return o;
-  };
-#if K6_BPF
-  auto issue_b = [&](int64_t hh) {
-    const T* bp = Bm + bbase(hh) + boff;
-#pragma unroll
-    for (int q = 0; q < NQ; ++q)
-#pragma unroll
-      for (int s = 0; s < NS; ++s) cp_async(bst + (q * NS + s) * NT + tid, bp + qoffB[q] + soffB[s]);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  issue_b(h);
-#endif
   for (; h < h_end; ++h) {
-    int64_t obase = 0, gb = 0;
+    int64_t bb = 0, obase = 0, gb = 0;
     for (int b = 0; b < P.nH; ++b)
       if ((h >> b) & 1) {
+        bb += P.hs[P.iB][b];
         obase += P.hs[nm][b];
         gb += FP.ghs[b];
       }
-    // B for every (q, s), U folded in
-    T bv[NQ][NS];
-#if K6_BPF2
-    if (h + 1 < h_end) {   // the next tile's B lines into L2 while this tile computes
-      const T* bpn = Bm + bbase(h + 1) + boff;
-#pragma unroll
-      for (int q = 0; q < NQ; ++q)
-#pragma unroll
-        for (int s = 0; s < NS; ++s) prefetch_l2(bpn + qoffB[q] + soffB[s]);
-    }
-#endif
+    // B for every (q, s) of this lane: NQL * NS independent loads in flight, U folded in
+    T bv[NQL][NS];
     {
-#if K6_BPF
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-#pragma unroll
-      for (int q = 0; q < NQ; ++q)
-#pragma unroll
-        for (int s = 0; s < NS; ++s) bv[q][s] = bst[(q * NS + s) * NT + tid];
-#pragma unroll
-      for (int q = 0; q < NQ; ++q)
-#pragma unroll
-        for (int s = 0; s < NS; ++s) arrived(bv[q][s]);
-      if (h + 1 < h_end) issue_b(h + 1);   // the next tile's B lands while this one computes
-#else
-      const int64_t bb = bbase(h);
       const T* bp = Bm + bb + boff;
 #pragma unroll
-      for (int q = 0; q < NQ; ++q)
+      for (int ql = 0; ql < NQL; ++ql)
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
-          K4_CHECK(bb + boff + qoffB[q] + soffB[s] >= 0 && bb + boff + qoffB[q] + soffB[s] < P.span[P.iB],
-                   "K6 B element %lld", (long long)(bb + boff + qoffB[q] + soffB[s]));
-          bv[q][s] = __ldg(bp + qoffB[q] + soffB[s]);
+          K4_CHECK(bb + boff + qoffB[ql] + soffB[s] >= 0 && bb + boff + qoffB[ql] + soffB[s] < P.span[P.iB],
+                   "K6 B element %lld", (long long)(bb + boff + qoffB[ql] + soffB[s]));
+          bv[ql][s] = __ldg(bp + qoffB[ql] + soffB[s]);
         }
-#endif
       if (FP.nu) {
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-          const T u = sU[q];
+        for (int ql = 0; ql < NQL; ++ql) {
+          const T u = sU[((ql / QN) * SPLIT + lr) * QN + ql % QN];
 #pragma unroll
-          for (int s = 0; s < NS; ++s) bv[q][s] = cmul(u, bv[q][s]);
+          for (int s = 0; s < NS; ++s) bv[ql][s] = cmul(u, bv[ql][s]);
         }
       }
     }
@@ -337,7 +299,7 @@ __device__ __forceinline__ void k6_body(const FPlan& FP) {
       const int32_t oh = ehv.x, fh = ehv.y, gh = ehv.z;
       // G for the whole batch first (one long-latency round trip per batch);
       // the next batch's lines are prefetched into L1 meanwhile
-      T gv[NEVL][NR];
+      T gv[NEVL][NRL];
 #if K6_GPF
       if constexpr (GQ > 0) {
         if (eh + 1 < (1 << neh)) {
@@ -345,7 +307,7 @@ __device__ __forceinline__ void k6_body(const FPlan& FP) {
 #pragma unroll
           for (int e = 0; e < NEVL; ++e)
 #pragma unroll
-            for (int r = 0; r < NR; ++r) prefetch_l1(gp + ge[e] + ghn + gro[r]);
+            for (int rl = 0; rl < NRL; ++rl) prefetch_l1(gp + ge[e] + ghn + gro[rl]);
         }
       }
 #endif
@@ -353,47 +315,68 @@ __device__ __forceinline__ void k6_body(const FPlan& FP) {
 #pragma unroll
         for (int e = 0; e < NEVL; ++e)
 #pragma unroll
-          for (int r = 0; r < NR; ++r) {
-            K4_CHECK(gb + ge[e] + gh + gro[r] >= 0 && gb + ge[e] + gh + gro[r] < FP.gspan, "K6 G element %lld",
-                     (long long)(gb + ge[e] + gh + gro[r]));
-#ifdef K6_EXP_NOG
-            gv[e][r] = T{R(1) + R(ge[e] + gh + gro[r]) * R(1e-30), R(0)};   // timing experiment only
-#else
-            gv[e][r] = __ldg(gp + ge[e] + gh + gro[r]);
-#endif
+          for (int rl = 0; rl < NRL; ++rl) {
+            K4_CHECK(gb + ge[e] + gh + gro[rl] >= 0 && gb + ge[e] + gh + gro[rl] < FP.gspan, "K6 G element %lld",
+                     (long long)(gb + ge[e] + gh + gro[rl]));
+            gv[e][rl] = __ldg(gp + ge[e] + gh + gro[rl]);
           }
       }
+      // per result: this lane's runs, G applied per run
+      T acc[NEVL];
 #pragma unroll
       for (int e = 0; e < NEVL; ++e) {
         const T* fpe = F + fe[e] + fh;
-        T acc;
 #pragma unroll
-        for (int r = 0; r < NR; ++r) {
+        for (int rl = 0; rl < NRL; ++rl) {
           T xs;
 #pragma unroll
           for (int qi = 0; qi < QN; ++qi) {
-            const int q = r * QN + qi;
-            const T* fp = fpe + fqo[q];
-            K4_CHECK(fe[e] + fh + fqo[q] + NS <= nfe, "K6 F entry %d of %d", fe[e] + fh + fqo[q] + NS, nfe);
+            const int ql = rl * QN + qi;
+            const T* fp = fpe + fqo[ql];
+            K4_CHECK(fe[e] + fh + fqo[ql] + NS <= nfe, "K6 F entry %d of %d", fe[e] + fh + fqo[ql] + NS, nfe);
             if (qi == 0)
-              xs = cmul(bv[q][0], fp[0]);
+              xs = cmul(bv[ql][0], fp[0]);
             else
-              cfma(xs, bv[q][0], fp[0]);
+              cfma(xs, bv[ql][0], fp[0]);
 #pragma unroll
-            for (int s = 1; s < NS; ++s) cfma(xs, bv[q][s], fp[s]);
+            for (int s = 1; s < NS; ++s) cfma(xs, bv[ql][s], fp[s]);
           }
           if constexpr (GQ > 0) {
-            if (r == 0)
-              acc = cmul(gv[e][r], xs);
+            if (rl == 0)
+              acc[e] = cmul(gv[e][rl], xs);
             else
-              cfma(acc, gv[e][r], xs);
+              cfma(acc[e], gv[e][rl], xs);
           } else {
-            acc = xs;
+            acc[e] = xs;
           }
         }
-        K4_CHECK(obase + ob + oh + oe[e] >= 0 && obase + ob + oh + oe[e] < P.out_elems, "K6 result %lld",
-                 (long long)(obase + ob + oh + oe[e]));
-        op[oh + oe[e]] = acc;
+      }
+      if constexpr (SPLIT == 1) {
+#pragma unroll
+        for (int e = 0; e < NEVL; ++e) {
+          K4_CHECK(obase + ob + oh + oe[e] >= 0 && obase + ob + oh + oe[e] < P.out_elems, "K6 result %lld",
+                   (long long)(obase + ob + oh + oe[e]));
+          op[oh + oe[e]] = acc[e];
+        }
+      } else if constexpr (NEVL == 1) {
+        // both lanes hold the same result: the run-0 lane adds its partner's
+        const T o = shfl_xor(acc[0], 16);
+        if (lr == 0) op[oh + oe[0]] = T{acc[0].x + o.x, acc[0].y + o.y};
+      } else {
+        // reduce-scatter over the lane pair: lane lr keeps results
+        // [lr * HALF, lr * HALF + HALF), run-0 partial first
+        constexpr int HALF = NEVL / 2;
+#pragma unroll
+        for (int j = 0; j < HALF; ++j) {
+          const T keep = lr ? acc[HALF + j] : acc[j];
+          const T send = lr ? acc[j] : acc[HALF + j];
+          const T o = shfl_xor(send, 16);
+          const T v = lr ? T{o.x + keep.x, o.y + keep.y} : T{keep.x + o.x, keep.y + o.y};
+          const int32_t oo = lr ? oe[HALF + j] : oe[j];
+          K4_CHECK(obase + ob + oh + oo >= 0 && obase + ob + oh + oo < P.out_elems, "K6 result %lld",
+                   (long long)(obase + ob + oh + oo));
+          op[oh + oo] = v;
+        }
       }
     }
   }
@@ -413,48 +396,70 @@ __device__ __forceinline__ void k6_body(const FPlan& FP) {
 #ifndef K6_MINB_C128
 #define K6_MINB_C128 2
 #endif
+#ifndef K6_MINB_SPLIT_C64
+#define K6_MINB_SPLIT_C64 4
+#endif
+#ifndef K6_MINB_SPLIT_C128
+#define K6_MINB_SPLIT_C128 3
+#endif
 #if K6_PART == 1
 using KR = float;
 #define K6_MINB K6_MINB_C64
+#define K6_MINB_SPLIT K6_MINB_SPLIT_C64
 #define K6_KERNEL k6_kernel_c64
 #define K6_FN k6_fn_c64
 #else
 using KR = double;
 #define K6_MINB K6_MINB_C128
+#define K6_MINB_SPLIT K6_MINB_SPLIT_C128
 #define K6_KERNEL k6_kernel_c128
 #define K6_FN k6_fn_c128
 #endif
 
-template <int K, int NQ, int GQ, int NEL>
-__global__ void __launch_bounds__(NT, K6_MINB) K6_KERNEL(const __grid_constant__ FPlan FP) {
-  k6_body<KR, K, NQ, GQ, NEL>(FP);
+template <int K, int NQ, int GQ, int NEL, int SPLIT>
+__global__ void __launch_bounds__(NT, SPLIT == 2 ? K6_MINB_SPLIT : K6_MINB) K6_KERNEL(const __grid_constant__ FPlan FP) {
+  k6_body<KR, K, NQ, GQ, NEL, SPLIT>(FP);
+}
+
+// kernel selectors: internal linkage — part 1 and part 2 instantiate the same
+// helper names for different kernels, and the linker must not merge them
+namespace {
+
+template <int K, int NQ, int GQ, int SPLIT>
+const void* fn_nel(int nel) {
+  if (nel == 0) return (const void*)K6_KERNEL<K, NQ, GQ, 0, SPLIT>;
+  if (nel == 1) return (const void*)K6_KERNEL<K, NQ, GQ, 1, SPLIT>;
+  return (const void*)K6_KERNEL<K, NQ, GQ, 2, SPLIT>;
 }
 
 template <int K, int NQ, int GQ>
-const void* fn_nel(int nel) {
-  if (nel == 0) return (const void*)K6_KERNEL<K, NQ, GQ, 0>;
-  if (nel == 1) return (const void*)K6_KERNEL<K, NQ, GQ, 1>;
-  return (const void*)K6_KERNEL<K, NQ, GQ, 2>;
+const void* fn_split(int nel, int split) {
+  if constexpr (GQ >= 2) {
+    if (split == 2) return fn_nel<K, NQ, GQ, 2>(nel);
+  }
+  return split == 1 ? fn_nel<K, NQ, GQ, 1>(nel) : nullptr;
 }
 
 template <int K, int NQ>
-const void* fn_gq(int gq, int nel) {
-  if (gq == 0) return fn_nel<K, NQ, 0>(nel);
-  if (gq == 1) return fn_nel<K, NQ, 1>(nel);
-  if (gq == 2 && NQ >= 2) return fn_nel<K, NQ, (NQ >= 2 ? 2 : 1)>(nel);
-  if (gq == 4 && NQ >= 4) return fn_nel<K, NQ, (NQ >= 4 ? 4 : 1)>(nel);
-  if (gq == 8 && NQ >= 8) return fn_nel<K, NQ, (NQ >= 8 ? 8 : 1)>(nel);
+const void* fn_gq(int gq, int nel, int split) {
+  if (gq == 0) return fn_split<K, NQ, 0>(nel, split);
+  if (gq == 1) return fn_split<K, NQ, 1>(nel, split);
+  if (gq == 2 && NQ >= 2) return fn_split<K, NQ, (NQ >= 2 ? 2 : 1)>(nel, split);
+  if (gq == 4 && NQ >= 4) return fn_split<K, NQ, (NQ >= 4 ? 4 : 1)>(nel, split);
+  if (gq == 8 && NQ >= 8) return fn_split<K, NQ, (NQ >= 8 ? 8 : 1)>(nel, split);
   return nullptr;
 }
 
+}  // namespace
+
 // B file: NQ * 2^K values per thread, at most 16
-const void* K6_FN(int k, int nq, int gq, int nel) {
-  if (k == 1 && nq == 2) return fn_gq<1, 2>(gq, nel);
-  if (k == 1 && nq == 4) return fn_gq<1, 4>(gq, nel);
-  if (k == 1 && nq == 8) return fn_gq<1, 8>(gq, nel);
-  if (k == 2 && nq == 2) return fn_gq<2, 2>(gq, nel);
-  if (k == 2 && nq == 4) return fn_gq<2, 4>(gq, nel);
-  if (k == 3 && nq == 2) return fn_gq<3, 2>(gq, nel);
+const void* K6_FN(int k, int nq, int gq, int nel, int split) {
+  if (k == 1 && nq == 2) return fn_gq<1, 2>(gq, nel, split);
+  if (k == 1 && nq == 4) return fn_gq<1, 4>(gq, nel, split);
+  if (k == 1 && nq == 8) return fn_gq<1, 8>(gq, nel, split);
+  if (k == 2 && nq == 2) return fn_gq<2, 2>(gq, nel, split);
+  if (k == 2 && nq == 4) return fn_gq<2, 4>(gq, nel, split);
+  if (k == 3 && nq == 2) return fn_gq<3, 2>(gq, nel, split);
   return nullptr;
 }
 
@@ -479,8 +484,23 @@ int make_fplan(const qtn_bucket_desc_t* dp, const qtn_bucket_desc_t* dc, int ipc
       return fail(QTN_E_UNSUPPORTED, "K6: consumer member %d is not the whole producer result", ipc);
   if ((1 << kc) * (1 << dp->k) > 16)
     return fail(QTN_E_UNSUPPORTED, "K6: %d B registers per thread", (1 << kc) * (1 << dp->k));
-  int rc = make_plan(dp, 0, &F->p, smem, kc, K6_NE_MAX);
+  // lane split (K6_SPLIT, per element type) when G runs exist — decided from
+  // the consumer members before the producer plan (7 thread bits)
+  int ng = 0;
+  bool gcarries_q = false;
+  for (int i = 0; i < nmc; ++i) {
+    if (i == ipc) continue;
+    bool res = false;
+    for (int b = 0; b < wc; ++b) res |= dc->mem[i].strides[b] != 0;
+    if (res) {
+      ++ng;
+      for (int q = 0; q < kc; ++q) gcarries_q |= dc->mem[i].strides[wc + q] != 0;
+    }
+  }
+  const int split = (ng == 1 && gcarries_q && ((K6_SPLIT >> (dp->dtype == QTN_C128 ? 1 : 0)) & 1)) ? 2 : 1;
+  int rc = make_plan(dp, 0, &F->p, smem, kc, K6_NE_MAX, split == 2 ? TBB - 1 : TBB);
   if (rc) return rc;
+  F->split = split;
   Plan& P = F->p;
   if (!dc->out) return fail(QTN_E_INVALID, "K6: null output");
   P.out = dc->out;
@@ -535,7 +555,7 @@ const void* fn_of_plan(const FPlan& F, int dtype) {
   const int gq = F.ng ? (nq >> F.nqn) : 0;
   const int nel_max = dtype == QTN_C64 ? K6_NEL_C64 : K6_NEL_C128;
   const int nel = F.p.nE < nel_max ? F.p.nE : nel_max;
-  return dtype == QTN_C64 ? k6_fn_c64(F.p.k, nq, gq, nel) : k6_fn_c128(F.p.k, nq, gq, nel);
+  return dtype == QTN_C64 ? k6_fn_c64(F.p.k, nq, gq, nel, F.split) : k6_fn_c128(F.p.k, nq, gq, nel, F.split);
 }
 
 }  // namespace qtn_k4
@@ -549,7 +569,6 @@ int qtn_k6_node(const qtn_bucket_desc_t* dp, const qtn_bucket_desc_t* dc, int ip
   FPlan* F = reinterpret_cast<FPlan*>(plan);
   int rc = make_fplan(dp, dc, ipc, F, smem);
   if (rc) return rc;
-  *smem = ((*smem + 15) & ~15) + k6_stage_bytes(dp->dtype, F->p.k, F->p.nq);
   F->p.timing = timing;
   F->p.item = item_p;
   F->item_c = item_c;

@@ -87,8 +87,10 @@ __device__ __forceinline__ void cfma(T& acc, T a, T b) {
 // planner (host): K4 tile plan of descriptor d; nq > 0 sets the top nq result
 // fail(): set the thread's error message, return code.
 // bits aside (K6); at most ne_max B-lacking bits become expansion bits (the
-// others tile bits: smaller tiles, B read once per tile).
-int make_plan(const qtn_bucket_desc_t* d, int min_e, Plan* P, int* smem, int nq = 0, int ne_max = MAXE);
+// others tile bits: smaller tiles, B read once per tile); ntb thread bits
+// (K6 lane-split plans use 7: the 8th thread bit splits the q runs).
+int make_plan(const qtn_bucket_desc_t* d, int min_e, Plan* P, int* smem, int nq = 0, int ne_max = MAXE,
+              int ntb = TBB);
 int fail(int code, const char* fmt, ...);
 int sm_count();
 

@@ -308,23 +308,23 @@ def test_program_items_through_k4(min_e):
         assert n64 > 0 and n128 > 0
 
 
-def test_k6_pairs_with_memory_reuse_repeatable(monkeypatch):
-    """Programs with K6 pairs and liveness reuse forced on every block (cfg-4
-    cones sliced to 32, one batch): NaN-poisoned arena (no uninitialised
-    read), bitwise-identical repeat launches (no race between a pair's reads
-    and its result writes), values equal to the no-reuse program."""
+def test_k6_pairs_with_memory_reuse_repeatable():
+    """Programs with K6 pairs and liveness reuse of the large blocks (cfg-4
+    cones sliced to 26, one batch, 75 pairs): NaN-poisoned arena (no
+    uninitialised read), bitwise-identical repeat launches (no race between a
+    pair's reads and its result writes), values equal to the no-reuse
+    program."""
     from paper_2210_15874_b200 import distributed as D
     from paper_2210_15874_b200 import engine as E
     g = Q.random_regular_graph(200, 3, seed=0)
     c = Q.qaoa_maxcut_circuit(g, Q.QaoaParams.seeded(5, 0))
-    cones = [Q.extract_lightcone(c, e, cone="tight") for e in g.edges[:24]]
-    plan = D.plan_units(cones, C64, slice_target=28, mem_cap=1 << 40, n_workers=4)
+    cones = [Q.extract_lightcone(c, e, cone="tight") for e in g.edges[:12]]
+    plan = D.plan_units(cones, C64, slice_target=26, mem_cap=1 << 40, n_workers=4)
     insts = [E.Instance(plan.templates[u.cone], u.assignment) for u in plan.units]
     raws = [plan.raws[u.cone] for u in plan.units]
     base = E.Executor(E.Program(insts, "complex64", reuse_above=1 << 62)).run(raws)
-    monkeypatch.setattr(E, "REUSE_MIN_ELEMS", 1)
     prog = E.Program(insts, "complex64", reuse_above=0)
-    assert prog.reuse and prog.fused
+    assert prog.reuse and len(prog.fused) > 10
     ex = E.Executor(prog)
     ex.buf.fill_(float("nan"))
     first = np.array(ex.run(raws))

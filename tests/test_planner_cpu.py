@@ -1,6 +1,8 @@
 """Host planner parity (CPU): orders, dry runs and slicing choices equal the
 reference's golden outputs; device programs emulated in numpy equal the
 oracle's values."""
+import os
+
 import numpy as np
 import pytest
 
@@ -542,3 +544,24 @@ def test_cfg4_pairs_never_overwrite_their_inputs():
                 n_pairs += 1
                 assert not pair_overlaps(prog, nd)
     assert n_pairs > 1000
+
+
+@pytest.mark.parametrize("dtype", ["complex64", "complex128"])
+def test_k6_plan_of_cfg2_pair(dtype):
+    """The K6 planner (qtn_bucket_expand_fused_plan, host only) on the cfg-2
+    w = 24 -> w = 22 pair: producer k = 2, the consumer's 2 summed bits set
+    aside, 4 expansion bits, one gathered consumer member, two uniform ones."""
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
+    from k6_survey import pair_plans
+    g, graph, params = _cfg("cfg2")
+    c = Q.qaoa_maxcut_circuit(graph, params)
+    lc = Q.extract_lightcone(c, (0, 15), cone="tight")
+    order = Q.greedy_order(lc.network)
+    t = E.plan_template([x.indices for x in lc.network.tensors], order, dtype, wave_aware=True)
+    plans = {(wp, wc): info for wp, wc, info in pair_plans(E.Program([E.Instance(t)], dtype))}
+    info = plans[(24, 22)]
+    assert not isinstance(info, str), info
+    k, nq, ne, nf, ng, nu, nqn, nh = info
+    assert (k, nq, ne, ng, nu) == (2, 2, 4, 1, 2)
+    assert nf + k <= (12 if dtype == "complex64" else 11)
