@@ -214,6 +214,46 @@ def peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def peak_fp(dtype):
+    """Measured FMA peak of the element type's arithmetic (tools/fp_peak.cu,
+    profiles/r02_fp_peak.json): TFLOP/s and its source."""
+    p = os.path.join(ROOT, "profiles", "r02_fp_peak.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["fp64_fma_tflops" if dtype == "complex128" else "fp32_fma_tflops"]), \
+            "measured (tools/fp_peak.cu, profiles/r02_fp_peak.json)"
+    except Exception:
+        return None, None
+
+
+def node_flops(prog, node):
+    """Algorithmic floating-point work of one graph node: every complex
+    multiply-add 8 flops.  An item: 2^(w+k) (result, assignment) products of
+    its n_mem members (n_mem - 1 complex multiplies + the add).  A K6 pair:
+    the producer's X values (2^(w_P + k_P) multiply-adds with its dominant
+    member) and the consumer's 2^(w_C + k_C) multiply-adds of X by its other
+    members' product."""
+    nd = prog.nodes[node]
+    first, count = int(nd["first"]), int(nd["count"])
+    b = prog.buckets
+    if count == 2:
+        p_, c_ = b[first], b[first + 1]
+        return 8 * ((1 << (int(p_["w"]) + int(p_["k"]))) + (1 << (int(c_["w"]) + int(c_["k"]))))
+    it = b[first]
+    return 8 * (1 << (int(it["w"]) + int(it["k"]))) * max(1, int(it["n_mem"]) - 1)
+
+
+def arith_block(dom, dtype):
+    """The dominant node's arithmetic against the measured FMA peak of its
+    element type (a K6 pair is not HBM-bound: it moves 151 MB but does
+    0.6 GFLOP of complex128 work at cfg-2)."""
+    pk, src = peak_fp(dtype)
+    tf = dom["flops"] / (dom["us"] * 1e-6) / 1e12
+    return {"flops": dom["flops"], "achieved_tflops": tf, "peak_tflops": pk, "frac": (tf / pk) if pk else None,
+            "peak_source": src, "note": "flops = 8 per complex multiply-add (bench.node_flops)"}
+
+
 def ncu_traffic(key):
     """DRAM bytes (read + write) per launch of the dominant kernel from the
     committed `ncu --set full` capture (profiles/traffic.json, keyed by
@@ -425,6 +465,7 @@ def dominant_kernel(lcp, stream, flush, reps=50):
     key = f"{lcp.dtype}:{fam0}:w{int(b['w'])}k{int(b['k'])}"
     return {"item": int(g), "kernel": fam0, "key": key, "w": int(b["w"]), "k": int(b["k"]),
             "items": list(range(int(nd["first"]), int(nd["first"]) + int(nd["count"]))),
+            "flops": node_flops(prog, node_of[g]),
             "bytes": lcp.ex.node_bytes(node_of[g]), "us": dur * 1e6, "top_items_live": items}
 
 
@@ -538,6 +579,7 @@ def run_ours(args):
                       f"result once{'; a K6 pair neither writes nor reads its producer result' if dom['kernel'] == 'K6' else ''}"
                       f" = {dom['bytes']}) / launch duration",
             "dominant_share_of_step": dom["us"] / 1e3 / ms,
+            "arith": arith_block(dom, hd),
             "traffic_source": (traffic or {}).get("source"),
             "step": {"executed_GBps": exe / (ms / 1e3) / 1e9, "frac_executed": exe / (ms / 1e3) / 1e9 / peak,
                      "frac_vs_unfused": alg / (ms / 1e3) / 1e9 / peak,
