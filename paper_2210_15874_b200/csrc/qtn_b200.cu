@@ -179,6 +179,11 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
 // launch as soon as all of its blocks are running, and a successor waits for
 // its predecessors' completion (and memory) only where it first reads their
 // outputs — launch latency and table prologues overlap the predecessor.
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+// K2 stages warm L2 with their item / member records and the input image
+#ifndef K2_WARM
+#define K2_WARM 1
+#endif
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
@@ -270,6 +275,30 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
   int pend_item = 0;
 
   pdl_launch_dependents();
+#if K2_WARM
+  // Warm L2 with what every item of the stage reads first: the stage's item
+  // and member records and the program's input image (cold after an L2
+  // flush or between calls).  L2 is the coherence point, so lines a
+  // predecessor node is still writing stay correct.
+  {
+    const size_t stride = (size_t)gridDim.x * NT * 128;
+    const size_t t0 = ((size_t)blockIdx.x * NT + tid) * 128;
+    const char* b0 = reinterpret_cast<const char*>(P.buckets + first);
+    for (size_t o = t0; o < (size_t)count * sizeof(qtn_bucket_t); o += stride) prefetch_l2(b0 + o);
+    const size_t ib = (size_t)P.n_in_elems * sizeof(T);
+    for (size_t o = t0; o < ib; o += stride) prefetch_l2(reinterpret_cast<const char*>(P.arena) + o);
+    if (HI && P.inputs_hi)
+      for (size_t o = t0; o < (size_t)P.n_in_elems * 16; o += stride)
+        prefetch_l2(reinterpret_cast<const char*>(P.inputs_hi) + o);
+    if (blockIdx.x == 0 && tid < 32) {
+      const int m0 = __ldg(&P.buckets[first].mem_begin);
+      const int m1 = __ldg(&P.buckets[first + count - 1].mem_begin) + 8;
+      const char* mb = reinterpret_cast<const char*>(P.members + m0);
+      for (size_t o = (size_t)tid * 128; o < (size_t)(m1 - m0) * sizeof(qtn_member_t); o += 32 * 128)
+        prefetch_l2(mb + o);
+    }
+  }
+#endif
   // The stage's counters were zeroed by its previous run's last block (or by
   // qtn_program_reset), both stream-ordered before this graph launch, and the
   // program records are uploaded before it: the first ticket, its search and
