@@ -48,20 +48,21 @@
 #ifndef K6_NE_MAX
 #define K6_NE_MAX 8
 #endif
-// expansion bits unrolled per result batch (at most 2)
+// expansion bits unrolled per result batch (at most 2; complex128 1: with the
+// lane split it fits 80 registers without spills, 3 blocks/SM)
 #ifndef K6_NEL_C64
 #define K6_NEL_C64 2
 #endif
 #ifndef K6_NEL_C128
-#define K6_NEL_C128 2
+#define K6_NEL_C128 1
 #endif
 // lane-split kernels (two lanes per B coordinate, each with half the q runs)
 // for plans with at least two G runs, per element type: bit 0 complex64,
 // bit 1 complex128.  cfg-2 w24 pair: complex64 55.3 -> 49.8 us (64 registers,
-// 4 blocks/SM), complex128 73.7 -> 77.8 us (80 registers with spills): on
-// for complex64 only
+// 4 blocks/SM); complex128 73.7 -> 69.6 us with one unrolled expansion bit
+// (80 registers, 3 blocks/SM; with two it spilled: 77.8 us)
 #ifndef K6_SPLIT
-#define K6_SPLIT 1
+#define K6_SPLIT 3
 #endif
 
 namespace qtn_k4 {
