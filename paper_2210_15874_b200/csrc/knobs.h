@@ -23,6 +23,8 @@ struct QtnKnobs {
   int k3_ulim;      // QTN_K3_ULIM   K3 folded-table bits limit
   int k3_inv2;      // QTN_K3_INV2   0: no second invariant operand in K3
   int k6_min_w;     // QTN_K6        narrowest producer fused with its consumer by K6 (0 = K6 off)
+  int k2_jitter;    // QTN_K2_JITTER 0 off | seed: K2 blocks stall a pseudo-random 0-4 us before each tile
+                    //               (schedule perturbation for the race tests, tests/test_k2_schedule.py)
 };
 
 const QtnKnobs& qtn_knobs();

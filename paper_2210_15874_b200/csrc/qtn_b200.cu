@@ -245,7 +245,7 @@ struct SmallCtx {
 
 template <typename R>
 __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_t first, int32_t count,
-                                                   int32_t n_tickets, uint32_t* ctl) {
+                                                   int32_t n_tickets, uint32_t* ctl, uint32_t jitter) {
   using T = typename Cx<R>::T;
   // complex64 programs may carry unrounded inputs (P.inputs_hi), staged in
   // shared memory as complex128 before the item waits for its producers
@@ -378,7 +378,11 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
           if (HI && m.off < n_hi && lg <= 6 && q < (1 << lg)) shi[e] = __ldg(Ahi + m.off + q);
         }
       }
+#ifndef QTN_MUTANT_NO_WAIT   // mutation build (make variant EXTRA=-DQTN_MUTANT_NO_WAIT): proves the race test bites
       for (int d = tid; d < S.b.n_dep; d += NT) {
+#else
+      for (int d = tid; d < 0; d += NT) {
+#endif
         const qtn_dep_t dp = P.deps[S.b.dep_begin + d];
         const uint32_t* c = done + dp.bucket;
         int spins = 0;
@@ -390,6 +394,20 @@ __global__ void __launch_bounds__(NT) small_kernel(const qtn_program_t P, int32_
       prepared = cur;
     }
     const int h = tk - S.b.tick_begin;
+    if (jitter) {
+      // schedule perturbation (QTN_K2_JITTER, race tests): the block stalls a
+      // pseudo-random 0-4 us before computing the tile, so producers finish
+      // in an order unrelated to their tickets; a consumer that read before
+      // its producer's completion would read the test's NaN poison
+      if (tid == 0) {
+        uint32_t x = jitter ^ (uint32_t)globaltimer() ^ ((uint32_t)blockIdx.x * 0x9e3779b9u) ^ ((uint32_t)tk * 0x85ebca6bu);
+        x ^= x >> 15;
+        x *= 0x2c1b3c6du;
+        x ^= x >> 12;
+        __nanosleep(x & 4095u);
+      }
+      __syncthreads();
+    }
     unsigned long long t_start = 0;
     if (P.timing && tid == 0) t_start = globaltimer();
     if (S.b.w < 0) {
@@ -1062,10 +1080,11 @@ struct LaunchSpec {
   const void* fn;
   int grid;
   int smem;
-  void* args[5];
+  void* args[6];
   // storage for the arguments (the graph copies them at node creation)
   qtn_program_t prog;
   int32_t a0, a1, a2;
+  uint32_t a3;
   uint32_t* ctl;
   K1Item k1item;                       // K1 node: its item (kernel parameter)
   std::vector<unsigned char> k3plan;   // K3 node: its Plan (kernel parameter)
@@ -1098,11 +1117,13 @@ int make_launch(const qtn_program_t* p, const qtn_node_t* nd, int ni, const K1It
     L->a1 = nd->count;
     L->a2 = nd->n_tickets;
     L->ctl = p->ctrl + 2 * ni;
+    L->a3 = (uint32_t)qtn_knobs().k2_jitter;
     L->args[0] = &L->prog;
     L->args[1] = &L->a0;
     L->args[2] = &L->a1;
     L->args[3] = &L->a2;
     L->args[4] = &L->ctl;
+    L->args[5] = &L->a3;
   } else if (nd->kind == QTN_NODE_LARGE) {
     L->fn = p->dtype == QTN_C64 ? (const void*)large_fn<float>(nd->variant)
                                 : (const void*)large_fn<double>(nd->variant);
@@ -1171,6 +1192,7 @@ QtnKnobs read_knobs() {
   k.k3_ulim = knob("QTN_K3_ULIM", 5, 0, 8);
   k.k3_inv2 = knob("QTN_K3_INV2", 1, 0, 1);
   k.k6_min_w = knob("QTN_K6", 18, 0, 40);
+  k.k2_jitter = knob("QTN_K2_JITTER", 0, 0, 1 << 30);
   return k;
 }
 
@@ -1238,9 +1260,9 @@ const char* qtn_route_config(void) {
     char buf[512];
     snprintf(buf, sizeof(buf),
              "k3_route=%d k4_min_e=%d k4_all=%d k5=%d pdl=%d k3_tcap=%d k3_stage_kb=%d k3_run=%d k3_v1=%d k3_ulim=%d "
-             "k3_inv2=%d k6_min_w=%d",
+             "k3_inv2=%d k6_min_w=%d k2_jitter=%d",
              k.k3_route, k.k4_min_e, k.k4_all, k.k5, k.pdl, k.k3_tcap, k.k3_stage_kb, k.k3_run, k.k3_v1, k.k3_ulim,
-             k.k3_inv2, k.k6_min_w);
+             k.k3_inv2, k.k6_min_w, k.k2_jitter);
     return std::string(buf);
   }();
   return txt.c_str();
