@@ -1382,6 +1382,7 @@ int qtn_graph_create_host(const qtn_program_t* p, const qtn_bucket_t* items, con
   std::vector<LaunchSpec> specs(n_nodes);
   // optional input upload: every kernel node without a predecessor waits for it
   cudaGraphNode_t h2d = nullptr;
+  bool h2d_kernel = false;   // h2d is the device gather kernel (a PDL edge can follow it)
   if (io && io->n_gather > 0) {
     // device-side gather of the raw inputs (mapped pinned host memory)
     if (!io->gather_raw || !io->gather_src || !io->gather_dst || !p->arena) {
@@ -1406,6 +1407,7 @@ int qtn_graph_create_host(const qtn_program_t* p, const qtn_bucket_t* items, con
     kp.sharedMemBytes = 0;
     kp.kernelParams = args;
     e = cudaGraphAddKernelNode(&h2d, g->graph, nullptr, 0, &kp);   // parameters copied at node creation
+    h2d_kernel = true;
     if (e != cudaSuccess) {
       qtn_graph_destroy(g);
       return cuda_err(e, "cudaGraphAddKernelNode(gather)");
@@ -1485,9 +1487,22 @@ int qtn_graph_create_host(const qtn_program_t* p, const qtn_bucket_t* items, con
     kp.blockDim = dim3(NT);
     kp.sharedMemBytes = spec.smem;
     kp.kernelParams = const_cast<void**>(spec.args);
-    cudaError_t e2 = cudaGraphAddKernelNode(node, g->graph, (h2d && first_node) ? &h2d : nullptr,
-                                            (h2d && first_node) ? 1 : 0, &kp);
+    // a K2 stage after the device gather follows it over a programmatic edge
+    // (its ticket, records and L2 warm-up overlap the gather's PCIe reads; it
+    // reads no input before griddepcontrol.wait); other kernels may read
+    // input members in their prologue, so they wait for the gather's end
+    const bool k2 = spec.fn == (const void*)small_kernel<float> || spec.fn == (const void*)small_kernel<double>;
+    const bool pdl_in = h2d && first_node && h2d_kernel && use_pdl && k2;
+    cudaError_t e2 = cudaGraphAddKernelNode(node, g->graph, (h2d && first_node && !pdl_in) ? &h2d : nullptr,
+                                            (h2d && first_node && !pdl_in) ? 1 : 0, &kp);
     if (e2 != cudaSuccess) return cuda_err(e2, "cudaGraphAddKernelNode");
+    if (pdl_in) {
+      cudaGraphEdgeData ed = {};
+      ed.from_port = cudaGraphKernelNodePortProgrammatic;
+      ed.type = cudaGraphDependencyTypeProgrammatic;
+      e2 = cudaGraphAddDependencies_v2(g->graph, &h2d, node, &ed, 1);
+      if (e2 != cudaSuccess) return cuda_err(e2, "cudaGraphAddDependencies_v2(gather)");
+    }
     // programmatic edges (PDL): the kernels call griddepcontrol.wait before
     // reading predecessor outputs
     for (cudaGraphNode_t from : deps) {
