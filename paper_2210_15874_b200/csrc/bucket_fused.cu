@@ -48,13 +48,13 @@
 #ifndef K6_NE_MAX
 #define K6_NE_MAX 8
 #endif
-// expansion bits unrolled per result batch (at most 2; complex128 1: with the
-// lane split it fits 80 registers without spills, 3 blocks/SM)
+// expansion bits unrolled per result batch (at most 2; complex128 with the
+// lane split: 1 fits 80 registers, 3 blocks/SM; 2 needs 124, 2 blocks/SM)
 #ifndef K6_NEL_C64
 #define K6_NEL_C64 2
 #endif
 #ifndef K6_NEL_C128
-#define K6_NEL_C128 1
+#define K6_NEL_C128 2
 #endif
 // lane-split kernels (two lanes per B coordinate, each with half the q runs)
 // for plans with at least two G runs, per element type: bit 0 complex64,
@@ -400,8 +400,11 @@ __device__ __forceinline__ void k6_body(const FPlan& FP) {
 #ifndef K6_MINB_SPLIT_C64
 #define K6_MINB_SPLIT_C64 4
 #endif
+// complex128 split kernels: 2 blocks/SM with two unrolled expansion bits (124
+// registers, more loads in flight per thread) measured 1 % faster on cfg-2
+// than 3 blocks/SM with one (80 registers)
 #ifndef K6_MINB_SPLIT_C128
-#define K6_MINB_SPLIT_C128 3
+#define K6_MINB_SPLIT_C128 2
 #endif
 #if K6_PART == 1
 using KR = float;
