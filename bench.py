@@ -687,6 +687,7 @@ def rank_shares(plan, be, local, stream, flush, ns=(2, 4, 8), reps=5):
     for n in ns:
         owner = D.lpt_assign(costs, n)
         worst = 0.0
+        per_rank = []
         for r in range(n):
             mine = [u for u in range(len(plan.units)) if owner[u] == r]
             if not mine:
@@ -703,9 +704,12 @@ def rank_shares(plan, be, local, stream, flush, ns=(2, 4, 8), reps=5):
                 b.record(stream)
                 ts.append((a, b))
             torch.cuda.synchronize()
-            worst = max(worst, sum(a.elapsed_time(b) for a, b in ts) / reps)
+            t_r = sum(a.elapsed_time(b) for a, b in ts) / reps
+            per_rank.append({"units": len(mine), "ms": round(t_r, 4),
+                             "cost_share": round(sum(costs[u] for u in mine) / max(sum(costs), 1e-30), 4)})
+            worst = max(worst, t_r)
             del prep
-        out[str(n)] = {"makespan_ms": round(worst, 4)}
+        out[str(n)] = {"makespan_ms": round(worst, 4), "ranks": per_rank}
     return out
 
 
